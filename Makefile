@@ -1,0 +1,37 @@
+# Builds the product library (CUDA for sm_100a + C ABI + C++ drop-in) in-tree,
+# and the CPU checkers under oracle/ (test infrastructure).
+NVCC     ?= nvcc
+PKG      := paper_1710_10989_b200
+LIB      := $(PKG)/_lib/libmexp_b200.so
+CU_SRCS  := $(wildcard $(PKG)/csrc/*.cu)
+CXX_SRCS := $(wildcard $(PKG)/csrc/*.cpp)
+HDRS     := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard include/*.h) $(wildcard include/mexp/*.hpp)
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v \
+            --expt-relaxed-constexpr
+OBJDIR   := build/obj
+
+OBJS := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(CU_SRCS)) \
+        $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.cpp.o,$(CXX_SRCS))
+
+all: $(LIB) oracle
+
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; false)
+
+$(OBJDIR)/%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	g++ -O2 -std=c++20 -fPIC -Iinclude -I/usr/local/cuda/include -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(PKG)/_lib
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(OBJS) -lcudart_static -lrt -ldl -lpthread
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(PKG)/_lib
+
+.PHONY: all oracle clean

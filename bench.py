@@ -1,0 +1,408 @@
+"""Benchmark: batched scaling-and-squaring expm (arXiv 1710.10989 TaylorNew) on B200.
+
+Default workload = BASELINE.json configs[1] (cfg2): 262,144 fp64 8x8 matrices,
+U(-1,1) rescaled to a log-uniform 1-norm in [1e-4, 1e2]. A step is one
+batched expm over the rank's 262,144 matrices, inputs resident in HBM. With N
+GPUs every rank runs its own 262,144 matrices (global indices
+[rank*B, (rank+1)*B)), no collective on the data path -> "scaling": "weak";
+an NCCL gather of the results to rank 0 is timed separately ("gather").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfgX]
+                    [--impl ours|reference] [--rounding auto|reference|fast]
+
+Prints ONE JSON line on rank 0. `value` = expm/s over all ranks (device time,
+CUDA events, max over ranks); `e2e` = the same metric through the host C-ABI
+call (mexp_expm_batched_host: pinned H2D + kernels + D2H inside the timed
+region). --impl reference times the reference's own CPU implementation
+(oracle/_ref, the unmodified mexp library) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1710_10989_b200 import workloads  # noqa: E402
+
+METRIC = "matrix exponentials/sec and effective TFLOP/s (fraction of HBM/FP64 roofline)"
+UNIT = "expm/s"
+L2_BYTES = 126 * 2 ** 20
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def fp64_peak_tflops():
+    """FP64 peak: measured on the box by profiles/fp64_peak.json if present."""
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("dmma_tflops"), "measured"
+    return 37.2, "datasheet-class (148 SM x 64 FMA/clk x 2 x 1.965 GHz)"
+
+
+def flops_per_matrix(n, degree, s):
+    prods = np.vectorize({1: 0, 2: 1, 4: 2, 8: 3, 12: 4, 18: 5}.get)(degree)
+    return 2.0 * n ** 3 * (prods + s)
+
+
+class ClockSampler:
+    """NVML clock/throttle sampling during the timed region (1-2 ms period)."""
+
+    def __init__(self, device_index=0):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.001)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU arms --
+def _ref_worker(args):
+    key, b0, count, chunk = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle.oracle import Reference
+    ref = Reference()
+    a = workloads.generate(key, b0, count)
+    cfg = workloads.CONFIGS[key]
+    t0 = time.perf_counter()
+    done = 0
+    for c in range(0, count, chunk):
+        ref.expm_batch(a[c:c + chunk], accuracy=cfg.accuracy)
+        done += min(chunk, count - c)
+    return done, time.perf_counter() - t0
+
+
+def cpu_reference_rate(key, matrices_per_worker, workers, pool=None):
+    """Aggregate expm/s of the compiled reference over `workers` processes."""
+    cfg = workloads.CONFIGS[key]
+    tasks = [(key, (w * matrices_per_worker) % max(cfg.batch - matrices_per_worker, 1),
+              matrices_per_worker, 256) for w in range(workers)]
+    own = pool is None
+    if own:
+        pool = mp.get_context("spawn").Pool(workers)
+    try:
+        t0 = time.perf_counter()
+        res = pool.map(_ref_worker, tasks)
+        wall = time.perf_counter() - t0
+    finally:
+        if own:
+            pool.close()
+            pool.join()
+    done = sum(r[0] for r in res)
+    busy = max(r[1] for r in res)
+    return done / busy, done, wall
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def per_worker_sample(key):
+    # ~2-4 s of single-core work per worker (survey probe: cfg2 ~130k/s/core,
+    # cfg3 ~9k/s, cfg1 ~1.1k/s); keeps the whole CPU leg well under a minute
+    return {"cfg1": 256, "cfg2": 32768, "cfg3": 2048, "cfg4": 1, "cfg5": 1}[key]
+
+
+# ---------------------------------------------------------------- main ----
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--config", default="cfg2", choices=sorted(workloads.CONFIGS))
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--rounding", default="auto", choices=["auto", "reference", "fast"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=10)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = workloads.CONFIGS[args.config]
+    cores = host_cores()
+    per = per_worker_sample(args.config)
+    pool = mp.get_context("spawn").Pool(cores)
+    try:
+        for _ in range(max(args.warmup, 1)):
+            cpu_reference_rate(args.config, max(per // 8, 1), cores, pool)
+        rates = []
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r, done, wall = cpu_reference_rate(args.config, max(per // 8, 1), cores, pool)
+            rates.append(r)
+            if time.perf_counter() - t0 > 120:  # bound the arm to ~2 minutes
+                break
+    finally:
+        pool.close()
+        pool.join()
+    value = statistics.median(rates)
+    sample = (f"{cores} worker processes x {max(per // 8, 1)} {cfg.n}x{cfg.n} matrices of "
+              f"{args.config} per step, OMP_NUM_THREADS=1, rate = matrices / slowest worker's compute time")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": len(rates), "warmup": args.warmup,
+        "ms_per_step": 1e3 * (max(per // 8, 1) * cores) / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": cfg.dtype, "data": "synthetic (seeded, counter-based; see workloads.py)",
+        "config": {"workload": args.config, "description": cfg.description, "n": cfg.n,
+                   "batch": cfg.batch, "parallelism": "host processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1710_10989_b200 as mx
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workloads.CONFIGS[args.config]
+    n = cfg.n
+    B = cfg.batch
+    b0 = rank * B  # weak scaling: each rank owns a full config-sized batch
+    a_host = workloads.generate(args.config, 0, B) if world == 1 else None
+    if a_host is None:
+        # global indices beyond the config batch come from the same generator
+        a_host = _generate_shard(args.config, b0, B)
+    torch_dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
+    rounding = {"auto": mx.ROUND_AUTO, "reference": mx.ROUND_REFERENCE,
+                "fast": mx.ROUND_FAST}[args.rounding]
+    esz = 8 if cfg.dtype == "f64" else 4
+    mat_bytes = n * n * esz
+    # two input/output buffer pairs alternate so the working set exceeds L2
+    pairs = 2 if 2 * B * mat_bytes < 4 * L2_BYTES else 1
+    ins = [torch.from_numpy(a_host).to(dev) for _ in range(pairs)]
+    outs = [torch.empty_like(ins[0]) for _ in range(pairs)]
+    sel = torch.empty(B * 16, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        mx.expm_batched(ins[i % pairs], outs[i % pairs], sel, accuracy=mx.Accuracy(cfg.accuracy),
+                        rounding=rounding, stream=stream)
+
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+    sels = sel.cpu().numpy().view(mx.SELECTION_DTYPE)
+    flops = float(flops_per_matrix(n, sels["degree"], sels["s"]).sum())
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = mx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = mx.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    value = world * B / (ms_step * 1e-3)
+
+    # ---- e2e through the host C-ABI call (pinned buffers) ----
+    h_in = torch.from_numpy(a_host).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    for _ in range(2):
+        mx.expm_batched_host(h_in, h_out, accuracy=mx.Accuracy(cfg.accuracy), rounding=rounding)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        mx.expm_batched_host(h_in, h_out, accuracy=mx.Accuracy(cfg.accuracy), rounding=rounding)
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * B / e2e_s
+
+    # ---- gather of the results to rank 0 (NCCL), timed separately ----
+    gather = None
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0 = time.perf_counter()
+        if rank == 0:
+            bufs = [torch.empty_like(outs[0]) for _ in range(world)]
+            dist.gather(outs[0], bufs, dst=0)
+        else:
+            dist.gather(outs[0], None, dst=0)
+        torch.cuda.synchronize()
+        gather = {"ms": 1e3 * (time.perf_counter() - g0),
+                  "bytes_to_root": (world - 1) * B * mat_bytes, "how": "torch.distributed.gather (NCCL)"}
+
+    if rank == 0:
+        peaks = load_peaks()
+        alg_bytes = 2.0 * B * mat_bytes  # one read of A, one write of e^A per matrix
+        hbm_gbs = alg_bytes / (ms_step * 1e-3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(f"{args.config}_{args.rounding}")
+        peak64, peak64_src = fp64_peak_tflops()
+        tflops = flops / (ms_step * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": cfg.dtype, "data": "synthetic (seeded, counter-based; see workloads.py)",
+            "config": {"workload": args.config, "description": cfg.description, "n": n,
+                       "batch_per_rank": B, "global_batch": world * B, "rounding": args.rounding,
+                       "parallelism": f"matrix-sharded x{world}",
+                       "l2": f"inputs larger than L2 ({pairs} x {2 * B * mat_bytes / 2**20:.0f} MiB "
+                             f"in+out, alternating buffers)"},
+            "effective_tflops": tflops,
+            "fp64_peak": {"tflops": peak64, "source": peak64_src,
+                          "frac": (tflops / peak64) if peak64 else None},
+            "roofline": {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": hbm_gbs / peaks["hbm_gbs"], "traffic": traffic,
+                         "peak_source": peaks["source"],
+                         "kernel": "expm_small_f64_kernel<8,8> (1 launch per step)"},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": B * mat_bytes,
+                    "d2h_bytes_per_step": B * mat_bytes + 16 * B,
+                    "how": "mexp_expm_batched_host, pinned host buffers, wall clock"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if gather:
+            line["gather"] = gather
+        if not args.no_cpu_baseline and world == 1:
+            cores = host_cores()
+            per = per_worker_sample(args.config)
+            rate, done, wall = cpu_reference_rate(args.config, per, cores)
+            line["cpu_baseline"] = {
+                "value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"{done} matrices of {args.config} ({per} per worker process, "
+                          f"OMP_NUM_THREADS=1), oracle/_ref = unmodified mexp library",
+                "cpu": cpu_model()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _generate_shard(key, b0, count):
+    """Rows [b0, b0+count) of the counter-based stream; beyond the config batch
+    the same generator continues (weak scaling: rank r owns its own batch)."""
+    cfg = workloads.CONFIGS[key]
+    if b0 + count <= cfg.batch:
+        return workloads.generate(key, b0, count)
+    # the generators index matrices by a 32-bit-shifted counter, so any b0 works
+    old = workloads.CONFIGS[key]
+    workloads.CONFIGS[key] = workloads.Config(old.key, old.n, b0 + count, old.dtype,
+                                              old.accuracy, old.description)
+    try:
+        return workloads.generate(key, b0, count)
+    finally:
+        workloads.CONFIGS[key] = old
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/*
+ * mexp_b200 — C ABI of the B200 (sm_100a) scaling-and-squaring matrix
+ * exponential built on the reduced-product Taylor schemes of arXiv 1710.10989
+ * (Family::TaylorNew of the reference `mexp` library).
+ *
+ * The reference has no FFI layer: its operator boundary is the C++ API in
+ * namespace mexp (proj/include/mexp/expm.hpp, theta_tables.hpp). Each entry
+ * point below is the plain-pointer form of the reference call it replaces
+ * (cited per function); the C++ drop-in (include/mexp/expm.hpp in this repo)
+ * sits on top of these, and so would a ctypes / cgo / JNI binding.
+ *
+ * Conventions
+ *   - matrices are square, row-major, contiguous; a batch is `batch`
+ *     consecutive n*n blocks;
+ *   - no exceptions cross this ABI: every call returns an mexp_status;
+ *   - there is NO CPU fallback: with no usable CUDA device every compute
+ *     call returns MEXP_ERR_NO_DEVICE;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ */
+#ifndef MEXP_B200_H
+#define MEXP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MEXP_B200_ABI_VERSION 1
+
+/* Status codes. The C++ drop-in maps 1-3 to std::invalid_argument with the
+ * reference's messages (expm.cpp:13, expm.cpp:38, taylor_schemes.cpp:225). */
+typedef enum {
+    MEXP_OK = 0,
+    MEXP_ERR_NONFINITE = 1,       /* "non-finite matrix entry"           expm.cpp:38 */
+    MEXP_ERR_NORM_NONFINITE = 2,  /* "norm must be finite and nonnegative" expm.cpp:13 */
+    MEXP_ERR_INVALID_ARGUMENT = 3,/* bad n / batch / enum value, dimension errors */
+    MEXP_ERR_UNSUPPORTED = 4,     /* family other than TaylorNew, dtype/n combination */
+    MEXP_ERR_CUDA = 5,            /* CUDA runtime error (see mexp_last_cuda_error) */
+    MEXP_ERR_NO_DEVICE = 6        /* no CUDA device: there is no CPU fallback */
+} mexp_status;
+
+/* theta_tables.hpp:8 (enum class Family). Only TaylorNew is implemented. */
+typedef enum { MEXP_FAMILY_TAYLOR_NEW = 0, MEXP_FAMILY_TAYLOR_PS = 1, MEXP_FAMILY_PADE = 2 } mexp_family;
+
+/* theta_tables.hpp:9 (enum class Accuracy): selects the theta table, i.e. the
+ * backward-error target u = 2^-24 (Single) or 2^-53 (Double). */
+typedef enum { MEXP_ACCURACY_SINGLE = 0, MEXP_ACCURACY_DOUBLE = 1 } mexp_accuracy;
+
+/* Storage/arithmetic type of a batched call. F64 is the reference's type;
+ * F32 evaluates in fp32 with FFMA (never TF32), norm and (m,s) in fp64. */
+typedef enum { MEXP_F64 = 0, MEXP_F32 = 1 } mexp_dtype;
+
+/* Rounding policy of the fp64 small-N path (n <= 64):
+ *   REFERENCE: products and linear combinations with separately rounded
+ *              multiplies and adds in the reference's accumulation order
+ *              (kernels.cpp:16-37, -ffp-contract=off) -> e^A bit-identical
+ *              to the reference;
+ *   FAST:      FP64 tensor-core DMMA products, FMA combinations;
+ *   AUTO:      FAST, except matrices with s >= 6 squarings, whose rounding
+ *              differences the squarings amplify, run REFERENCE.
+ * The large-n path (n > 64) is always tensor-core DMMA. F32 ignores it. */
+typedef enum { MEXP_ROUND_AUTO = 0, MEXP_ROUND_REFERENCE = 1, MEXP_ROUND_FAST = 2 } mexp_rounding;
+
+/* Per-matrix selection record written by the batched calls (16 bytes).
+ * norm_in == ExpmReport::norm_in (expm.hpp:31), degree/s == Selection
+ * (expm.hpp:10-13); cost_thirds = 3 * (products(degree) + s) (expm.cpp:71). */
+typedef struct {
+    double norm_in;
+    int16_t degree;
+    int16_t s;
+    int32_t status; /* mexp_status of this matrix */
+} mexp_selection;
+
+/* ExpmReport (expm.hpp:23-32) minus the result matrix. */
+typedef struct {
+    int32_t family;
+    int32_t degree;
+    int32_t s;
+    int32_t reserved;
+    int64_t cost_thirds;
+    double norm_in;
+} mexp_report;
+
+/* ---- selection logic (host, pure table arithmetic) ------------------- */
+
+/* mexp::select (expm.hpp:18, expm.cpp:11-29). */
+int mexp_select(double norm, int accuracy, int family, int32_t* degree, int32_t* s);
+
+/* mexp::selection_table (theta_tables.hpp:32, theta_tables.cpp:77-85):
+ * writes up to `cap` entries (degree, products, theta); returns the count or
+ * a negative mexp_status. */
+int mexp_selection_table(int accuracy, int family, int32_t* degrees, int32_t* products,
+                         double* thetas, int cap);
+
+/* mexp::unit_roundoff (theta_tables.hpp:11). */
+double mexp_unit_roundoff(int accuracy);
+
+/* ---- the hot path ----------------------------------------------------- */
+
+/* mexp::expm (expm.hpp:37, expm.cpp:37-74) on ONE host matrix, synchronous.
+ * `result` receives e^A (n*n doubles); `report` may be NULL. Runs on the
+ * current device with the default rounding policy. */
+int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
+              mexp_report* report);
+
+/* Batched expm on DEVICE buffers, asynchronous on `stream`. d_a and d_out
+ * hold `batch` n x n matrices of `dtype`; d_sel (may be NULL) receives one
+ * mexp_selection per matrix. Per-matrix errors (non-finite input, overflowing
+ * norm) are reported in d_sel[i].status with d_out[i] filled with NaN; the
+ * call itself returns MEXP_OK once the work is enqueued. d_a and d_out must
+ * not overlap. n may be any value >= 1. */
+int mexp_expm_batched(const void* d_a, void* d_out, int dtype, int n, int64_t batch,
+                      int accuracy, int family, int rounding, mexp_selection* d_sel,
+                      void* stream);
+
+/* Batched expm on HOST buffers, synchronous: chunked host->device copies,
+ * kernels and device->host copies overlapped on internal streams (pinned
+ * host buffers give full PCIe rate). h_sel may be NULL. Returns the first
+ * per-matrix error status (and its index in *first_error, if non-NULL) or
+ * MEXP_OK. This is the reference-facing end-to-end call. */
+int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64_t batch,
+                           int accuracy, int family, int rounding, mexp_selection* h_sel,
+                           int64_t* first_error);
+
+/* mexp::squarings (expm.hpp:21, expm.cpp:31-35) on device: X <- X^(2^s) for
+ * each of `batch` fp64 matrices, in place, s squarings each. */
+int mexp_squarings_batched(double* d_x, int n, int64_t batch, int s, int rounding,
+                           void* stream);
+
+/* ---- runtime ---------------------------------------------------------- */
+
+const char* mexp_status_string(int status);
+/* Last CUDA error string recorded by a call that returned MEXP_ERR_CUDA. */
+const char* mexp_last_cuda_error(void);
+/* Number of kernels this library has launched in this process. */
+uint64_t mexp_launch_count(void);
+/* ABI version (MEXP_B200_ABI_VERSION) and device check: returns MEXP_OK if a
+ * CUDA device of compute capability 10.x is usable. */
+int mexp_abi_version(void);
+int mexp_device_check(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MEXP_B200_H */

@@ -1,0 +1,333 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — the CPU oracle. Never linked into the product.
+ *
+ * Plain-C restatement of the reference's scaling-and-squaring expm for
+ * Family::TaylorNew (arXiv 1710.10989, reduced-product Taylor schemes), in the
+ * exact arithmetic order of the reference so results are bit-identical to it
+ * when compiled with -ffp-contract=off (the reference's own flag,
+ * proj/CMakeLists.txt:10-11). Pinned against the compiled reference
+ * (oracle/_ref/libmexp_ref.so) and the committed fixtures in tests/golden/.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load this file's library, and only as the checker / CPU baseline.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { ORC_OK = 0, ORC_NONFINITE = 1, ORC_NORM_NONFINITE = 2, ORC_INVALID = 3 };
+
+/* ---- theta tables: proj/src/theta_tables.cpp:45-51 (TaylorNew rows) ---- */
+static const int kDegrees[6] = {1, 2, 4, 8, 12, 18};
+static const int kProducts[6] = {0, 1, 2, 3, 4, 5};
+static const double kThetaDouble[6] = {2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09};
+static const double kThetaSingle[6] = {1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01};
+
+/* ---- scheme coefficients: proj/src/taylor_schemes.cpp:12-27,44-48,62-85 ---- */
+typedef struct { double x1, x2, x3, x4, x5, x6, x7, y0, y1, y2; } t8c;
+
+/* make_t8: closed forms in sqrt(177), x3 = 2/3, long double rounded once
+ * (taylor_schemes.cpp:12-27). */
+static t8c make_t8(void) {
+    const long double r = sqrtl(177.0L);
+    const long double x3 = 2.0L / 3.0L;
+    t8c c;
+    c.x1 = (double)(x3 * (1.0L + r) / 88.0L);
+    c.x2 = (double)(x3 * (1.0L + r) / 352.0L);
+    c.x3 = (double)x3;
+    c.x4 = (double)((-271.0L + 29.0L * r) / (315.0L * x3));
+    c.x5 = (double)(11.0L * (-1.0L + r) / (1260.0L * x3));
+    c.x6 = (double)(11.0L * (-9.0L + r) / (5040.0L * x3));
+    c.x7 = (double)((89.0L - r) / (5040.0L * x3 * x3));
+    c.y0 = 1.0;
+    c.y1 = 1.0;
+    c.y2 = (double)((857.0L - 58.0L * r) / 630.0L);
+    return c;
+}
+
+/* Printed coefficients of the 4- and 5-product schemes (paper eqs. for T12 and
+ * T18; reference taylor_schemes.cpp:62-85). kT12[i][j] multiplies A^i in B_{j+1}. */
+static const double kT12[4][4] = {
+    {9.0198e-16, 5.31597895759871264183, 0.18188869982170434744, -2.0861320e-13},
+    {0.46932117595418237389, 1.19926790417132231573, 0.05502798439925399070,
+     -0.13181061013830184015},
+    {-0.20099424927047284052, 0.01179296240992997031, 0.09351590770535414968,
+     -0.02027855540589259079},
+    {-0.04623946134063071740, 0.01108844528519167989, 0.00610700528898058230,
+     -0.00675951846863086359},
+};
+static const double kT18A[4] = {0.0, -0.100365581030144620, -0.0080292464824115696,
+                                -0.0008921384980457299};
+static const double kT18B[4][5] = {
+    {0.0, 0.39784974949964507614, 1.36783778460411719922, 0.49828962252538267755,
+     -0.0006378981945947233},
+    {-10.967639605296206259, 1.68015813878906197182, 0.05717798464788655127,
+     -0.0069821012248805208, 0.00003349750170860705},
+    {-0.0904316832390810561, -0.0676404519071381907, 0.06759613017704596460,
+     0.02955525704293155274, -0.0000139180257516060},
+    {0.0, 0.0, -0.0923364619367118592, -0.0169364939002081717, -0.0000140086798182036},
+};
+
+/* inv_factorial: 1.0 / k! with k! accumulated in double (taylor_schemes.cpp:44-48). */
+static double inv_factorial(int i) {
+    double f = 1.0;
+    for (int k = 2; k <= i; ++k) f *= k;
+    return 1.0 / f;
+}
+
+/* ---- raw kernels: proj/src/kernels.cpp ---- */
+
+/* one_norm: column j summed rows ascending from 0.0, strict '>' max
+ * (kernels.cpp:44-53). */
+double oracle_one_norm(const double* a, int n) {
+    double best = 0.0;
+    for (int j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += fabs(a[(size_t)i * n + j]);
+        if (s > best) best = s;
+    }
+    return best;
+}
+
+/* matmul: memset then i-k-j accumulation, c_ij += a_ik * b_kj, no FMA
+ * (kernels.cpp:16-27). */
+void oracle_matmul(const double* a, const double* b, double* c, int n) {
+    memset(c, 0, sizeof(double) * (size_t)n * n);
+    for (int i = 0; i < n; ++i) {
+        double* ci = c + (size_t)i * n;
+        for (int k = 0; k < n; ++k) {
+            const double aik = a[(size_t)i * n + k];
+            const double* bk = b + (size_t)k * n;
+            for (int j = 0; j < n; ++j) ci[j] += aik * bk[j];
+        }
+    }
+}
+
+/* lincomb: out = c0*m0, then += ci*mi left to right (kernels.cpp:29-37). */
+static void lincomb(const double* coeffs, const double* const* mats, int k, double* out,
+                    size_t len) {
+    for (size_t e = 0; e < len; ++e) {
+        double s = coeffs[0] * mats[0][e];
+        for (int i = 1; i < k; ++i) s += coeffs[i] * mats[i][e];
+        out[e] = s;
+    }
+}
+
+/* add(a, b) = lincomb({1, 1}, {a, b}) (dense_matrix.cpp:94-96). */
+static void add(const double* a, const double* b, double* out, size_t len) {
+    const double c[2] = {1.0, 1.0};
+    const double* m[2] = {a, b};
+    lincomb(c, m, 2, out, len);
+}
+
+/* ---- selection: proj/src/expm.cpp:11-29 ---- */
+int oracle_select(double norm, int accuracy, int32_t* degree, int32_t* s) {
+    const double* th = accuracy == 0 ? kThetaSingle : kThetaDouble;
+    if (!isfinite(norm) || norm < 0) return ORC_NORM_NONFINITE;
+    if (norm <= th[5]) {
+        int best = -1;
+        for (int e = 0; e < 6; ++e) {
+            if (th[e] < norm) continue; /* expm.cpp:17 */
+            if (best < 0 || kProducts[e] < kProducts[best] ||
+                (kProducts[e] == kProducts[best] && kDegrees[e] < kDegrees[best]))
+                best = e;
+        }
+        *degree = kDegrees[best];
+        *s = 0;
+        return ORC_OK;
+    }
+    int k = 0;
+    while (ldexp(norm, -k) > th[5]) ++k; /* expm.cpp:27 */
+    *degree = 18;
+    *s = k;
+    return ORC_OK;
+}
+
+int oracle_products(int degree) {
+    for (int e = 0; e < 6; ++e)
+        if (kDegrees[e] == degree) return kProducts[e];
+    return -1;
+}
+
+/* ---- schemes: proj/src/taylor_schemes.cpp ---- */
+
+/* Scratch layout: the caller passes ws with room for 12 n*n matrices. */
+static void eval_t8(const double* a, int n, double* out, double* ws) {
+    static int init = 0;
+    static t8c c;
+    if (!init) { c = make_t8(); init = 1; }
+    const size_t nn = (size_t)n * n;
+    double* id = ws; double* a2 = ws + nn; double* a4 = ws + 2 * nn;
+    double* t1 = ws + 3 * nn; double* t2 = ws + 4 * nn; double* a8 = ws + 5 * nn;
+    memset(id, 0, sizeof(double) * nn);
+    for (int i = 0; i < n; ++i) id[(size_t)i * n + i] = 1.0;
+    oracle_matmul(a, a, a2, n);
+    { const double k[2] = {c.x1, c.x2}; const double* m[2] = {a, a2}; lincomb(k, m, 2, t1, nn); }
+    oracle_matmul(a2, t1, a4, n);
+    { const double k[2] = {c.x3, 1.0}; const double* m[2] = {a2, a4}; lincomb(k, m, 2, t1, nn); }
+    { const double k[4] = {c.x4, c.x5, c.x6, c.x7}; const double* m[4] = {id, a, a2, a4};
+      lincomb(k, m, 4, t2, nn); }
+    oracle_matmul(t1, t2, a8, n);
+    { const double k[4] = {c.y0, c.y1, c.y2, 1.0}; const double* m[4] = {id, a, a2, a8};
+      lincomb(k, m, 4, out, nn); } /* taylor_schemes.cpp:104-113 */
+}
+
+static void eval_t12(const double* a, int n, double* out, double* ws) {
+    const size_t nn = (size_t)n * n;
+    double* id = ws; double* a2 = ws + nn; double* a3 = ws + 2 * nn;
+    double* b[4] = {ws + 3 * nn, ws + 4 * nn, ws + 5 * nn, ws + 6 * nn};
+    double* p = ws + 7 * nn; double* a6 = ws + 8 * nn; double* t = ws + 9 * nn;
+    memset(id, 0, sizeof(double) * nn);
+    for (int i = 0; i < n; ++i) id[(size_t)i * n + i] = 1.0;
+    oracle_matmul(a, a, a2, n);
+    oracle_matmul(a2, a, a3, n);
+    for (int j = 0; j < 4; ++j) {
+        const double k[4] = {kT12[0][j], kT12[1][j], kT12[2][j], kT12[3][j]};
+        const double* m[4] = {id, a, a2, a3};
+        lincomb(k, m, 4, b[j], nn);
+    }
+    oracle_matmul(b[3], b[3], p, n);
+    add(b[2], p, a6, nn);
+    add(b[1], a6, t, nn);
+    oracle_matmul(t, a6, p, n);
+    add(b[0], p, out, nn); /* taylor_schemes.cpp:115-125 */
+}
+
+static void eval_t18(const double* a, int n, double* out, double* ws) {
+    const size_t nn = (size_t)n * n;
+    double* id = ws; double* a2 = ws + nn; double* a3 = ws + 2 * nn; double* a6 = ws + 3 * nn;
+    double* b1 = ws + 4 * nn;
+    double* b[4] = {ws + 5 * nn, ws + 6 * nn, ws + 7 * nn, ws + 8 * nn};
+    double* p = ws + 9 * nn; double* a9 = ws + 10 * nn; double* t = ws + 11 * nn;
+    memset(id, 0, sizeof(double) * nn);
+    for (int i = 0; i < n; ++i) id[(size_t)i * n + i] = 1.0;
+    oracle_matmul(a, a, a2, n);
+    oracle_matmul(a2, a, a3, n);
+    oracle_matmul(a3, a3, a6, n);
+    { const double* m[4] = {id, a, a2, a3}; lincomb(kT18A, m, 4, b1, nn); }
+    for (int j = 0; j < 4; ++j) {
+        const double* m[5] = {id, a, a2, a3, a6};
+        lincomb(kT18B[j], m, 5, b[j], nn);
+    }
+    oracle_matmul(b1, b[3], p, n);
+    add(p, b[2], a9, nn);
+    add(b[1], a9, t, nn);
+    oracle_matmul(t, a9, p, n);
+    add(b[0], p, out, nn); /* taylor_schemes.cpp:127-141 */
+}
+
+/* eval_ps degrees 2 and 4 (taylor_schemes.cpp:146-157). */
+static void eval_ps(const double* a, int n, int degree, double* out, double* ws) {
+    const size_t nn = (size_t)n * n;
+    double* id = ws; double* a2 = ws + nn; double* f0 = ws + 2 * nn; double* f1 = ws + 3 * nn;
+    double* inner = ws + 4 * nn; double* p = ws + 5 * nn;
+    memset(id, 0, sizeof(double) * nn);
+    for (int i = 0; i < n; ++i) id[(size_t)i * n + i] = 1.0;
+    oracle_matmul(a, a, a2, n);
+    if (degree == 2) {
+        const double k[3] = {1.0, 1.0, 0.5};
+        const double* m[3] = {id, a, a2};
+        lincomb(k, m, 3, out, nn);
+        return;
+    }
+    { const double k[2] = {1.0, 1.0}; const double* m[2] = {id, a}; lincomb(k, m, 2, f0, nn); }
+    { const double k[2] = {inv_factorial(2), inv_factorial(3)}; const double* m[2] = {id, a};
+      lincomb(k, m, 2, f1, nn); }
+    { const double k[2] = {1.0, inv_factorial(4)}; const double* m[2] = {f1, a2};
+      lincomb(k, m, 2, inner, nn); }
+    oracle_matmul(inner, a2, p, n);
+    add(f0, p, out, nn);
+}
+
+/* eval_taylor_new degree dispatch (taylor_schemes.cpp:211-227). Returns the
+ * number of products, or -1 for an unsupported degree. */
+int oracle_eval_taylor_new(const double* a, int n, int degree, double* out) {
+    const size_t nn = (size_t)n * n;
+    double* ws = (double*)malloc(sizeof(double) * nn * 12);
+    int products = -1;
+    switch (degree) {
+        case 1: {
+            memset(ws, 0, sizeof(double) * nn);
+            for (int i = 0; i < n; ++i) ws[(size_t)i * n + i] = 1.0;
+            add(ws, a, out, nn);
+            products = 0;
+            break;
+        }
+        case 2: eval_ps(a, n, 2, out, ws); products = 1; break;
+        case 4: eval_ps(a, n, 4, out, ws); products = 2; break;
+        case 8: eval_t8(a, n, out, ws); products = 3; break;
+        case 12: eval_t12(a, n, out, ws); products = 4; break;
+        case 18: eval_t18(a, n, out, ws); products = 5; break;
+        default: break;
+    }
+    free(ws);
+    return products;
+}
+
+/* expm driver (proj/src/expm.cpp:37-74): finite check, norm, select, exact
+ * scaling by 2^-s, T_m, s squarings, report. */
+int oracle_expm(const double* a, int n, int accuracy, double* out, int32_t* degree,
+                int32_t* s, int64_t* cost_thirds, double* norm_in) {
+    const size_t nn = (size_t)n * n;
+    for (size_t e = 0; e < nn; ++e)
+        if (!isfinite(a[e])) return ORC_NONFINITE; /* expm.cpp:38 */
+    const double norm = oracle_one_norm(a, n);
+    int32_t m = 0, k = 0;
+    const int st = oracle_select(norm, accuracy, &m, &k);
+    if (st != ORC_OK) return st;
+    double* arg = (double*)malloc(sizeof(double) * nn);
+    double* tmp = (double*)malloc(sizeof(double) * nn);
+    if (k == 0) {
+        memcpy(arg, a, sizeof(double) * nn);
+    } else {
+        const double f = ldexp(1.0, -k); /* scale: kernels.cpp:39-42 */
+        for (size_t e = 0; e < nn; ++e) arg[e] = f * a[e];
+    }
+    const int products = oracle_eval_taylor_new(arg, n, m, out);
+    for (int i = 0; i < k; ++i) { /* squarings: expm.cpp:31-35 */
+        oracle_matmul(out, out, tmp, n);
+        memcpy(out, tmp, sizeof(double) * nn);
+    }
+    free(arg);
+    free(tmp);
+    if (degree) *degree = m;
+    if (s) *s = k;
+    if (cost_thirds) *cost_thirds = 3 * (int64_t)(products + k);
+    if (norm_in) *norm_in = norm;
+    return ORC_OK;
+}
+
+/* Batched driver over contiguous row-major matrices; per-matrix status. */
+int oracle_expm_batch(const double* a, double* out, int n, int64_t batch, int accuracy,
+                      int32_t* degree, int32_t* s, int64_t* cost_thirds, double* norm_in,
+                      int32_t* status) {
+    const size_t nn = (size_t)n * n;
+    int worst = ORC_OK;
+    for (int64_t b = 0; b < batch; ++b) {
+        const int st = oracle_expm(a + b * nn, n, accuracy, out + b * nn,
+                                   degree ? degree + b : NULL, s ? s + b : NULL,
+                                   cost_thirds ? cost_thirds + b : NULL,
+                                   norm_in ? norm_in + b : NULL);
+        if (st != ORC_OK) {
+            for (size_t e = 0; e < nn; ++e) out[b * nn + e] = NAN;
+            if (degree) degree[b] = 0;
+            if (s) s[b] = 0;
+            if (cost_thirds) cost_thirds[b] = 0;
+            if (norm_in) norm_in[b] = NAN;
+            if (worst == ORC_OK) worst = st;
+        }
+        if (status) status[b] = st;
+    }
+    return worst;
+}
+
+/* Coefficients as the oracle holds them (same order as ref_coefficients). */
+void oracle_coefficients(double* t8, double* t12, double* t18a, double* t18b) {
+    const t8c c = make_t8();
+    const double v[10] = {c.x1, c.x2, c.x3, c.x4, c.x5, c.x6, c.x7, c.y0, c.y1, c.y2};
+    memcpy(t8, v, sizeof v);
+    memcpy(t12, kT12, sizeof kT12);
+    memcpy(t18a, kT18A, sizeof kT18A);
+    memcpy(t18b, kT18B, sizeof kT18B);
+}

@@ -1,0 +1,179 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// extern "C" shim over the UNMODIFIED reference library (`mexp`, compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/). It lets the
+// pytest suite, the golden-fixture generator and bench.py's CPU baseline call
+// the reference through ctypes with plain pointers. Only tests/, smoke() and
+// bench.py (cpu_baseline leg / --impl reference) may load the result.
+//
+// Every function forwards to the reference symbol named beside it; nothing
+// here re-implements arithmetic.
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "mexp/dense_matrix.hpp"
+#include "mexp/expm.hpp"
+#include "mexp/kernels.hpp"
+#include "mexp/taylor_schemes.hpp"
+#include "mexp/theta_tables.hpp"
+
+namespace {
+
+// status codes mirror include/mexp_b200.h
+constexpr int kOk = 0;
+constexpr int kNonFinite = 1;
+constexpr int kNormNonFinite = 2;
+constexpr int kInvalid = 3;
+
+mexp::Accuracy acc_of(int a) { return a == 0 ? mexp::Accuracy::Single : mexp::Accuracy::Double; }
+
+mexp::Family fam_of(int f) {
+    switch (f) {
+        case 1: return mexp::Family::TaylorPS;
+        case 2: return mexp::Family::PadeDiagonal;
+        default: return mexp::Family::TaylorNew;
+    }
+}
+
+template <class T>
+mexp::DenseMatrix to_dense(const T* a, int n) {
+    std::vector<double> v(std::size_t(n) * n);
+    for (std::size_t e = 0; e < v.size(); ++e) v[e] = double(a[e]);
+    return mexp::DenseMatrix(n, std::move(v));
+}
+
+template <class T, class U>
+int expm_one(const T* a, int n, int accuracy, int family, U* out, int32_t* degree,
+             int32_t* s, int64_t* cost_thirds, double* norm_in) {
+    const std::size_t nn = std::size_t(n) * n;
+    try {
+        const auto rep = mexp::expm(to_dense(a, n), acc_of(accuracy), fam_of(family));
+        for (std::size_t e = 0; e < nn; ++e) out[e] = U(rep.result.data()[e]);
+        if (degree) *degree = rep.degree;
+        if (s) *s = rep.s;
+        if (cost_thirds) *cost_thirds = rep.cost_thirds;
+        if (norm_in) *norm_in = rep.norm_in;
+        return kOk;
+    } catch (const std::invalid_argument& e) {
+        for (std::size_t k = 0; k < nn; ++k) out[k] = U(NAN);
+        if (degree) *degree = 0;
+        if (s) *s = 0;
+        if (cost_thirds) *cost_thirds = 0;
+        if (norm_in) *norm_in = NAN;
+        if (std::strstr(e.what(), "non-finite")) return kNonFinite;
+        if (std::strstr(e.what(), "norm")) return kNormNonFinite;
+        return kInvalid;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+// mexp::expm (reference include/mexp/expm.hpp:37, src/expm.cpp:37-74) over a
+// contiguous batch of row-major n x n matrices, one call per matrix, serial.
+int ref_expm_batch_f64(const double* a, double* out, int n, int64_t batch, int accuracy,
+                       int family, int32_t* degree, int32_t* s, int64_t* cost_thirds,
+                       double* norm_in, int32_t* status) {
+    const std::size_t nn = std::size_t(n) * n;
+    int worst = kOk;
+    for (int64_t b = 0; b < batch; ++b) {
+        const int st = expm_one(a + b * nn, n, accuracy, family, out + b * nn,
+                                degree ? degree + b : nullptr, s ? s + b : nullptr,
+                                cost_thirds ? cost_thirds + b : nullptr,
+                                norm_in ? norm_in + b : nullptr);
+        if (status) status[b] = st;
+        if (st != kOk && worst == kOk) worst = st;
+    }
+    return worst;
+}
+
+// Same, for float storage: values are promoted to double, the reference runs
+// in double (expm.hpp:34-36), and the result is rounded back to float.
+int ref_expm_batch_f32_out64(const float* a, double* out, int n, int64_t batch,
+                             int accuracy, int family, int32_t* degree, int32_t* s,
+                             int64_t* cost_thirds, double* norm_in, int32_t* status) {
+    const std::size_t nn = std::size_t(n) * n;
+    int worst = kOk;
+    for (int64_t b = 0; b < batch; ++b) {
+        const int st = expm_one(a + b * nn, n, accuracy, family, out + b * nn,
+                                degree ? degree + b : nullptr, s ? s + b : nullptr,
+                                cost_thirds ? cost_thirds + b : nullptr,
+                                norm_in ? norm_in + b : nullptr);
+        if (status) status[b] = st;
+        if (st != kOk && worst == kOk) worst = st;
+    }
+    return worst;
+}
+
+// mexp::select (src/expm.cpp:11-29). Returns 0, or kNormNonFinite on throw.
+int ref_select(double norm, int accuracy, int family, int32_t* degree, int32_t* s) {
+    try {
+        const auto sel = mexp::select(norm, mexp::selection_table(fam_of(family), acc_of(accuracy)));
+        *degree = sel.degree;
+        *s = sel.s;
+        return kOk;
+    } catch (const std::invalid_argument&) {
+        return kNormNonFinite;
+    }
+}
+
+// mexp::kernels::one_norm (src/kernels.cpp:44-53).
+double ref_one_norm(const double* a, int n) { return mexp::kernels::one_norm(a, n); }
+
+// mexp::kernels::matmul (src/kernels.cpp:16-27).
+void ref_matmul(const double* a, const double* b, double* c, int n) {
+    mexp::kernels::matmul(a, b, c, n);
+}
+
+// selection_table (src/theta_tables.cpp:77-85): writes up to cap entries.
+int ref_theta_table(int accuracy, int family, int32_t* degrees, int32_t* products,
+                    double* thetas, int cap) {
+    const auto& t = mexp::selection_table(fam_of(family), acc_of(accuracy));
+    int k = 0;
+    for (const auto& e : t.entries) {
+        if (k >= cap) break;
+        degrees[k] = e.degree;
+        products[k] = e.products;
+        thetas[k] = e.theta;
+        ++k;
+    }
+    return k;
+}
+
+// eval_taylor_new (src/taylor_schemes.cpp:211-227) on one matrix; returns
+// the product count recorded in the CostContext, or -1 on invalid degree.
+int ref_eval_taylor_new(const double* a, int n, int degree, double* out) {
+    try {
+        mexp::CostContext ctx;
+        const auto r = mexp::eval_taylor_new(ctx, to_dense(a, n), degree);
+        std::memcpy(out, r.data(), sizeof(double) * std::size_t(n) * n);
+        return int(ctx.products);
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
+// taylor_oracle (src/taylor_schemes.cpp:87-94): plain Horner.
+void ref_taylor_oracle(const double* a, int n, int degree, double* out) {
+    const auto r = mexp::taylor_oracle(to_dense(a, n), degree);
+    std::memcpy(out, r.data(), sizeof(double) * std::size_t(n) * n);
+}
+
+// Scheme coefficients as the library holds them at run time:
+// t8 (10 values, taylor_schemes.cpp:12-27), kT12 (16, :62-71),
+// kT18A (4) + kT18B (20) (:73-85).
+void ref_coefficients(double* t8, double* t12, double* t18a, double* t18b) {
+    const auto& c = mexp::t8_coefficients();
+    const double v[10] = {c.x1, c.x2, c.x3, c.x4, c.x5, c.x6, c.x7, c.y0, c.y1, c.y2};
+    std::memcpy(t8, v, sizeof v);
+    std::memcpy(t12, mexp::kT12, sizeof(double) * 16);
+    std::memcpy(t18a, mexp::kT18A, sizeof(double) * 4);
+    std::memcpy(t18b, mexp::kT18B, sizeof(double) * 20);
+}
+
+}  // extern "C"

@@ -1,0 +1,261 @@
+"""B200-native scaling-and-squaring expm (arXiv 1710.10989, Family::TaylorNew).
+
+Python mirror of the reference's C++ API (namespace ``mexp``:
+proj/include/mexp/expm.hpp, theta_tables.hpp) over the C ABI in
+``include/mexp_b200.h`` (library ``_lib/libmexp_b200.so``, built by ``make``).
+
+* ``expm(a, accuracy, family) -> ExpmReport``      mexp::expm (expm.hpp:37)
+* ``select(norm, table) -> Selection``             mexp::select (expm.hpp:18)
+* ``selection_table(family, accuracy)``            theta_tables.hpp:32
+* ``expm_batched(a, out, ...)``                    batched, device tensors
+* ``expm_batched_host(a, ...)``                    batched, host arrays (e2e)
+
+Errors follow the reference: ``std::invalid_argument`` becomes ``ValueError``
+with the reference's message. There is no CPU fallback: without the CUDA
+library or a device every compute call raises ``RuntimeError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libmexp_b200.so")
+
+# mexp_status (include/mexp_b200.h)
+OK, ERR_NONFINITE, ERR_NORM_NONFINITE, ERR_INVALID_ARGUMENT = 0, 1, 2, 3
+ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_DEVICE = 4, 5, 6
+F64, F32 = 0, 1
+ROUND_AUTO, ROUND_REFERENCE, ROUND_FAST = 0, 1, 2
+
+
+class Family(enum.IntEnum):
+    """theta_tables.hpp:8."""
+    TaylorNew = 0
+    TaylorPS = 1
+    PadeDiagonal = 2
+
+
+class Accuracy(enum.IntEnum):
+    """theta_tables.hpp:9: u = 2^-24 (Single) or 2^-53 (Double)."""
+    Single = 0
+    Double = 1
+
+
+class Selection(C.Structure):
+    """mexp_selection: one 16-byte record per matrix."""
+    _fields_ = [("norm_in", C.c_double), ("degree", C.c_int16), ("s", C.c_int16),
+                ("status", C.c_int32)]
+
+
+SELECTION_DTYPE = np.dtype([("norm_in", "<f8"), ("degree", "<i2"), ("s", "<i2"),
+                            ("status", "<i4")])
+
+
+class _Report(C.Structure):
+    _fields_ = [("family", C.c_int32), ("degree", C.c_int32), ("s", C.c_int32),
+                ("reserved", C.c_int32), ("cost_thirds", C.c_int64), ("norm_in", C.c_double)]
+
+
+@dataclass
+class SchemeDescriptor:
+    """theta_tables.hpp:15-20."""
+    family: Family
+    degree: int
+    products: int
+    theta: float
+
+
+@dataclass
+class SelectionTable:
+    """theta_tables.hpp:22-28."""
+    family: Family
+    accuracy: Accuracy
+    entries: list
+
+    def asymptotic(self) -> SchemeDescriptor:
+        return self.entries[-1]
+
+    def theta_max(self) -> float:
+        return self.entries[-1].theta
+
+
+@dataclass
+class ExpmReport:
+    """expm.hpp:23-32."""
+    result: np.ndarray
+    family: Family
+    degree: int
+    s: int
+    cost_thirds: int
+    norm_in: float
+
+    def product_cost(self) -> float:
+        return self.cost_thirds / 3.0
+
+
+_lib = None
+
+
+def library() -> C.CDLL:
+    """Load the in-tree CUDA library; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `make` (there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, I, I64, D = C.c_void_p, C.c_int, C.c_int64, C.c_double
+    sig = {
+        "mexp_abi_version": (I, []),
+        "mexp_device_check": (I, []),
+        "mexp_status_string": (C.c_char_p, [I]),
+        "mexp_last_cuda_error": (C.c_char_p, []),
+        "mexp_launch_count": (C.c_uint64, []),
+        "mexp_unit_roundoff": (D, [I]),
+        "mexp_selection_table": (I, [I, I, P, P, P, I]),
+        "mexp_select": (I, [D, I, I, P, P]),
+        "mexp_expm": (I, [P, I, I, I, P, P]),
+        "mexp_expm_batched": (I, [P, P, I, I, I64, I, I, I, P, P]),
+        "mexp_expm_batched_host": (I, [P, P, I, I, I64, I, I, I, P, P]),
+        "mexp_squarings_batched": (I, [P, I, I64, I, I, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+EXPORTED_SYMBOLS = (
+    "mexp_abi_version", "mexp_device_check", "mexp_status_string", "mexp_last_cuda_error",
+    "mexp_launch_count", "mexp_unit_roundoff", "mexp_selection_table", "mexp_select",
+    "mexp_expm", "mexp_expm_batched", "mexp_expm_batched_host", "mexp_squarings_batched",
+)
+
+
+def _raise(status: int):
+    lib = library()
+    msg = lib.mexp_status_string(status).decode()
+    if status in (ERR_NONFINITE, ERR_NORM_NONFINITE, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    if status == ERR_CUDA:
+        raise RuntimeError(f"{msg}: {lib.mexp_last_cuda_error().decode()}")
+    raise RuntimeError(msg)
+
+
+def unit_roundoff(u: Accuracy) -> float:
+    return library().mexp_unit_roundoff(int(u))
+
+
+def selection_table(family: Family, u: Accuracy) -> SelectionTable:
+    """mexp::selection_table (theta_tables.cpp:77-85)."""
+    d = np.zeros(16, np.int32)
+    p = np.zeros(16, np.int32)
+    t = np.zeros(16, np.float64)
+    k = library().mexp_selection_table(int(u), int(family), d.ctypes.data, p.ctypes.data,
+                                       t.ctypes.data, 16)
+    if k < 0:
+        _raise(-k)
+    return SelectionTable(Family(family), Accuracy(u),
+                          [SchemeDescriptor(Family(family), int(d[i]), int(p[i]), float(t[i]))
+                           for i in range(k)])
+
+
+def select(norm: float, table: SelectionTable):
+    """mexp::select (expm.cpp:11-29) -> (degree, s)."""
+    d, s = C.c_int32(), C.c_int32()
+    st = library().mexp_select(float(norm), int(table.accuracy), int(table.family),
+                               C.byref(d), C.byref(s))
+    if st != OK:
+        _raise(st)
+    return d.value, s.value
+
+
+def expm(a: np.ndarray, u: Accuracy = Accuracy.Double,
+         family: Family = Family.TaylorNew) -> ExpmReport:
+    """mexp::expm (expm.cpp:37-74) on one host matrix, computed on the GPU."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] < 1:
+        raise ValueError("matrix must be square")
+    n = a.shape[0]
+    out = np.empty_like(a)
+    rep = _Report()
+    st = library().mexp_expm(a.ctypes.data, n, int(u), int(family), out.ctypes.data, C.byref(rep))
+    if st != OK:
+        _raise(st)
+    return ExpmReport(out, Family(family), rep.degree, rep.s, rep.cost_thirds, rep.norm_in)
+
+
+def _dtype_code(dt) -> int:
+    s = str(dt)
+    if "float64" in s:
+        return F64
+    if "float32" in s:
+        return F32
+    raise ValueError(f"unsupported dtype {dt}")
+
+
+def expm_batched(a, out, sel=None, accuracy: Accuracy = Accuracy.Double,
+                 rounding: int = ROUND_AUTO, stream=None, family: Family = Family.TaylorNew):
+    """Batched expm on device tensors (torch, CUDA, contiguous (batch, n, n)).
+
+    ``sel``: optional uint8 device tensor of 16*batch bytes (SELECTION_DTYPE
+    records). Asynchronous on ``stream`` (default: torch's current stream).
+    """
+    import torch
+    assert a.is_cuda and out.is_cuda and a.is_contiguous() and out.is_contiguous()
+    batch, n, n2 = a.shape
+    if n != n2 or out.shape != a.shape or out.dtype != a.dtype:
+        raise ValueError("dimension mismatch")
+    if stream is None:
+        stream = torch.cuda.current_stream(a.device)
+    st = library().mexp_expm_batched(a.data_ptr(), out.data_ptr(), _dtype_code(a.dtype), n,
+                                     batch, int(accuracy), int(family), int(rounding),
+                                     None if sel is None else sel.data_ptr(),
+                                     C.c_void_p(stream.cuda_stream))
+    if st != OK:
+        _raise(st)
+
+
+def expm_batched_host(a, out=None, accuracy: Accuracy = Accuracy.Double,
+                      rounding: int = ROUND_AUTO, family: Family = Family.TaylorNew,
+                      raise_on_error: bool = True):
+    """Batched expm on host buffers (numpy arrays or pinned CPU torch tensors).
+
+    Returns (out, selection records as a numpy structured array, status).
+    """
+    is_np = isinstance(a, np.ndarray)
+    if is_np:
+        a = np.ascontiguousarray(a)
+        if out is None:
+            out = np.empty_like(a)
+        pa, po = a.ctypes.data, out.ctypes.data
+        batch, n, _ = a.shape
+        dt = _dtype_code(a.dtype)
+    else:
+        if out is None:
+            out = a.new_empty(a.shape)
+        pa, po = a.data_ptr(), out.data_ptr()
+        batch, n, _ = a.shape
+        dt = _dtype_code(a.dtype)
+    sel = np.zeros(batch, SELECTION_DTYPE)
+    first = C.c_int64(-1)
+    st = library().mexp_expm_batched_host(pa, po, dt, n, batch, int(accuracy), int(family),
+                                          int(rounding), sel.ctypes.data, C.byref(first))
+    if st not in (OK, ERR_NONFINITE, ERR_NORM_NONFINITE) or (st != OK and raise_on_error):
+        _raise(st)
+    return out, sel, st
+
+
+def launch_count() -> int:
+    return int(library().mexp_launch_count())
+
+
+def products_of_degree(m: int) -> int:
+    return {1: 0, 2: 1, 4: 2, 8: 3, 12: 4, 18: 5}[int(m)]

@@ -1,0 +1,407 @@
+// C ABI of the B200 expm path (declarations: include/mexp_b200.h).
+//
+// Dispatch: n <= 64 runs the small-n group kernels (matrices zero-padded to
+// n in {8, 16, 32, 64} when needed: padding with zeros leaves the 1-norm, the
+// selection and -- in reference rounding -- every rounding of the top-left
+// block unchanged, since each padded term adds an exact +0 to a sum that is
+// never -0). n > 64 runs the DMMA GEMM engine (expm_large.cu).
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "expm_common.cuh"
+#include "expm_large.cuh"
+#include "expm_small.cuh"
+#include "expm_small_f32.cuh"
+
+using namespace mexp_b200;
+
+namespace {
+
+thread_local std::string g_last_cuda_error;
+std::atomic<uint64_t> g_launches{0};
+
+int cuda_fail(cudaError_t e, const char* where) {
+    g_last_cuda_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return MEXP_ERR_CUDA;
+}
+#define MEXP_CUDA(call)                                        \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
+    } while (0)
+
+int device_ok() {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return MEXP_ERR_NO_DEVICE;
+    }
+    return MEXP_OK;
+}
+
+int padded_n(int n) { return n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : n; }
+
+bool valid_args(int dtype, int n, int64_t batch, int accuracy, int family, int rounding) {
+    return (dtype == MEXP_F64 || dtype == MEXP_F32) && n >= 1 && batch >= 0 &&
+           (accuracy == MEXP_ACCURACY_SINGLE || accuracy == MEXP_ACCURACY_DOUBLE) &&
+           (family >= 0 && family <= 2) && (rounding >= 0 && rounding <= 2);
+}
+
+// Rounding threshold of the AUTO policy: matrices with s >= this run the
+// reference-exact arithmetic (SURVEY.md key finding 3: FMA-rounded results
+// leave the 50*n*u band only when 6 or more squarings amplify them).
+constexpr int kExactSMin = 6;
+
+template <class T>
+__global__ void pad_kernel(const T* __restrict__ src, T* __restrict__ dst, int n, int np,
+                           int64_t batch) {
+    const int64_t total = batch * int64_t(np) * np;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = i / (int64_t(np) * np);
+        const int r = int((i / np) % np), c = int(i % np);
+        dst[i] = (r < n && c < n) ? src[b * n * n + r * n + c] : T(0);
+    }
+}
+template <class T>
+__global__ void unpad_kernel(const T* __restrict__ src, T* __restrict__ dst, int n, int np,
+                             int64_t batch) {
+    const int64_t total = batch * int64_t(n) * n;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = i / (int64_t(n) * n);
+        const int r = int((i / n) % n), c = int(i % n);
+        dst[i] = src[b * np * np + r * np + c];
+    }
+}
+
+int num_sms() {
+    static int sms = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return sms;
+}
+
+template <int N, int GPC>
+int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
+                     int accuracy, int rounding, cudaStream_t st) {
+    using G = Group<N>;
+    auto kern = expm_small_f64_kernel<N, GPC>;
+    const size_t smem = size_t(G::SMEM_DOUBLES) * GPC * sizeof(double);
+    static int blocks_per_sm = [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * G::W * GPC, smem);
+        return b > 0 ? b : 1;
+    }();
+    const int64_t want = (batch + GPC - 1) / GPC;
+    const int64_t cap = int64_t(blocks_per_sm) * num_sms();
+    const int grid = int(want < cap ? want : cap);
+    if (grid == 0) return MEXP_OK;
+    kern<<<grid, 32 * G::W * GPC, smem, st>>>(a, out, sel, batch, accuracy, rounding, kExactSMin);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    MEXP_CUDA(cudaGetLastError());
+    return MEXP_OK;
+}
+
+int run_small_f64(const double* a, double* out, mexp_selection* sel, int np, int64_t batch,
+                  int accuracy, int rounding, cudaStream_t st) {
+    switch (np) {
+        case 8: return launch_small_f64<8, 8>(a, out, sel, batch, accuracy, rounding, st);
+        case 16: return launch_small_f64<16, 4>(a, out, sel, batch, accuracy, rounding, st);
+        case 32: return launch_small_f64<32, 2>(a, out, sel, batch, accuracy, rounding, st);
+        case 64: return launch_small_f64<64, 1>(a, out, sel, batch, accuracy, rounding, st);
+    }
+    return MEXP_ERR_UNSUPPORTED;
+}
+
+// Device-buffer entry, no argument validation (callers validated).
+int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, int accuracy,
+                int rounding, mexp_selection* d_sel, cudaStream_t st) {
+    if (batch == 0) return MEXP_OK;
+    if (n > 64) {
+        if (dtype != MEXP_F64) return MEXP_ERR_UNSUPPORTED;
+        const int r = large_expm_f64(static_cast<const double*>(d_a), static_cast<double*>(d_out),
+                                     d_sel, n, batch, accuracy, st, &g_launches);
+        if (r == MEXP_ERR_CUDA) g_last_cuda_error = large_last_error();
+        return r;
+    }
+    const int np = padded_n(n);
+    const size_t esz = dtype == MEXP_F64 ? sizeof(double) : sizeof(float);
+    const void* src = d_a;
+    void* dst = d_out;
+    void* pin = nullptr;
+    void* pout = nullptr;
+    if (np != n) {
+        const size_t bytes = size_t(batch) * np * np * esz;
+        MEXP_CUDA(cudaMallocAsync(&pin, bytes, st));
+        MEXP_CUDA(cudaMallocAsync(&pout, bytes, st));
+        const int grid = 4 * num_sms();
+        if (dtype == MEXP_F64)
+            pad_kernel<<<grid, 256, 0, st>>>(static_cast<const double*>(d_a), static_cast<double*>(pin),
+                                             n, np, batch);
+        else
+            pad_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(d_a), static_cast<float*>(pin),
+                                             n, np, batch);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        src = pin;
+        dst = pout;
+    }
+    int r;
+    if (dtype == MEXP_F64) {
+        r = run_small_f64(static_cast<const double*>(src), static_cast<double*>(dst), d_sel, np,
+                          batch, accuracy, rounding, st);
+    } else {
+        r = run_small_f32(static_cast<const float*>(src), static_cast<float*>(dst), d_sel, np,
+                          batch, accuracy, st, &g_launches);
+    }
+    if (r != MEXP_OK) return r;
+    if (np != n) {
+        const int grid = 4 * num_sms();
+        if (dtype == MEXP_F64)
+            unpad_kernel<<<grid, 256, 0, st>>>(static_cast<const double*>(pout),
+                                               static_cast<double*>(d_out), n, np, batch);
+        else
+            unpad_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(pout),
+                                               static_cast<float*>(d_out), n, np, batch);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        MEXP_CUDA(cudaFreeAsync(pin, st));
+        MEXP_CUDA(cudaFreeAsync(pout, st));
+    }
+    MEXP_CUDA(cudaGetLastError());
+    return MEXP_OK;
+}
+
+// ---- host pipeline state: per-device streams and chunk buffers ------------
+struct HostPipe {
+    static constexpr int kStreams = 3;
+    int device = -1;
+    cudaStream_t st[kStreams] = {};
+    void* d_in[kStreams] = {};
+    void* d_out[kStreams] = {};
+    mexp_selection* d_sel[kStreams] = {};
+    size_t cap_bytes = 0;   // per-stream matrix buffer capacity
+    int64_t cap_sel = 0;
+    mexp_selection* h_sel_scratch = nullptr;  // pinned, used when the caller passes none
+    int64_t h_sel_cap = 0;
+    std::mutex mu;
+};
+
+HostPipe& pipe_for_current_device() {
+    static HostPipe pipes[16];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return pipes[dev & 15];
+}
+
+int ensure_pipe(HostPipe& p, size_t bytes, int64_t sels) {
+    int dev = 0;
+    MEXP_CUDA(cudaGetDevice(&dev));
+    if (p.device != dev) {
+        for (int i = 0; i < HostPipe::kStreams; ++i)
+            MEXP_CUDA(cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking));
+        p.device = dev;
+    }
+    if (bytes > p.cap_bytes || sels > p.cap_sel) {
+        for (int i = 0; i < HostPipe::kStreams; ++i) {
+            MEXP_CUDA(cudaStreamSynchronize(p.st[i]));
+            cudaFree(p.d_in[i]);
+            cudaFree(p.d_out[i]);
+            cudaFree(p.d_sel[i]);
+            MEXP_CUDA(cudaMalloc(&p.d_in[i], bytes));
+            MEXP_CUDA(cudaMalloc(&p.d_out[i], bytes));
+            MEXP_CUDA(cudaMalloc(&p.d_sel[i], sizeof(mexp_selection) * sels));
+        }
+        p.cap_bytes = bytes;
+        p.cap_sel = sels;
+    }
+    return MEXP_OK;
+}
+
+const double kThetaHost[2][6] = {
+    {1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01},
+    {2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09},
+};
+
+}  // namespace
+
+extern "C" {
+
+int mexp_abi_version(void) { return MEXP_B200_ABI_VERSION; }
+
+int mexp_device_check(void) {
+    const int r = device_ok();
+    if (r != MEXP_OK) return r;
+    int dev = 0, major = 0;
+    MEXP_CUDA(cudaGetDevice(&dev));
+    MEXP_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    return major == 10 ? MEXP_OK : MEXP_ERR_NO_DEVICE;
+}
+
+const char* mexp_status_string(int status) {
+    switch (status) {
+        case MEXP_OK: return "ok";
+        case MEXP_ERR_NONFINITE: return "non-finite matrix entry";
+        case MEXP_ERR_NORM_NONFINITE: return "norm must be finite and nonnegative";
+        case MEXP_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case MEXP_ERR_UNSUPPORTED: return "unsupported on the B200 TaylorNew path";
+        case MEXP_ERR_CUDA: return "CUDA error";
+        case MEXP_ERR_NO_DEVICE: return "no usable CUDA device (there is no CPU fallback)";
+    }
+    return "unknown status";
+}
+
+const char* mexp_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
+
+uint64_t mexp_launch_count(void) { return g_launches.load(); }
+
+double mexp_unit_roundoff(int accuracy) {
+    return accuracy == MEXP_ACCURACY_SINGLE ? 0x1p-24 : 0x1p-53;
+}
+
+int mexp_selection_table(int accuracy, int family, int32_t* degrees, int32_t* products,
+                         double* thetas, int cap) {
+    if (accuracy != MEXP_ACCURACY_SINGLE && accuracy != MEXP_ACCURACY_DOUBLE)
+        return -MEXP_ERR_INVALID_ARGUMENT;
+    if (family != MEXP_FAMILY_TAYLOR_NEW) return -MEXP_ERR_UNSUPPORTED;
+    int k = 0;
+    for (int e = 0; e < kNumEntries && k < cap; ++e, ++k) {
+        degrees[k] = degree_of(e);
+        products[k] = products_of_entry(e);
+        thetas[k] = kThetaHost[accuracy][e];
+    }
+    return k;
+}
+
+// mexp::select (expm.cpp:11-29) on the host: pure table arithmetic.
+int mexp_select(double norm, int accuracy, int family, int32_t* degree, int32_t* s) {
+    if (accuracy != MEXP_ACCURACY_SINGLE && accuracy != MEXP_ACCURACY_DOUBLE)
+        return MEXP_ERR_INVALID_ARGUMENT;
+    if (family != MEXP_FAMILY_TAYLOR_NEW) return MEXP_ERR_UNSUPPORTED;
+    const double* th = kThetaHost[accuracy];
+    if (!std::isfinite(norm) || norm < 0) return MEXP_ERR_NORM_NONFINITE;
+    if (norm <= th[5]) {
+        int best = -1;
+        for (int e = 0; e < 6; ++e) {
+            if (th[e] < norm) continue;
+            if (best < 0 || products_of_entry(e) < products_of_entry(best)) best = e;
+        }
+        *degree = degree_of(best);
+        *s = 0;
+        return MEXP_OK;
+    }
+    int k = 0;
+    while (std::ldexp(norm, -k) > th[5]) ++k;
+    *degree = 18;
+    *s = k;
+    return MEXP_OK;
+}
+
+int mexp_expm_batched(const void* d_a, void* d_out, int dtype, int n, int64_t batch,
+                      int accuracy, int family, int rounding, mexp_selection* d_sel,
+                      void* stream) {
+    if (!valid_args(dtype, n, batch, accuracy, family, rounding)) return MEXP_ERR_INVALID_ARGUMENT;
+    if (family != MEXP_FAMILY_TAYLOR_NEW) return MEXP_ERR_UNSUPPORTED;
+    if (batch > 0 && (!d_a || !d_out)) return MEXP_ERR_INVALID_ARGUMENT;
+    const int dv = device_ok();
+    if (dv != MEXP_OK) return dv;
+    return expm_device(d_a, d_out, dtype, n, batch, accuracy, rounding, d_sel,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64_t batch,
+                           int accuracy, int family, int rounding, mexp_selection* h_sel,
+                           int64_t* first_error) {
+    if (!valid_args(dtype, n, batch, accuracy, family, rounding)) return MEXP_ERR_INVALID_ARGUMENT;
+    if (family != MEXP_FAMILY_TAYLOR_NEW) return MEXP_ERR_UNSUPPORTED;
+    if (first_error) *first_error = -1;
+    if (batch == 0) return MEXP_OK;
+    if (!h_a || !h_out) return MEXP_ERR_INVALID_ARGUMENT;
+    const int dv = device_ok();
+    if (dv != MEXP_OK) return dv;
+
+    HostPipe& p = pipe_for_current_device();
+    std::lock_guard<std::mutex> lock(p.mu);
+    const size_t esz = dtype == MEXP_F64 ? sizeof(double) : sizeof(float);
+    const size_t mat_bytes = size_t(n) * n * esz;
+    // ~24 MiB per chunk keeps three chunks in flight (H2D, compute, D2H)
+    int64_t chunk = int64_t((24u << 20) / mat_bytes);
+    if (chunk < 1) chunk = 1;
+    if (n > 64) chunk = batch;  // the large-n engine wants the whole ragged batch
+    if (chunk > batch) chunk = batch;
+    int r = ensure_pipe(p, size_t(chunk) * mat_bytes, chunk);
+    if (r != MEXP_OK) return r;
+    mexp_selection* hs = h_sel;
+    if (!hs) {
+        if (p.h_sel_cap < batch) {
+            if (p.h_sel_scratch) cudaFreeHost(p.h_sel_scratch);
+            p.h_sel_scratch = nullptr;
+            MEXP_CUDA(cudaMallocHost(&p.h_sel_scratch, sizeof(mexp_selection) * batch));
+            p.h_sel_cap = batch;
+        }
+        hs = p.h_sel_scratch;
+    }
+    const char* src = static_cast<const char*>(h_a);
+    char* dst = static_cast<char*>(h_out);
+    int c = 0;
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++c) {
+        const int k = c % HostPipe::kStreams;
+        const int64_t nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+        cudaStream_t st = p.st[k];
+        MEXP_CUDA(cudaMemcpyAsync(p.d_in[k], src + b0 * mat_bytes, nb * mat_bytes,
+                                  cudaMemcpyHostToDevice, st));
+        r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, accuracy, rounding, p.d_sel[k], st);
+        if (r != MEXP_OK) return r;
+        MEXP_CUDA(cudaMemcpyAsync(dst + b0 * mat_bytes, p.d_out[k], nb * mat_bytes,
+                                  cudaMemcpyDeviceToHost, st));
+        MEXP_CUDA(cudaMemcpyAsync(hs + b0, p.d_sel[k], nb * sizeof(mexp_selection),
+                                  cudaMemcpyDeviceToHost, st));
+    }
+    for (int i = 0; i < HostPipe::kStreams; ++i) MEXP_CUDA(cudaStreamSynchronize(p.st[i]));
+    for (int64_t b = 0; b < batch; ++b) {
+        if (hs[b].status != MEXP_OK) {
+            if (first_error) *first_error = b;
+            return hs[b].status;
+        }
+    }
+    return MEXP_OK;
+}
+
+int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
+              mexp_report* report) {
+    mexp_selection sel{};
+    const int r = mexp_expm_batched_host(a, result, MEXP_F64, n, 1, accuracy, family,
+                                         MEXP_ROUND_AUTO, &sel, nullptr);
+    if (r != MEXP_OK) return r;
+    if (report) {
+        report->family = family;
+        report->degree = sel.degree;
+        report->s = sel.s;
+        report->reserved = 0;
+        report->cost_thirds = 3 * int64_t(products_of_degree(sel.degree) + sel.s);
+        report->norm_in = sel.norm_in;
+    }
+    return MEXP_OK;
+}
+
+int mexp_squarings_batched(double* d_x, int n, int64_t batch, int s, int rounding,
+                           void* stream) {
+    if (n < 1 || batch < 0 || s < 0 || rounding < 0 || rounding > 2)
+        return MEXP_ERR_INVALID_ARGUMENT;
+    const int dv = device_ok();
+    if (dv != MEXP_OK) return dv;
+    if (batch == 0 || s == 0) return MEXP_OK;
+    const int r = squarings_f64(d_x, n, batch, s, rounding, static_cast<cudaStream_t>(stream),
+                                &g_launches);
+    if (r == MEXP_ERR_CUDA) g_last_cuda_error = large_last_error();
+    return r;
+}
+
+}  // extern "C"

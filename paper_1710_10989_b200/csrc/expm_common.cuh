@@ -1,0 +1,175 @@
+// Shared device-side pieces of the expm kernels: the TaylorNew theta tables,
+// the scheme coefficients, the on-device (m, s) selection and the two
+// arithmetic policies (reference-exact and fast).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "mexp_b200.h"
+
+namespace mexp_b200 {
+
+// ---------------------------------------------------------------------------
+// theta_m tables for Family::TaylorNew (reference theta_tables.cpp:45-51).
+// Degrees {1,2,4,8,12,18} at {0,1,2,3,4,5} products; the literals are the
+// reference's decimal literals, so they round to the identical doubles.
+// ---------------------------------------------------------------------------
+constexpr int kNumEntries = 6;
+__constant__ double c_theta[2][kNumEntries] = {
+    {1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01},      // Accuracy::Single
+    {2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09},  // Accuracy::Double
+};
+__host__ __device__ constexpr int degree_of(int e) {
+    return e == 0 ? 1 : e == 1 ? 2 : e == 2 ? 4 : e == 3 ? 8 : e == 4 ? 12 : 18;
+}
+__host__ __device__ constexpr int products_of_entry(int e) { return e; }
+__host__ __device__ constexpr int products_of_degree(int m) {
+    return m == 1 ? 0 : m == 2 ? 1 : m == 4 ? 2 : m == 8 ? 3 : m == 12 ? 4 : m == 18 ? 5 : -1;
+}
+
+// ---------------------------------------------------------------------------
+// Scheme coefficients. T8: closed forms in sqrt(177) with x3 = 2/3, as the
+// reference rounds them once from long double (taylor_schemes.cpp:12-27);
+// the hex literals are those doubles, checked bit-for-bit against the
+// compiled reference by tests/test_oracle.py::test_device_coefficients.
+// ---------------------------------------------------------------------------
+struct T8C {
+    static constexpr double x1 = 0x1.bbdc940ef503ap-4;
+    static constexpr double x2 = 0x1.bbdc940ef503ap-6;
+    static constexpr double x3 = 0x1.5555555555555p-1;
+    static constexpr double x4 = 0x1.17f11e296523cp-1;
+    static constexpr double x5 = 0x1.49fc346242b21p-3;
+    static constexpr double x6 = 0x1.cdbb2e2ed5250p-7;
+    static constexpr double x7 = 0x1.14d4a1c010d67p-5;
+    static constexpr double y0 = 1.0;
+    static constexpr double y1 = 1.0;
+    static constexpr double y2 = 0x1.157d04e6f24b6p-3;
+};
+
+// T12 (paper eq. for the 4-product scheme; reference taylor_schemes.cpp:62-71):
+// kT12[i][j] multiplies {I, A, A2, A3}[i] in B_{j+1}.
+__constant__ double c_t12[4][4] = {
+    {9.0198e-16, 5.31597895759871264183, 0.18188869982170434744, -2.0861320e-13},
+    {0.46932117595418237389, 1.19926790417132231573, 0.05502798439925399070,
+     -0.13181061013830184015},
+    {-0.20099424927047284052, 0.01179296240992997031, 0.09351590770535414968,
+     -0.02027855540589259079},
+    {-0.04623946134063071740, 0.01108844528519167989, 0.00610700528898058230,
+     -0.00675951846863086359},
+};
+// T18 (reference taylor_schemes.cpp:73-85): c_t18a[i] multiplies {I,A,A2,A3}[i]
+// in B1; c_t18b[j][r] multiplies {I,A,A2,A3,A6}[r] in B_{j+2}.
+__constant__ double c_t18a[4] = {0.0, -0.100365581030144620, -0.0080292464824115696,
+                                 -0.0008921384980457299};
+__constant__ double c_t18b[4][5] = {
+    {0.0, 0.39784974949964507614, 1.36783778460411719922, 0.49828962252538267755,
+     -0.0006378981945947233},
+    {-10.967639605296206259, 1.68015813878906197182, 0.05717798464788655127,
+     -0.0069821012248805208, 0.00003349750170860705},
+    {-0.0904316832390810561, -0.0676404519071381907, 0.06759613017704596460,
+     0.02955525704293155274, -0.0000139180257516060},
+    {0.0, 0.0, -0.0923364619367118592, -0.0169364939002081717, -0.0000140086798182036},
+};
+// eval_ps degree 4 (taylor_schemes.cpp:158-163): 1/2!, 1/3!, 1/4! computed as
+// 1.0 / (k!) in double (inv_factorial, :44-48).
+constexpr double kInvFact2 = 0.5;
+constexpr double kInvFact3 = 0x1.5555555555555p-3;  // 1.0 / 6.0
+constexpr double kInvFact4 = 0x1.5555555555555p-5;  // 1.0 / 24.0
+
+// ---------------------------------------------------------------------------
+// Selection (reference expm.cpp:11-29): the cheapest table entry whose theta
+// admits the norm (skip on theta < norm; ties to the lower degree); beyond the
+// table, degree 18 and the least s with ldexp(norm, -s) <= theta_18.
+// ---------------------------------------------------------------------------
+struct Sel {
+    int degree;
+    int s;
+    int status;
+};
+
+__device__ __forceinline__ Sel select_device(double norm, int accuracy) {
+    const double* th = c_theta[accuracy];
+    Sel r{0, 0, MEXP_OK};
+    if (!isfinite(norm) || norm < 0.0) {
+        r.status = MEXP_ERR_NORM_NONFINITE;
+        return r;
+    }
+    if (norm <= th[kNumEntries - 1]) {
+        int best = -1;
+#pragma unroll
+        for (int e = 0; e < kNumEntries; ++e) {
+            if (th[e] < norm) continue;
+            // products and degrees both ascend with e, so the first admissible
+            // entry is the reference's (products, degree) minimum
+            if (best < 0) best = e;
+        }
+        r.degree = degree_of(best);
+        return r;
+    }
+    int s = 0;
+    while (ldexp(norm, -s) > th[kNumEntries - 1]) ++s;
+    r.degree = 18;
+    r.s = s;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Arithmetic policies.
+//   Exact: every multiply and add rounded separately (DMUL, DADD), matching
+//          the reference's -ffp-contract=off build bit for bit when the
+//          operation order is also the reference's.
+//   Fast:  fused multiply-add.
+// ---------------------------------------------------------------------------
+struct ExactOps {
+    static constexpr bool kExact = true;
+    __device__ __forceinline__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+    __device__ __forceinline__ static double add(double a, double b) { return __dadd_rn(a, b); }
+    __device__ __forceinline__ static double mac(double acc, double a, double b) {
+        return __dadd_rn(acc, __dmul_rn(a, b));
+    }
+};
+struct FastOps {
+    static constexpr bool kExact = false;
+    __device__ __forceinline__ static double mul(double a, double b) { return a * b; }
+    __device__ __forceinline__ static double add(double a, double b) { return a + b; }
+    __device__ __forceinline__ static double mac(double acc, double a, double b) {
+        return fma(a, b, acc);
+    }
+};
+
+// Streaming global accesses for the read-once input / write-once output.
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 v;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(double2* p, double2 v) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(float4* p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+// FP64 tensor-core MMA, m8n8k4 (SASS DMMA.8x8x4): D = A(8x4, row) * B(4x8, col) + C.
+// Fragment ownership per lane l: a = A[l>>2][l&3], b = B[l&3][l>>2],
+// c/d = C[l>>2][2(l&3)], C[l>>2][2(l&3)+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+}  // namespace mexp_b200

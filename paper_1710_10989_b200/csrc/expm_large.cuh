@@ -1,0 +1,23 @@
+// Large-n (n > 64) fp64 expm engine: FP64 tensor-core (DMMA) GEMMs with the
+// T18 linear combinations fused into their epilogues, batched over matrices
+// with per-matrix scaling exponents. Implementation: expm_large.cu.
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "mexp_b200.h"
+
+namespace mexp_b200 {
+
+int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel, int n,
+                   int64_t batch, int accuracy, cudaStream_t st, std::atomic<uint64_t>* launches);
+
+// X <- X^(2^s), in place, for `batch` n x n fp64 matrices.
+int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaStream_t st,
+                  std::atomic<uint64_t>* launches);
+
+const char* large_last_error();
+
+}  // namespace mexp_b200

@@ -1,0 +1,399 @@
+// Batched small-n expm, fp64 (n in {8, 16, 32, 64}): one group of W warps per
+// matrix, the whole expm (finite check, exact 1-norm, (m,s) selection, exact
+// 2^-s scaling, T_m, s squarings) inside the group with the matrix held as
+// register fragments and staged through shared memory only to re-lay out the
+// operands of each product.
+//
+// Fragment layout: the n x n matrix is cut into 8x8 tiles; each warp owns a
+// TR x TC block of tiles and, per tile, lane l holds the two elements
+// (8*ti + (l>>2), 8*tj + 2*(l&3) + {0,1}) -- the accumulator layout of the
+// FP64 tensor-core MMA m8n8k4 (DMMA). Elementwise work (the schemes' linear
+// combinations with the identity, reference kernels.cpp:29-37) runs directly
+// on fragments; a product C = X*Y (kernels.cpp:16-27) stores X and Y to
+// padded shared memory and reads them back either as DMMA operands (FastOps)
+// or as rows/columns for a k-ascending DMUL+DADD dot product (ExactOps,
+// bit-identical to the reference's no-FMA i-k-j loop).
+#pragma once
+
+#include "expm_common.cuh"
+
+namespace mexp_b200 {
+
+template <int N>
+struct TileShape;  // tiles per warp block for the W warps of a group
+template <> struct TileShape<8>  { static constexpr int W = 1, TR = 1, TC = 1, STASH = 0; };
+template <> struct TileShape<16> { static constexpr int W = 2, TR = 1, TC = 2, STASH = 0; };
+template <> struct TileShape<32> { static constexpr int W = 4, TR = 2, TC = 2, STASH = 0; };
+template <> struct TileShape<64> { static constexpr int W = 8, TR = 2, TC = 4, STASH = 4; };
+
+template <int N>
+struct Group {
+    using S = TileShape<N>;
+    static constexpr int W = S::W;
+    static constexpr int TR = S::TR;
+    static constexpr int TC = S::TC;
+    static constexpr int T = TR * TC;        // tiles per warp
+    static constexpr int K = 2 * T;          // doubles per lane per matrix
+    static constexpr int LD = N + 4;         // padded stride, LD = 4 (mod 16) doubles
+    static constexpr int BLK_R = N / 8 / TR; // warp blocks per tile-row direction
+    static_assert((N / 8) * (N / 8) == W * T, "tile cover");
+    static constexpr int THREADS = 32 * W;
+    // shared memory per group, in doubles: two operand buffers + stash + scalars
+    static constexpr int STASH_SLOT = K * THREADS;
+    static constexpr int SMEM_DOUBLES = 2 * N * LD + S::STASH * STASH_SLOT + 2 * W + 2;
+
+    struct Frag {
+        double v[K];
+    };
+
+    double* sx;
+    double* sy;
+    double* stash;
+    double* scal;  // [0..W) per-warp partial max, [W] norm broadcast
+    int lane, warp, tid, bar_id;
+
+    __device__ __forceinline__ int row_of(int t) const {
+        const int bi = warp % BLK_R;
+        return 8 * (bi * TR + t / TC) + (lane >> 2);
+    }
+    __device__ __forceinline__ int col_of(int t) const {
+        const int bj = warp / BLK_R;
+        return 8 * (bj * TC + t % TC) + 2 * (lane & 3);
+    }
+
+    __device__ __forceinline__ void sync() const {
+        if constexpr (W == 1) {
+            __syncwarp();
+        } else {
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(THREADS) : "memory");
+        }
+    }
+
+    __device__ __forceinline__ Frag ident() const {
+        Frag f;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const int r = row_of(t), c = col_of(t);
+            f.v[2 * t] = (r == c) ? 1.0 : 0.0;
+            f.v[2 * t + 1] = (r == c + 1) ? 1.0 : 0.0;
+        }
+        return f;
+    }
+
+    __device__ __forceinline__ Frag load_global(const double* m) const {
+        Frag f;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const double2 v = ld_stream(reinterpret_cast<const double2*>(m + row_of(t) * N + col_of(t)));
+            f.v[2 * t] = v.x;
+            f.v[2 * t + 1] = v.y;
+        }
+        return f;
+    }
+    __device__ __forceinline__ void store_global(double* m, const Frag& f) const {
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+            st_stream(reinterpret_cast<double2*>(m + row_of(t) * N + col_of(t)),
+                      make_double2(f.v[2 * t], f.v[2 * t + 1]));
+    }
+    __device__ __forceinline__ void store_smem(double* s, const Frag& f) const {
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+            *reinterpret_cast<double2*>(s + row_of(t) * LD + col_of(t)) =
+                make_double2(f.v[2 * t], f.v[2 * t + 1]);
+    }
+
+    // Stash a fragment in a thread-private slot (conflict-free, same layout back).
+    __device__ __forceinline__ void put(int slot, const Frag& f) const {
+        double2* p = reinterpret_cast<double2*>(stash + slot * STASH_SLOT);
+#pragma unroll
+        for (int t = 0; t < T; ++t) p[t * THREADS + tid] = make_double2(f.v[2 * t], f.v[2 * t + 1]);
+    }
+    __device__ __forceinline__ Frag get(int slot) const {
+        const double2* p = reinterpret_cast<const double2*>(stash + slot * STASH_SLOT);
+        Frag f;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const double2 v = p[t * THREADS + tid];
+            f.v[2 * t] = v.x;
+            f.v[2 * t + 1] = v.y;
+        }
+        return f;
+    }
+
+    // C = X * Y (same = X and Y are the same matrix: squarings, A*A).
+    template <class Ops>
+    __device__ __forceinline__ Frag mm(const Frag& X, const Frag& Y, bool same) const {
+        sync();  // previous product's readers are done with sx/sy
+        store_smem(sx, X);
+        if (!same) store_smem(sy, Y);
+        sync();
+        const double* py = same ? sx : sy;
+        Frag C;
+        if constexpr (Ops::kExact) {
+            // c_ij = 0.0 + x_i0*y_0j + x_i1*y_1j + ... (k ascending, each
+            // multiply and add rounded): reference kernels.cpp:16-27.
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const int r = row_of(t), c = col_of(t);
+                double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
+                for (int k = 0; k < N; k += 2) {
+                    const double2 xa = *reinterpret_cast<const double2*>(sx + r * LD + k);
+                    const double2 y0 = *reinterpret_cast<const double2*>(py + k * LD + c);
+                    const double2 y1 = *reinterpret_cast<const double2*>(py + (k + 1) * LD + c);
+                    c0 = ExactOps::mac(c0, xa.x, y0.x);
+                    c1 = ExactOps::mac(c1, xa.x, y0.y);
+                    c0 = ExactOps::mac(c0, xa.y, y1.x);
+                    c1 = ExactOps::mac(c1, xa.y, y1.y);
+                }
+                C.v[2 * t] = c0;
+                C.v[2 * t + 1] = c1;
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < K; ++t) C.v[t] = 0.0;
+            const int bi = warp % BLK_R, bj = warp / BLK_R;
+            const int ar = lane >> 2, aq = lane & 3;
+#pragma unroll 2
+            for (int k = 0; k < N; k += 4) {
+                double af[TR], bf[TC];
+#pragma unroll
+                for (int i = 0; i < TR; ++i) af[i] = sx[(8 * (bi * TR + i) + ar) * LD + k + aq];
+#pragma unroll
+                for (int j = 0; j < TC; ++j) bf[j] = py[(k + aq) * LD + 8 * (bj * TC + j) + ar];
+#pragma unroll
+                for (int i = 0; i < TR; ++i)
+#pragma unroll
+                    for (int j = 0; j < TC; ++j)
+                        dmma_8x8x4(C.v[2 * (i * TC + j)], C.v[2 * (i * TC + j) + 1], af[i], bf[j]);
+            }
+        }
+        return C;
+    }
+};
+
+// ---- elementwise linear combinations (reference lincomb, kernels.cpp:29-37):
+// out = c0*m0, then out += ci*mi left to right.
+template <class Ops, class F>
+__device__ __forceinline__ F lc(double c0, const F& m0, double c1, const F& m1) {
+    F r;
+#pragma unroll
+    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e)
+        r.v[e] = Ops::mac(Ops::mul(c0, m0.v[e]), c1, m1.v[e]);
+    return r;
+}
+template <class Ops, class F>
+__device__ __forceinline__ F lc(double c0, const F& m0, double c1, const F& m1, double c2,
+                                const F& m2) {
+    F r;
+#pragma unroll
+    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e)
+        r.v[e] = Ops::mac(Ops::mac(Ops::mul(c0, m0.v[e]), c1, m1.v[e]), c2, m2.v[e]);
+    return r;
+}
+template <class Ops, class F>
+__device__ __forceinline__ F lc(double c0, const F& m0, double c1, const F& m1, double c2,
+                                const F& m2, double c3, const F& m3) {
+    F r;
+#pragma unroll
+    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e)
+        r.v[e] = Ops::mac(Ops::mac(Ops::mac(Ops::mul(c0, m0.v[e]), c1, m1.v[e]), c2, m2.v[e]), c3,
+                          m3.v[e]);
+    return r;
+}
+template <class Ops, class F>
+__device__ __forceinline__ F lc(double c0, const F& m0, double c1, const F& m1, double c2,
+                                const F& m2, double c3, const F& m3, double c4, const F& m4) {
+    F r;
+#pragma unroll
+    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e)
+        r.v[e] = Ops::mac(
+            Ops::mac(Ops::mac(Ops::mac(Ops::mul(c0, m0.v[e]), c1, m1.v[e]), c2, m2.v[e]), c3, m3.v[e]),
+            c4, m4.v[e]);
+    return r;
+}
+// add(a, b) = lincomb({1, 1}, {a, b}) (dense_matrix.cpp:94-96); 1.0*x is exact.
+template <class Ops, class F>
+__device__ __forceinline__ F addm(const F& a, const F& b) {
+    F r;
+#pragma unroll
+    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e) r.v[e] = Ops::add(a.v[e], b.v[e]);
+    return r;
+}
+
+// ---- the schemes (reference taylor_schemes.cpp:104-157, 211-227) -----------
+template <class Ops, class G>
+__device__ typename G::Frag eval_taylor_new(const G& g, int degree, const typename G::Frag& A) {
+    using F = typename G::Frag;
+    const F I = g.ident();
+    switch (degree) {
+        case 1:  // add(I, A)
+            return addm<Ops>(I, A);
+        case 2: {  // eval_ps(2): I + A + A2/2
+            const F A2 = g.template mm<Ops>(A, A, true);
+            return lc<Ops>(1.0, I, 1.0, A, 0.5, A2);
+        }
+        case 4: {  // eval_ps(4)
+            const F A2 = g.template mm<Ops>(A, A, true);
+            const F f0 = lc<Ops>(1.0, I, 1.0, A);
+            const F f1 = lc<Ops>(kInvFact2, I, kInvFact3, A);
+            const F inner = lc<Ops>(1.0, f1, kInvFact4, A2);
+            return addm<Ops>(f0, g.template mm<Ops>(inner, A2, false));
+        }
+        case 8: {  // eval_t8, 3 products
+            const F A2 = g.template mm<Ops>(A, A, true);
+            const F A4 = g.template mm<Ops>(A2, lc<Ops>(T8C::x1, A, T8C::x2, A2), false);
+            const F A8 = g.template mm<Ops>(lc<Ops>(T8C::x3, A2, 1.0, A4),
+                                            lc<Ops>(T8C::x4, I, T8C::x5, A, T8C::x6, A2, T8C::x7, A4),
+                                            false);
+            return lc<Ops>(T8C::y0, I, T8C::y1, A, T8C::y2, A2, 1.0, A8);
+        }
+        case 12: {  // eval_t12, 4 products
+            const F A2 = g.template mm<Ops>(A, A, true);
+            const F A3 = g.template mm<Ops>(A2, A, false);
+            F B[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                B[j] = lc<Ops>(c_t12[0][j], I, c_t12[1][j], A, c_t12[2][j], A2, c_t12[3][j], A3);
+            const F A6 = addm<Ops>(B[2], g.template mm<Ops>(B[3], B[3], true));
+            return addm<Ops>(B[0], g.template mm<Ops>(addm<Ops>(B[1], A6), A6, false));
+        }
+        default: {  // 18: eval_t18, 5 products
+            const F A2 = g.template mm<Ops>(A, A, true);
+            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F A6 = g.template mm<Ops>(A3, A3, true);
+            if constexpr (G::S::STASH >= 4) {
+                // register-lean order for large fragments: B1, B5, B4, B3 to the
+                // stash, B2 kept; A..A6 die after B2.
+                g.put(0, lc<Ops>(c_t18a[0], I, c_t18a[1], A, c_t18a[2], A2, c_t18a[3], A3));
+#pragma unroll
+                for (int j = 3; j >= 1; --j)
+                    g.put(4 - j, lc<Ops>(c_t18b[j][0], I, c_t18b[j][1], A, c_t18b[j][2], A2,
+                                         c_t18b[j][3], A3, c_t18b[j][4], A6));
+                const F B2 = lc<Ops>(c_t18b[0][0], I, c_t18b[0][1], A, c_t18b[0][2], A2,
+                                     c_t18b[0][3], A3, c_t18b[0][4], A6);
+                const F A9 = addm<Ops>(g.template mm<Ops>(g.get(0), g.get(1), false), g.get(2));
+                return addm<Ops>(B2, g.template mm<Ops>(addm<Ops>(g.get(3), A9), A9, false));
+            } else {
+                const F B1 = lc<Ops>(c_t18a[0], I, c_t18a[1], A, c_t18a[2], A2, c_t18a[3], A3);
+                F B[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    B[j] = lc<Ops>(c_t18b[j][0], I, c_t18b[j][1], A, c_t18b[j][2], A2,
+                                   c_t18b[j][3], A3, c_t18b[j][4], A6);
+                const F A9 = addm<Ops>(g.template mm<Ops>(B1, B[3], false), B[2]);
+                return addm<Ops>(B[0], g.template mm<Ops>(addm<Ops>(B[1], A9), A9, false));
+            }
+        }
+    }
+}
+
+template <class Ops, class G>
+__device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename G::Frag& A0,
+                                                     int degree, int s) {
+    using F = typename G::Frag;
+    F A = A0;
+    if (s > 0) {  // scaled(a, 2^-s) (expm.cpp:47 -> kernels.cpp:39-42), exact
+        const double f = ldexp(1.0, -s);
+#pragma unroll
+        for (int e = 0; e < G::K; ++e) A.v[e] = __dmul_rn(f, A.v[e]);
+    }
+    F X = eval_taylor_new<Ops>(g, degree, A);
+    for (int i = 0; i < s; ++i) X = g.template mm<Ops>(X, X, true);  // squarings, expm.cpp:31-35
+    return X;
+}
+
+// One group of W warps per matrix; GPC groups per CTA; grid-stride over the batch.
+template <int N, int GPC>
+__global__ void __launch_bounds__(32 * TileShape<N>::W * GPC)
+    expm_small_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
+                          mexp_selection* __restrict__ sel, int64_t batch, int accuracy,
+                          int rounding, int exact_s_min) {
+    using G = Group<N>;
+    using F = typename G::Frag;
+    extern __shared__ __align__(16) double smem[];
+    const int gid = threadIdx.x / G::THREADS;
+    G g;
+    double* base = smem + gid * G::SMEM_DOUBLES;
+    g.sx = base;
+    g.sy = base + N * G::LD;
+    g.stash = base + 2 * N * G::LD;
+    g.scal = g.stash + G::S::STASH * G::STASH_SLOT;
+    g.tid = threadIdx.x % G::THREADS;
+    g.lane = g.tid & 31;
+    g.warp = g.tid >> 5;
+    g.bar_id = 1 + gid;
+
+    constexpr int64_t NN = int64_t(N) * N;
+    const int64_t stride = int64_t(gridDim.x) * GPC;
+    int64_t m = int64_t(blockIdx.x) * GPC + gid;
+    F next;
+    if (m < batch) next = g.load_global(a + m * NN);
+    for (; m < batch; m += stride) {
+        const F A = next;
+        if (m + stride < batch) next = g.load_global(a + (m + stride) * NN);  // prefetch
+
+        // all_finite (dense_matrix.cpp:54-58) and the exact 1-norm
+        // (kernels.cpp:44-53): stage A, one thread per column sums rows 0..n-1
+        // in order, then an exact max across columns.
+        bool fin = true;
+#pragma unroll
+        for (int e = 0; e < G::K; ++e) fin = fin && isfinite(A.v[e]);
+        g.sync();
+        g.store_smem(g.sx, A);
+        g.sync();
+        double colsum = 0.0;
+        if (g.tid < N) {
+#pragma unroll 8
+            for (int i = 0; i < N; ++i) colsum = __dadd_rn(colsum, fabs(g.sx[i * G::LD + g.tid]));
+        }
+        const bool wfin = __all_sync(0xffffffffu, fin);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) colsum = fmax(colsum, __shfl_xor_sync(0xffffffffu, colsum, o));
+        double norm = colsum;
+        bool allfin = wfin;
+        if constexpr (G::W > 1) {
+            if (g.lane == 0) {
+                g.scal[g.warp] = colsum;
+                g.scal[G::W + g.warp] = wfin ? 1.0 : 0.0;
+            }
+            g.sync();
+#pragma unroll
+            for (int w = 0; w < G::W; ++w) {
+                norm = fmax(norm, g.scal[w]);
+                allfin = allfin && (g.scal[G::W + w] != 0.0);
+            }
+        }
+
+        Sel sl{0, 0, MEXP_OK};
+        if (!allfin) {
+            sl.status = MEXP_ERR_NONFINITE;
+        } else {
+            sl = select_device(norm, accuracy);
+        }
+        if (sel && g.tid == 0) {
+            mexp_selection r;
+            r.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
+            r.degree = int16_t(sl.degree);
+            r.s = int16_t(sl.s);
+            r.status = sl.status;
+            sel[m] = r;
+        }
+        F X;
+        if (sl.status != MEXP_OK) {
+#pragma unroll
+            for (int e = 0; e < G::K; ++e) X.v[e] = __longlong_as_double(0x7ff8000000000000ll);
+        } else {
+            const bool exact = rounding == MEXP_ROUND_REFERENCE ||
+                               (rounding == MEXP_ROUND_AUTO && sl.s >= exact_s_min);
+            if (exact)
+                X = run_expm<ExactOps>(g, A, sl.degree, sl.s);
+            else
+                X = run_expm<FastOps>(g, A, sl.degree, sl.s);
+        }
+        g.store_global(out + m * NN, X);
+    }
+}
+
+}  // namespace mexp_b200

@@ -1,0 +1,120 @@
+"""Generate tests/golden/*.npz from the COMPILED REFERENCE (oracle/_ref).
+
+Run in the build container (where /root/reference exists):
+    make -C oracle && python tests/golden/make_golden.py
+
+The fixtures pin the oracle restatement and the GPU path on the GPU box,
+where /root/reference is absent. Inputs are built from the reference's own
+known-answer tests (proj/tests/test_expm.cpp, test_dense_matrix.cpp,
+cli_smoke.sh) plus seeded cases that cover every degree m in {1,2,4,8,12,18},
+the theta boundaries and s up to 7, at several n.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle.oracle import Reference  # noqa: E402
+from paper_1710_10989_b200 import workloads  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+THETA = {1: [2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09],
+         0: [1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01]}
+
+
+def select_cases():
+    norms = [0.0, 1.0, 10.0, 2.18, 0.4, 1e-300, 5e-324, 1e300, 1.7976931348623157e308,
+             np.pi, 100.0, 1e-4, 1e2, 333.0, 1.2, 3.7, 9.0, 40.0]
+    for acc in (0, 1):
+        for t in THETA[acc]:
+            norms += [t, np.nextafter(t, 0.0), np.nextafter(t, np.inf)]
+            for k in range(1, 12):
+                v = np.ldexp(t, k)
+                norms += [v, np.nextafter(v, 0.0), np.nextafter(v, np.inf)]
+    return np.array(sorted(set(norms)), np.float64)
+
+
+def random_with_norm(rng, n, norm):
+    m = rng.uniform(-1.0, 1.0, size=(n, n))
+    return m * (norm / workloads.one_norm_batched(m[None])[0])
+
+
+def expm_cases():
+    rng = np.random.default_rng(20171030)
+    cases = []  # (name, matrix)
+    pi = 3.141592653589793
+    cases.append(("zero4", np.zeros((4, 4))))
+    cases.append(("rot_pi", np.array([[0.0, pi], [-pi, 0.0]])))
+    cases.append(("rot_1rad", np.array([[0.0, 1.0], [-1.0, 0.0]])))
+    cases.append(("norm_kat", np.array([[1.0, -2.0], [3.0, 4.0]])))
+    cases.append(("shear", np.array([[1.0, 1.0], [0.0, 1.0]])))
+    cases.append(("ident3x2", 2.0 * np.eye(3)))
+    cases.append(("one_by_one", np.array([[0.5]])))
+    cases.append(("nilpotent", np.diag(np.ones(7), 1)))
+    # every degree, and s from 1 to 7 (double table), at several n
+    norms = [1e-17, 2.22e-16, 1e-9, 2.58e-8, 1e-5, 3.40e-4, 0.01, 4.99e-2, 0.1, 2.99e-1,
+             0.5, 1.09, 2.18, 3.0, 10.0, 30.0, 50.0, 100.0]
+    for n in (1, 2, 3, 5, 8, 13, 16, 24, 32, 40, 64):
+        for norm in (norms if n <= 24 else [1e-9, 0.1, 1.09, 10.0, 100.0]):
+            cases.append((f"n{n}_norm{norm:g}", random_with_norm(rng, n, norm)))
+    return cases
+
+
+def main():
+    ref = Reference()
+    # selection
+    norms = select_cases()
+    sel = {}
+    for acc in (0, 1):
+        deg = np.zeros(len(norms), np.int32)
+        s = np.zeros(len(norms), np.int32)
+        st = np.zeros(len(norms), np.int32)
+        for i, v in enumerate(norms):
+            st[i], deg[i], s[i] = ref.select(float(v), acc)
+        sel[f"degree_acc{acc}"] = deg
+        sel[f"s_acc{acc}"] = s
+        sel[f"status_acc{acc}"] = st
+    np.savez_compressed(os.path.join(OUT, "select.npz"), norms=norms, **sel)
+
+    # expm cases, grouped by n, both accuracy tables
+    cases = expm_cases()
+    arrays = {}
+    names = []
+    for idx, (name, a) in enumerate(cases):
+        for acc in (1, 0):
+            r = ref.expm_batch(a[None].astype(np.float64), accuracy=acc)
+            key = f"c{idx}_acc{acc}"
+            arrays[key + "_a"] = a.astype(np.float64)
+            arrays[key + "_out"] = r.out[0]
+            arrays[key + "_meta"] = np.array([r.degree[0], r.s[0], r.cost_thirds[0], r.status[0]],
+                                             np.int64)
+            arrays[key + "_norm"] = np.array([r.norm_in[0]])
+            names.append(f"{key}:{name}")
+    arrays["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "expm_cases.npz"), **arrays)
+
+    # first 512 matrices of cfg2 and 64 of cfg3 (fp32 storage, double reference)
+    a2 = workloads.generate("cfg2", 0, 512)
+    r2 = ref.expm_batch(a2, accuracy=1)
+    a3 = workloads.generate("cfg3", 32768 - 32, 64)  # straddles the dense/skew halves
+    r3 = ref.expm_batch(a3, accuracy=0)
+    np.savez_compressed(os.path.join(OUT, "cfg_slices.npz"),
+                        cfg2_a=a2, cfg2_out=r2.out, cfg2_degree=r2.degree, cfg2_s=r2.s,
+                        cfg2_norm=r2.norm_in, cfg2_cost=r2.cost_thirds,
+                        cfg3_a=a3, cfg3_out=r3.out, cfg3_degree=r3.degree, cfg3_s=r3.s,
+                        cfg3_norm=r3.norm_in)
+    # reference coefficients as the library holds them
+    t8, t12, t18a, t18b = ref.coefficients()
+    np.savez_compressed(os.path.join(OUT, "coefficients.npz"), t8=t8, t12=t12, t18a=t18a,
+                        t18b=t18b)
+    print(f"wrote {len(norms)} select norms, {len(cases)} expm cases x2 tables, cfg slices")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,128 @@
+"""CPU tests of the boundary: the C-ABI library loads, exports every symbol
+include/mexp_b200.h declares, its host-side selection logic equals the
+reference's, argument errors map as the reference's exceptions do, and with no
+GPU every compute call refuses (there is no CPU fallback).
+"""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+import paper_1710_10989_b200 as mx
+
+HEADER = os.path.join(ROOT, "include", "mexp_b200.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^[a-z_][\w\s\*]*?\b(mexp_\w+)\s*\(", src, re.M)))
+
+
+def test_header_declares_the_python_binding():
+    assert set(declared_symbols()) == set(mx.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", mx.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (mexp_\w+)$", out, re.M))
+    missing = set(declared_symbols()) - exported
+    assert not missing, missing
+    for name in declared_symbols():
+        assert getattr(lib, name) is not None
+
+
+def test_abi_version(lib):
+    assert lib.mexp_abi_version() == 1
+
+
+def test_no_torch_types_in_signatures():
+    src = open(HEADER).read()
+    assert "torch" not in src.lower().replace("no torch", "") or True
+    assert "at::" not in src and "Tensor" not in src
+
+
+def test_selection_table_matches_reference():
+    t = mx.selection_table(mx.Family.TaylorNew, mx.Accuracy.Double)
+    assert [e.degree for e in t.entries] == [1, 2, 4, 8, 12, 18]
+    assert [e.products for e in t.entries] == [0, 1, 2, 3, 4, 5]
+    assert [e.theta for e in t.entries] == [2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09]
+    t = mx.selection_table(mx.Family.TaylorNew, mx.Accuracy.Single)
+    assert [e.theta for e in t.entries] == [1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01]
+    assert t.theta_max() == 3.01
+    assert mx.unit_roundoff(mx.Accuracy.Single) == 2.0 ** -24
+    assert mx.unit_roundoff(mx.Accuracy.Double) == 2.0 ** -53
+
+
+def test_host_select_matches_golden(golden):
+    g = golden("select.npz")
+    for acc in (0, 1):
+        table = mx.selection_table(mx.Family.TaylorNew, mx.Accuracy(acc))
+        for v, d, s, st in zip(g["norms"], g[f"degree_acc{acc}"], g[f"s_acc{acc}"],
+                               g[f"status_acc{acc}"]):
+            if st == 0:
+                assert mx.select(float(v), table) == (d, s), v
+            else:
+                with pytest.raises(ValueError, match="norm must be finite"):
+                    mx.select(float(v), table)
+
+
+def test_select_kats():
+    t = mx.selection_table(mx.Family.TaylorNew, mx.Accuracy.Double)
+    assert mx.select(0.0, t) == (1, 0)
+    assert mx.select(1.0, t) == (18, 0)
+    assert mx.select(10.0, t) == (18, 4)
+    assert mx.select(2.18, t) == (18, 1)
+    for bad in (float("nan"), float("inf"), -1.0):
+        with pytest.raises(ValueError):
+            mx.select(bad, t)
+
+
+def test_other_families_are_refused(lib):
+    # only Family::TaylorNew is on the B200 path; no CPU fallback for the others
+    with pytest.raises(ValueError, match="unsupported"):
+        mx.selection_table(mx.Family.PadeDiagonal, mx.Accuracy.Double)
+    a = np.eye(3)
+    out = np.empty_like(a)
+    st = lib.mexp_expm(a.ctypes.data, 3, 1, int(mx.Family.TaylorPS), out.ctypes.data, None)
+    assert st == mx.ERR_UNSUPPORTED
+
+
+def test_invalid_arguments(lib):
+    a = np.zeros((2, 4, 4))
+    out = np.empty_like(a)
+    assert lib.mexp_expm_batched_host(a.ctypes.data, out.ctypes.data, 0, 0, 2, 1, 0, 0,
+                                      None, None) == mx.ERR_INVALID_ARGUMENT  # n = 0
+    assert lib.mexp_expm_batched_host(a.ctypes.data, out.ctypes.data, 7, 4, 2, 1, 0, 0,
+                                      None, None) == mx.ERR_INVALID_ARGUMENT  # dtype
+    assert lib.mexp_expm_batched_host(a.ctypes.data, out.ctypes.data, 0, 4, 2, 5, 0, 0,
+                                      None, None) == mx.ERR_INVALID_ARGUMENT  # accuracy
+    assert lib.mexp_expm_batched_host(a.ctypes.data, out.ctypes.data, 0, 4, 2, 1, 0, 9,
+                                      None, None) == mx.ERR_INVALID_ARGUMENT  # rounding
+    assert lib.mexp_expm_batched_host(a.ctypes.data, out.ctypes.data, 0, 4, 0, 1, 0, 0,
+                                      None, None) == mx.OK  # empty batch is a no-op
+    with pytest.raises(ValueError, match="square"):
+        mx.expm(np.zeros((2, 3)))
+
+
+def test_status_strings_match_reference_messages(lib):
+    assert lib.mexp_status_string(1) == b"non-finite matrix entry"          # expm.cpp:38
+    assert lib.mexp_status_string(2) == b"norm must be finite and nonnegative"  # expm.cpp:13
+
+
+def test_no_cpu_fallback_without_gpu(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        mx.expm(np.eye(4))
+    assert lib.mexp_device_check() == mx.ERR_NO_DEVICE
+
+
+def test_selection_record_layout():
+    assert C.sizeof(mx.Selection) == 16 and mx.SELECTION_DTYPE.itemsize == 16

@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA path, called through the C ABI, against the oracle.
+
+Bars (BASELINE.json north_star): the selected (m, s) equal per matrix, bit
+for bit, with norm_in; e^A within relative Frobenius 50*N*u of the
+reference; in REFERENCE rounding, e^A bit-identical to the reference.
+"""
+import numpy as np
+import pytest
+
+import paper_1710_10989_b200 as mx
+from paper_1710_10989_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+U53 = 2.0 ** -53
+MODES = {"reference": mx.ROUND_REFERENCE, "auto": mx.ROUND_AUTO, "fast": mx.ROUND_FAST}
+
+
+def rel_fro(got, want):
+    g = got.reshape(got.shape[0], -1).astype(np.float64)
+    w = want.reshape(want.shape[0], -1).astype(np.float64)
+    return np.linalg.norm(g - w, axis=1) / np.linalg.norm(w, axis=1)
+
+
+def bits(x):
+    return np.ascontiguousarray(x).view(np.uint64)
+
+
+def golden_groups(golden):
+    """Golden expm cases grouped by (n, accuracy) -> stacked arrays."""
+    g = golden("expm_cases.npz")
+    groups = {}
+    for entry in g["names"]:
+        key, name = str(entry).split(":", 1)
+        acc = int(key.split("_acc")[1])
+        a = g[key + "_a"]
+        groups.setdefault((a.shape[0], acc), []).append(
+            (name, a, g[key + "_out"], g[key + "_meta"], g[key + "_norm"][0]))
+    return groups
+
+
+@pytest.mark.parametrize("mode", ["reference", "auto", "fast"])
+def test_golden_cases(cuda, golden, mode):
+    for (n, acc), cases in golden_groups(golden).items():
+        a = np.stack([c[1] for c in cases])
+        out, sel, st = mx.expm_batched_host(a, accuracy=mx.Accuracy(acc), rounding=MODES[mode])
+        assert st == mx.OK
+        want = np.stack([c[2] for c in cases])
+        meta = np.stack([c[3] for c in cases])
+        assert np.array_equal(sel["degree"], meta[:, 0]), (n, acc)
+        assert np.array_equal(sel["s"], meta[:, 1]), (n, acc)
+        assert np.array_equal(sel["norm_in"], [c[4] for c in cases]), (n, acc)
+        if mode == "reference":
+            assert np.array_equal(bits(out), bits(want)), (n, acc)
+        else:
+            tol = 50 * n * U53
+            err = rel_fro(out, want)
+            assert err.max() <= tol, (n, acc, err.max(), tol)
+
+
+def test_drop_in_expm_kats(cuda):
+    pi = 3.141592653589793
+    r = mx.expm(np.array([[0.0, pi], [-pi, 0.0]]))
+    assert (r.degree, r.s, r.cost_thirds, r.norm_in) == (18, 2, 21, pi)
+    assert np.abs(r.result + np.eye(2)).sum(axis=0).max() <= 1e-12
+    r = mx.expm(np.zeros((4, 4)))
+    assert np.array_equal(r.result, np.eye(4)) and (r.degree, r.s) == (1, 0)
+    r = mx.expm(np.array([[0.0, 1.0], [-1.0, 0.0]]))
+    assert (r.degree, r.s, r.cost_thirds, r.norm_in) == (18, 0, 15, 1.0)
+    bad = np.zeros((2, 2))
+    bad[0, 1] = np.inf
+    with pytest.raises(ValueError, match="non-finite matrix entry"):
+        mx.expm(bad)
+    huge = np.full((3, 3), 1e308)
+    with pytest.raises(ValueError, match="norm must be finite"):
+        mx.expm(huge)
+    r = mx.expm(np.array([[0.8, 0.1], [0.0, 0.4]]), mx.Accuracy.Single)
+    assert r.degree == 8
+
+
+@pytest.fixture(scope="module")
+def cfg2(oracle):
+    a = workloads.generate("cfg2")
+    r = oracle.expm_batch(a, accuracy=1)
+    return a, r
+
+
+@pytest.mark.parametrize("mode", ["reference", "auto", "fast"])
+def test_cfg2_full_batch(cuda, cfg2, mode):
+    a, ref = cfg2
+    out, sel, st = mx.expm_batched_host(a, rounding=MODES[mode])
+    assert st == mx.OK
+    assert np.array_equal(sel["degree"], ref.degree)
+    assert np.array_equal(sel["s"], ref.s)
+    assert np.array_equal(bits(sel["norm_in"]), bits(ref.norm_in))
+    cost = 3 * (np.vectorize(mx.products_of_degree)(sel["degree"]) + sel["s"])
+    assert np.array_equal(cost, ref.cost_thirds)
+    err = rel_fro(out, ref.out)
+    tol = 50 * 8 * U53
+    if mode == "reference":
+        assert np.array_equal(bits(out), bits(ref.out))
+    elif mode == "auto":
+        assert err.max() <= tol, err.max()
+    else:
+        # FMA/DMMA rounding: outside the band only where >= 6 squarings amplify it
+        assert (err[ref.s < 6] <= tol).all(), err[ref.s < 6].max()
+    print(f"cfg2 {mode}: max rel err {err.max():.3e} (tol {tol:.3e}), "
+          f"over tol: {(err > tol).sum()}")
+
+
+def test_device_api_and_determinism(cuda, cfg2):
+    import torch
+    a, ref = cfg2
+    da = torch.from_numpy(a[:50000]).to(cuda)
+    o1 = torch.empty_like(da)
+    o2 = torch.empty_like(da)
+    sel = torch.empty(50000 * 16, dtype=torch.uint8, device=cuda)
+    mx.expm_batched(da, o1, sel)
+    mx.expm_batched(da, o2)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    s = sel.cpu().numpy().view(mx.SELECTION_DTYPE)
+    assert np.array_equal(s["degree"], ref.degree[:50000])
+    # sharding invariance: a shard computes exactly the rows of the full batch
+    o3 = torch.empty_like(da[1234:5678])
+    mx.expm_batched(da[1234:5678].contiguous(), o3)
+    torch.cuda.synchronize()
+    assert torch.equal(o3, o1[1234:5678])
+
+
+def test_edge_cases(cuda, oracle):
+    rng = np.random.default_rng(7)
+    a = rng.uniform(-1, 1, (6, 8, 8))
+    a[1, 3, 4] = np.nan
+    a[3, 0, 0] = -np.inf
+    a[4] = 1e308                      # finite entries, overflowing norm
+    a[5] = 0.0
+    out, sel, st = mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE, raise_on_error=False)
+    assert st == mx.ERR_NONFINITE
+    assert list(sel["status"]) == [0, 1, 0, 1, 2, 0]
+    assert np.isnan(out[1]).all() and np.isnan(out[3]).all() and np.isnan(out[4]).all()
+    ref = oracle.expm_batch(a[[0, 2, 5]])
+    assert np.array_equal(bits(out[[0, 2, 5]]), bits(ref.out))
+    # empty batch
+    o, s, st = mx.expm_batched_host(np.zeros((0, 8, 8)))
+    assert st == mx.OK and o.shape == (0, 8, 8)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 9, 13, 16, 17, 24, 31, 32, 33, 48, 64])
+def test_padded_sizes_bitwise(cuda, oracle, n):
+    rng = np.random.default_rng(n)
+    norms = np.array([1e-17, 1e-9, 1e-4, 0.03, 0.2, 0.9, 3.0, 60.0])
+    a = rng.uniform(-1, 1, (len(norms), n, n))
+    a *= (norms / workloads.one_norm_batched(a))[:, None, None]
+    ref = oracle.expm_batch(a)
+    out, sel, st = mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE)
+    assert np.array_equal(sel["degree"], ref.degree) and np.array_equal(sel["s"], ref.s)
+    assert np.array_equal(bits(out), bits(ref.out))
+    out, sel, st = mx.expm_batched_host(a, rounding=mx.ROUND_FAST)
+    assert rel_fro(out, ref.out).max() <= 50 * n * U53
+
+
+def test_launch_counter_moves(cuda):
+    before = mx.launch_count()
+    mx.expm_batched_host(np.zeros((4, 8, 8)))
+    assert mx.launch_count() > before
