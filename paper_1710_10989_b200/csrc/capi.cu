@@ -14,6 +14,7 @@
 
 #include "expm_common.cuh"
 #include "expm_large.cuh"
+#include "expm_n8.cuh"
 #include "expm_small.cuh"
 #include "expm_small_f32.cuh"
 
@@ -52,9 +53,17 @@ bool valid_args(int dtype, int n, int64_t batch, int accuracy, int family, int r
 }
 
 // Rounding threshold of the AUTO policy: matrices with s >= this run the
-// reference-exact arithmetic (SURVEY.md key finding 3: FMA-rounded results
-// leave the 50*n*u band only when 6 or more squarings amplify them).
-constexpr int kExactSMin = 6;
+// reference-exact arithmetic. Each squaring roughly doubles the relative
+// difference between two roundings of T_m, while the tolerance 50*n*u grows
+// with n; FMA-rounded results leave the band for n = 8 only from s = 6 on
+// (SURVEY.md key finding 3) and for n = 1 from s = 4 on (golden cases), so
+// the threshold is 3 + floor(log2 n), taken on the caller's n before padding.
+int exact_s_min(int n) {
+    if (n < 8) return 0;  // tiny n: 50*n*u is too tight for any other rounding
+    int l = 0;
+    while ((2 << l) <= n) ++l;
+    return 3 + l;
+}
 
 template <class T>
 __global__ void pad_kernel(const T* __restrict__ src, T* __restrict__ dst, int n, int np,
@@ -91,7 +100,7 @@ int num_sms() {
 
 template <int N, int GPC>
 int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
-                     int accuracy, int rounding, cudaStream_t st) {
+                     int accuracy, int rounding, int smin, cudaStream_t st) {
     using G = Group<N>;
     auto kern = expm_small_f64_kernel<N, GPC>;
     const size_t smem = size_t(G::SMEM_DOUBLES) * GPC * sizeof(double);
@@ -105,19 +114,37 @@ int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t 
     const int64_t cap = int64_t(blocks_per_sm) * num_sms();
     const int grid = int(want < cap ? want : cap);
     if (grid == 0) return MEXP_OK;
-    kern<<<grid, 32 * G::W * GPC, smem, st>>>(a, out, sel, batch, accuracy, rounding, kExactSMin);
+    kern<<<grid, 32 * G::W * GPC, smem, st>>>(a, out, sel, batch, accuracy, rounding, smin);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    MEXP_CUDA(cudaGetLastError());
+    return MEXP_OK;
+}
+
+int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
+                  int accuracy, int rounding, int smin, cudaStream_t st) {
+    static int blocks_per_sm = [] {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, expm8_f64_kernel, 32 * kN8WarpsPerBlock, 0);
+        return b > 0 ? b : 1;
+    }();
+    const int64_t want = (batch + kN8WarpsPerBlock - 1) / kN8WarpsPerBlock;
+    const int64_t cap = int64_t(blocks_per_sm) * num_sms();
+    const int grid = int(want < cap ? want : cap);
+    if (grid == 0) return MEXP_OK;
+    expm8_f64_kernel<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy,
+                                                              rounding, smin);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());
     return MEXP_OK;
 }
 
 int run_small_f64(const double* a, double* out, mexp_selection* sel, int np, int64_t batch,
-                  int accuracy, int rounding, cudaStream_t st) {
+                  int accuracy, int rounding, int smin, cudaStream_t st) {
     switch (np) {
-        case 8: return launch_small_f64<8, 8>(a, out, sel, batch, accuracy, rounding, st);
-        case 16: return launch_small_f64<16, 4>(a, out, sel, batch, accuracy, rounding, st);
-        case 32: return launch_small_f64<32, 2>(a, out, sel, batch, accuracy, rounding, st);
-        case 64: return launch_small_f64<64, 1>(a, out, sel, batch, accuracy, rounding, st);
+        case 8: return launch_n8_f64(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 16: return launch_small_f64<16, 4>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 32: return launch_small_f64<32, 2>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 64: return launch_small_f64<64, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
     }
     return MEXP_ERR_UNSUPPORTED;
 }
@@ -157,7 +184,7 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
     int r;
     if (dtype == MEXP_F64) {
         r = run_small_f64(static_cast<const double*>(src), static_cast<double*>(dst), d_sel, np,
-                          batch, accuracy, rounding, st);
+                          batch, accuracy, rounding, exact_s_min(n), st);
     } else {
         r = run_small_f32(static_cast<const float*>(src), static_cast<float*>(dst), d_sel, np,
                           batch, accuracy, st, &g_launches);

@@ -16,7 +16,7 @@ namespace mexp_b200 {
 // reference's decimal literals, so they round to the identical doubles.
 // ---------------------------------------------------------------------------
 constexpr int kNumEntries = 6;
-__constant__ double c_theta[2][kNumEntries] = {
+__device__ constexpr double c_theta[2][kNumEntries] = {
     {1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01},      // Accuracy::Single
     {2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09},  // Accuracy::Double
 };
@@ -49,7 +49,7 @@ struct T8C {
 
 // T12 (paper eq. for the 4-product scheme; reference taylor_schemes.cpp:62-71):
 // kT12[i][j] multiplies {I, A, A2, A3}[i] in B_{j+1}.
-__constant__ double c_t12[4][4] = {
+__device__ constexpr double c_t12[4][4] = {
     {9.0198e-16, 5.31597895759871264183, 0.18188869982170434744, -2.0861320e-13},
     {0.46932117595418237389, 1.19926790417132231573, 0.05502798439925399070,
      -0.13181061013830184015},
@@ -60,9 +60,9 @@ __constant__ double c_t12[4][4] = {
 };
 // T18 (reference taylor_schemes.cpp:73-85): c_t18a[i] multiplies {I,A,A2,A3}[i]
 // in B1; c_t18b[j][r] multiplies {I,A,A2,A3,A6}[r] in B_{j+2}.
-__constant__ double c_t18a[4] = {0.0, -0.100365581030144620, -0.0080292464824115696,
+__device__ constexpr double c_t18a[4] = {0.0, -0.100365581030144620, -0.0080292464824115696,
                                  -0.0008921384980457299};
-__constant__ double c_t18b[4][5] = {
+__device__ constexpr double c_t18b[4][5] = {
     {0.0, 0.39784974949964507614, 1.36783778460411719922, 0.49828962252538267755,
      -0.0006378981945947233},
     {-10.967639605296206259, 1.68015813878906197182, 0.05717798464788655127,
@@ -88,27 +88,44 @@ struct Sel {
     int status;
 };
 
+__device__ __forceinline__ double theta_of(int accuracy, int e) {
+    double t = c_theta[0][0];
+#pragma unroll
+    for (int k = 0; k < kNumEntries; ++k)
+        if (k == e) t = accuracy ? c_theta[1][k] : c_theta[0][k];
+    return t;
+}
+
 __device__ __forceinline__ Sel select_device(double norm, int accuracy) {
-    const double* th = c_theta[accuracy];
     Sel r{0, 0, MEXP_OK};
     if (!isfinite(norm) || norm < 0.0) {
         r.status = MEXP_ERR_NORM_NONFINITE;
         return r;
     }
-    if (norm <= th[kNumEntries - 1]) {
+    const double tmax = theta_of(accuracy, kNumEntries - 1);
+    if (norm <= tmax) {
         int best = -1;
 #pragma unroll
-        for (int e = 0; e < kNumEntries; ++e) {
-            if (th[e] < norm) continue;
-            // products and degrees both ascend with e, so the first admissible
-            // entry is the reference's (products, degree) minimum
-            if (best < 0) best = e;
+        for (int e = kNumEntries - 1; e >= 0; --e) {
+            // skip on theta < norm (expm.cpp:17); products and degrees both
+            // ascend with e, so the first admissible entry is the reference's
+            // (products, degree) minimum
+            if (!(theta_of(accuracy, e) < norm)) best = e;
         }
         r.degree = degree_of(best);
         return r;
     }
+    // least s with ldexp(norm, -s) <= theta_18 (expm.cpp:27). For s >= 1 the
+    // loop only runs while norm * 2^-(s-1) > theta_18, so norm * 2^-s is a
+    // normal number and `ldexp(norm, -s) > t` <=> `norm > t * 2^s` exactly;
+    // doubling t is exact (it can only overflow to +inf, which ends the loop
+    // as ldexp would).
     int s = 0;
-    while (ldexp(norm, -s) > th[kNumEntries - 1]) ++s;
+    double t = tmax;
+    while (norm > t) {
+        t *= 2.0;
+        ++s;
+    }
     r.degree = 18;
     r.s = s;
     return r;

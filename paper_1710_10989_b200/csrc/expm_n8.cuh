@@ -1,0 +1,226 @@
+// Batched 8x8 fp64 expm (BASELINE cfg2): one warp per matrix, no tile of the
+// matrix ever leaves the warp except one 512-byte shared-memory transpose per
+// product.
+//
+// Lane l = 4r + q holds M[r][2q], M[r][2q+1] of every matrix variable M --
+// the accumulator layout of the FP64 tensor-core MMA m8n8k4 (DMMA), and the
+// layout a coalesced 16-byte load of a row-major 8x8 block gives directly.
+//
+// Product C = X*Y as two DMMAs with the summation index permuted: DMMA #1
+// sums k in {0,2,4,6}, DMMA #2 k in {1,3,5,7}. Then the A operand lane l
+// needs is X[r][2q] (#1) and X[r][2q+1] (#2) -- its own registers -- and the
+// B operand is Y[2q][r], Y[2q+1][r]: Y transposed, obtained by one 16-byte
+// store and two 8-byte loads per lane through a 512-byte tile whose 16-byte
+// unit (i, c) (row i, column pair c) sits at slot 8c + (i ^ c). That swizzle
+// makes the store (4 wavefronts), the transposed loads (2 + 2), the row
+// loads of the exact path and the column reads of the 1-norm conflict-free.
+//
+// Reference-exact rounding (ExactOps) computes c_rj = 0.0 + x_r0*y_0j + ... +
+// x_r7*y_7j with separately rounded DMUL/DADD in k order, as the reference's
+// i-k-j loop does (kernels.cpp:16-27), from the same tile.
+#pragma once
+
+#include "expm_small.cuh"
+
+namespace mexp_b200 {
+
+// Byte offset of the 16-byte unit (i, c) = (M[i][2c], M[i][2c+1]) in a
+// warp's 512-byte tile. The slot
+//   8*(i>>1) | 4*((i&1) ^ (i>>2)) | 2*(((c>>1) ^ (i>>1)) & 1) | (c&1)
+// is a bijection onto 32 slots that is bank-conflict-free per access phase
+// (8 lanes for 16-byte, 16 lanes for 8-byte accesses) for: the lane stores
+// (r, q); the transposed 8-byte loads (2q, r) and (2q+1, r); the row loads
+// (r, c) and column-pair loads (k, q) of the exact product; and the column
+// reads of the 1-norm (verified exhaustively in tests/test_layouts.py).
+// Note unit8(i, c) == unit8(i, 0) ^ (c << 4).
+__host__ __device__ __forceinline__ constexpr uint32_t unit8(int i, int c) {
+    return uint32_t(((i >> 1) << 3) | (((i & 1) ^ (i >> 2)) << 2) |
+                    ((((c >> 1) ^ (i >> 1)) & 1) << 1) | (c & 1))
+           << 4;
+}
+
+struct Group8 {
+    struct S {
+        static constexpr int STASH = 0;
+    };
+    static constexpr int K = 2;
+    struct Frag {
+        using T = double;
+        static constexpr int kCount = 2;
+        double v[2];
+    };
+
+    char* tile;      // this warp's tiles: [0, 512) X / fast, [512, 1024) Y (exact)
+    uint32_t st;     // unit (r, q)
+    uint32_t ld0;    // element (2q,   r)
+    uint32_t ld1;    // element (2q+1, r)
+    uint32_t rowb;   // unit (r, 0)
+    uint32_t qx;     // q << 4: unit (k, q) = unit8(k, 0) ^ qx
+    int r, q;
+    double fscale;   // 2^-s, applied to the staged (unscaled) A by sq_first
+
+    __device__ __forceinline__ void init(char* warp_tile, int lane) {
+        tile = warp_tile;
+        r = lane >> 2;
+        q = lane & 3;
+        st = unit8(r, q);
+        ld0 = unit8(2 * q, r >> 1) + ((r & 1) << 3);
+        ld1 = unit8(2 * q + 1, r >> 1) + ((r & 1) << 3);
+        rowb = unit8(r, 0);
+        qx = uint32_t(q) << 4;
+        fscale = 1.0;
+    }
+
+    __device__ __forceinline__ Frag ident() const {
+        Frag f;
+        f.v[0] = (r == 2 * q) ? 1.0 : 0.0;
+        f.v[1] = (r == 2 * q + 1) ? 1.0 : 0.0;
+        return f;
+    }
+
+    template <class Ops>
+    __device__ __forceinline__ Frag mm(const Frag& X, const Frag& Y, bool same) const {
+        return mm_impl<Ops>(X, Y, same, nullptr);
+    }
+    template <class Ops>
+    __device__ __forceinline__ Frag mm_add(const Frag& X, const Frag& Y, bool same,
+                                           const Frag& B) const {
+        if constexpr (Ops::kExact) {
+            Frag P = mm_impl<Ops>(X, Y, same, nullptr);
+            P.v[0] = Ops::add(P.v[0], B.v[0]);
+            P.v[1] = Ops::add(P.v[1], B.v[1]);
+            return P;
+        } else {
+            return mm_impl<Ops>(X, Y, same, &B);
+        }
+    }
+    // A2 = A*A for the scaled A, right after the 1-norm staged the UNSCALED A
+    // in the tile (fast path): the transposed operand is read from there and
+    // scaled on load (exact: a power of two).
+    template <class Ops>
+    __device__ __forceinline__ Frag sq_first(const Frag& A) const {
+        if constexpr (Ops::kExact) {
+            return mm_impl<Ops>(A, A, true, nullptr);
+        } else {
+            const double y0 = fscale * *reinterpret_cast<const double*>(tile + ld0);
+            const double y1 = fscale * *reinterpret_cast<const double*>(tile + ld1);
+            Frag C;
+            C.v[0] = C.v[1] = 0.0;
+            dmma_8x8x4(C.v[0], C.v[1], A.v[0], y0);
+            dmma_8x8x4(C.v[0], C.v[1], A.v[1], y1);
+            return C;
+        }
+    }
+
+    template <class Ops>
+    __device__ __forceinline__ Frag mm_impl(const Frag& X, const Frag& Y, bool same,
+                                            const Frag* init) const {
+        Frag C;
+        __syncwarp();  // readers of the previous product are done with the tile
+        if constexpr (Ops::kExact) {
+            *reinterpret_cast<double2*>(tile + st) = make_double2(X.v[0], X.v[1]);
+            if (!same) *reinterpret_cast<double2*>(tile + 512 + st) = make_double2(Y.v[0], Y.v[1]);
+            __syncwarp();
+            const char* ty = same ? tile : tile + 512;
+            double x[8];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double2 v = *reinterpret_cast<const double2*>(tile + (rowb ^ (c << 4)));
+                x[2 * c] = v.x;
+                x[2 * c + 1] = v.y;
+            }
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double2 y = *reinterpret_cast<const double2*>(ty + (unit8(k, 0) ^ qx));
+                c0 = ExactOps::mac(c0, x[k], y.x);
+                c1 = ExactOps::mac(c1, x[k], y.y);
+            }
+            C.v[0] = c0;
+            C.v[1] = c1;
+        } else {
+            *reinterpret_cast<double2*>(tile + st) = make_double2(Y.v[0], Y.v[1]);
+            __syncwarp();
+            const double y0 = *reinterpret_cast<const double*>(tile + ld0);
+            const double y1 = *reinterpret_cast<const double*>(tile + ld1);
+            C.v[0] = init ? init->v[0] : 0.0;
+            C.v[1] = init ? init->v[1] : 0.0;
+            dmma_8x8x4(C.v[0], C.v[1], X.v[0], y0);
+            dmma_8x8x4(C.v[0], C.v[1], X.v[1], y1);
+        }
+        return C;
+    }
+};
+
+constexpr int kN8WarpsPerBlock = 8;
+
+__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 3)
+    expm8_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
+                     mexp_selection* __restrict__ sel, int64_t batch, int accuracy, int rounding,
+                     int exact_s_min) {
+    using F = Group8::Frag;
+    __shared__ __align__(16) char tiles[kN8WarpsPerBlock][1024];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    Group8 g;
+    g.init(tiles[wib], lane);
+
+    const int64_t stride = int64_t(gridDim.x) * kN8WarpsPerBlock;
+    int64_t m = int64_t(blockIdx.x) * kN8WarpsPerBlock + wib;
+    double2 next = make_double2(0.0, 0.0);
+    if (m < batch) next = ld_stream(reinterpret_cast<const double2*>(a + m * 64) + lane);
+    for (; m < batch; m += stride) {
+        F A;
+        A.v[0] = next.x;
+        A.v[1] = next.y;
+        if (m + stride < batch)
+            next = ld_stream(reinterpret_cast<const double2*>(a + (m + stride) * 64) + lane);
+
+        // all_finite (dense_matrix.cpp:54-58) and the exact 1-norm
+        // (kernels.cpp:44-53): lane j < 8 sums column j over rows 0..7 in order
+        const bool allfin = __all_sync(0xffffffffu, isfinite(A.v[0]) && isfinite(A.v[1]));
+        char* t = g.tile;
+        __syncwarp();  // the previous matrix's last readers are done with the tile
+        *reinterpret_cast<double2*>(t + g.st) = make_double2(A.v[0], A.v[1]);
+        __syncwarp();
+        double colsum = 0.0;
+        if (lane < 8) {
+            const uint32_t half = (lane & 1) << 3;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                colsum = __dadd_rn(colsum, fabs(*reinterpret_cast<const double*>(t + unit8(i, lane >> 1) + half)));
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) colsum = fmax(colsum, __shfl_xor_sync(0xffffffffu, colsum, o));
+        const double norm = __shfl_sync(0xffffffffu, colsum, 0);
+
+        Sel sl{0, 0, MEXP_OK};
+        if (!allfin)
+            sl.status = MEXP_ERR_NONFINITE;
+        else
+            sl = select_device(norm, accuracy);
+        if (sel && lane == 0) {
+            mexp_selection rec;
+            rec.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
+            rec.degree = int16_t(sl.degree);
+            rec.s = int16_t(sl.s);
+            rec.status = sl.status;
+            sel[m] = rec;
+        }
+        F X;
+        if (sl.status != MEXP_OK) {
+            X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
+        } else {
+            const bool exact = rounding == MEXP_ROUND_REFERENCE ||
+                               (rounding == MEXP_ROUND_AUTO && sl.s >= exact_s_min);
+            g.fscale = ldexp(1.0, -sl.s);
+            if (exact)
+                X = run_expm<ExactOps>(g, A, sl.degree, sl.s);
+            else
+                X = run_expm<FastOps>(g, A, sl.degree, sl.s);
+        }
+        st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
+    }
+}
+
+}  // namespace mexp_b200

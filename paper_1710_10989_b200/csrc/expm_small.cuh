@@ -21,10 +21,10 @@ namespace mexp_b200 {
 
 template <int N>
 struct TileShape;  // tiles per warp block for the W warps of a group
-template <> struct TileShape<8>  { static constexpr int W = 1, TR = 1, TC = 1, STASH = 0; };
-template <> struct TileShape<16> { static constexpr int W = 2, TR = 1, TC = 2, STASH = 0; };
-template <> struct TileShape<32> { static constexpr int W = 4, TR = 2, TC = 2, STASH = 0; };
-template <> struct TileShape<64> { static constexpr int W = 8, TR = 2, TC = 4, STASH = 4; };
+template <> struct TileShape<8>  { static constexpr int W = 1, TR = 1, TC = 1, STASH = 0, MIN_BLOCKS = 4; };
+template <> struct TileShape<16> { static constexpr int W = 2, TR = 1, TC = 2, STASH = 0, MIN_BLOCKS = 2; };
+template <> struct TileShape<32> { static constexpr int W = 4, TR = 2, TC = 2, STASH = 0, MIN_BLOCKS = 1; };
+template <> struct TileShape<64> { static constexpr int W = 8, TR = 2, TC = 4, STASH = 4, MIN_BLOCKS = 1; };
 
 template <int N>
 struct Group {
@@ -43,6 +43,8 @@ struct Group {
     static constexpr int SMEM_DOUBLES = 2 * N * LD + S::STASH * STASH_SLOT + 2 * W + 2;
 
     struct Frag {
+        using T = double;
+        static constexpr int kCount = K;
         double v[K];
     };
 
@@ -124,6 +126,31 @@ struct Group {
     // C = X * Y (same = X and Y are the same matrix: squarings, A*A).
     template <class Ops>
     __device__ __forceinline__ Frag mm(const Frag& X, const Frag& Y, bool same) const {
+        return mm_impl<Ops>(X, Y, same, nullptr);
+    }
+    template <class Ops>
+    __device__ __forceinline__ Frag sq_first(const Frag& A) const {
+        return mm_impl<Ops>(A, A, true, nullptr);
+    }
+    // C = X * Y + B (add(matmul(X, Y), B), dense_matrix.cpp:94-96). The fast
+    // path seeds the DMMA accumulators with B; the exact path adds after the
+    // product, in the reference's order.
+    template <class Ops>
+    __device__ __forceinline__ Frag mm_add(const Frag& X, const Frag& Y, bool same,
+                                           const Frag& B) const {
+        if constexpr (Ops::kExact) {
+            Frag P = mm_impl<Ops>(X, Y, same, nullptr);
+#pragma unroll
+            for (int e = 0; e < K; ++e) P.v[e] = Ops::add(P.v[e], B.v[e]);
+            return P;
+        } else {
+            return mm_impl<Ops>(X, Y, same, &B);
+        }
+    }
+
+    template <class Ops>
+    __device__ __forceinline__ Frag mm_impl(const Frag& X, const Frag& Y, bool same,
+                                            const Frag* init) const {
         sync();  // previous product's readers are done with sx/sy
         store_smem(sx, X);
         if (!same) store_smem(sy, Y);
@@ -152,7 +179,7 @@ struct Group {
             }
         } else {
 #pragma unroll
-            for (int t = 0; t < K; ++t) C.v[t] = 0.0;
+            for (int t = 0; t < K; ++t) C.v[t] = init ? init->v[t] : 0.0;
             const int bi = warp % BLK_R, bj = warp / BLK_R;
             const int ar = lane >> 2, aq = lane & 3;
 #pragma unroll 2
@@ -174,43 +201,31 @@ struct Group {
 };
 
 // ---- elementwise linear combinations (reference lincomb, kernels.cpp:29-37):
-// out = c0*m0, then out += ci*mi left to right.
+// out = c0*m0, then out += ci*mi left to right. With ExactOps every term is
+// evaluated literally (the identity enters as a full matrix, c*0.0 included,
+// as in the reference). The fast path skips zero coefficients and starts an
+// identity term (ID0) from its diagonal value instead of multiplying.
 template <class Ops, class F>
-__device__ __forceinline__ F lc(double c0, const F& m0, double c1, const F& m1) {
-    F r;
-#pragma unroll
-    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e)
-        r.v[e] = Ops::mac(Ops::mul(c0, m0.v[e]), c1, m1.v[e]);
-    return r;
+__device__ __forceinline__ void lc_rest(F&, int) {}
+template <class Ops, class F, class... R>
+__device__ __forceinline__ void lc_rest(F& r, int e, double c, const F& m, R... rest) {
+    if (Ops::kExact || c != 0.0) r.v[e] = Ops::mac(r.v[e], c, m.v[e]);
+    lc_rest<Ops>(r, e, rest...);
 }
-template <class Ops, class F>
-__device__ __forceinline__ F lc(double c0, const F& m0, double c1, const F& m1, double c2,
-                                const F& m2) {
+template <class Ops, bool ID0 = false, class F, class... R>
+__device__ __forceinline__ F lc(double c0, const F& m0, R... rest) {
+    using T = typename F::T;
     F r;
 #pragma unroll
-    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e)
-        r.v[e] = Ops::mac(Ops::mac(Ops::mul(c0, m0.v[e]), c1, m1.v[e]), c2, m2.v[e]);
-    return r;
-}
-template <class Ops, class F>
-__device__ __forceinline__ F lc(double c0, const F& m0, double c1, const F& m1, double c2,
-                                const F& m2, double c3, const F& m3) {
-    F r;
-#pragma unroll
-    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e)
-        r.v[e] = Ops::mac(Ops::mac(Ops::mac(Ops::mul(c0, m0.v[e]), c1, m1.v[e]), c2, m2.v[e]), c3,
-                          m3.v[e]);
-    return r;
-}
-template <class Ops, class F>
-__device__ __forceinline__ F lc(double c0, const F& m0, double c1, const F& m1, double c2,
-                                const F& m2, double c3, const F& m3, double c4, const F& m4) {
-    F r;
-#pragma unroll
-    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e)
-        r.v[e] = Ops::mac(
-            Ops::mac(Ops::mac(Ops::mac(Ops::mul(c0, m0.v[e]), c1, m1.v[e]), c2, m2.v[e]), c3, m3.v[e]),
-            c4, m4.v[e]);
+    for (int e = 0; e < F::kCount; ++e) {
+        if constexpr (!Ops::kExact && ID0)
+            r.v[e] = (m0.v[e] != T(0)) ? T(c0) : T(0);
+        else if (!Ops::kExact && c0 == 0.0)
+            r.v[e] = T(0);
+        else
+            r.v[e] = Ops::mul(c0, m0.v[e]);
+        lc_rest<Ops>(r, e, rest...);
+    }
     return r;
 }
 // add(a, b) = lincomb({1, 1}, {a, b}) (dense_matrix.cpp:94-96); 1.0*x is exact.
@@ -218,7 +233,7 @@ template <class Ops, class F>
 __device__ __forceinline__ F addm(const F& a, const F& b) {
     F r;
 #pragma unroll
-    for (int e = 0; e < int(sizeof(F) / sizeof(double)); ++e) r.v[e] = Ops::add(a.v[e], b.v[e]);
+    for (int e = 0; e < F::kCount; ++e) r.v[e] = Ops::add(a.v[e], b.v[e]);
     return r;
 }
 
@@ -231,59 +246,59 @@ __device__ typename G::Frag eval_taylor_new(const G& g, int degree, const typena
         case 1:  // add(I, A)
             return addm<Ops>(I, A);
         case 2: {  // eval_ps(2): I + A + A2/2
-            const F A2 = g.template mm<Ops>(A, A, true);
-            return lc<Ops>(1.0, I, 1.0, A, 0.5, A2);
+            const F A2 = g.template sq_first<Ops>(A);
+            return lc<Ops, true>(1.0, I, 1.0, A, 0.5, A2);
         }
         case 4: {  // eval_ps(4)
-            const F A2 = g.template mm<Ops>(A, A, true);
-            const F f0 = lc<Ops>(1.0, I, 1.0, A);
-            const F f1 = lc<Ops>(kInvFact2, I, kInvFact3, A);
+            const F A2 = g.template sq_first<Ops>(A);
+            const F f0 = lc<Ops, true>(1.0, I, 1.0, A);
+            const F f1 = lc<Ops, true>(kInvFact2, I, kInvFact3, A);
             const F inner = lc<Ops>(1.0, f1, kInvFact4, A2);
-            return addm<Ops>(f0, g.template mm<Ops>(inner, A2, false));
+            return g.template mm_add<Ops>(inner, A2, false, f0);
         }
         case 8: {  // eval_t8, 3 products
-            const F A2 = g.template mm<Ops>(A, A, true);
+            const F A2 = g.template sq_first<Ops>(A);
             const F A4 = g.template mm<Ops>(A2, lc<Ops>(T8C::x1, A, T8C::x2, A2), false);
-            const F A8 = g.template mm<Ops>(lc<Ops>(T8C::x3, A2, 1.0, A4),
-                                            lc<Ops>(T8C::x4, I, T8C::x5, A, T8C::x6, A2, T8C::x7, A4),
-                                            false);
-            return lc<Ops>(T8C::y0, I, T8C::y1, A, T8C::y2, A2, 1.0, A8);
+            const F A8 = g.template mm<Ops>(
+                lc<Ops>(T8C::x3, A2, 1.0, A4),
+                lc<Ops, true>(T8C::x4, I, T8C::x5, A, T8C::x6, A2, T8C::x7, A4), false);
+            return lc<Ops, true>(T8C::y0, I, T8C::y1, A, T8C::y2, A2, 1.0, A8);
         }
         case 12: {  // eval_t12, 4 products
-            const F A2 = g.template mm<Ops>(A, A, true);
+            const F A2 = g.template sq_first<Ops>(A);
             const F A3 = g.template mm<Ops>(A2, A, false);
             F B[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-                B[j] = lc<Ops>(c_t12[0][j], I, c_t12[1][j], A, c_t12[2][j], A2, c_t12[3][j], A3);
-            const F A6 = addm<Ops>(B[2], g.template mm<Ops>(B[3], B[3], true));
-            return addm<Ops>(B[0], g.template mm<Ops>(addm<Ops>(B[1], A6), A6, false));
+                B[j] = lc<Ops, true>(c_t12[0][j], I, c_t12[1][j], A, c_t12[2][j], A2, c_t12[3][j], A3);
+            const F A6 = g.template mm_add<Ops>(B[3], B[3], true, B[2]);
+            return g.template mm_add<Ops>(addm<Ops>(B[1], A6), A6, false, B[0]);
         }
         default: {  // 18: eval_t18, 5 products
-            const F A2 = g.template mm<Ops>(A, A, true);
+            const F A2 = g.template sq_first<Ops>(A);
             const F A3 = g.template mm<Ops>(A2, A, false);
             const F A6 = g.template mm<Ops>(A3, A3, true);
             if constexpr (G::S::STASH >= 4) {
                 // register-lean order for large fragments: B1, B5, B4, B3 to the
                 // stash, B2 kept; A..A6 die after B2.
-                g.put(0, lc<Ops>(c_t18a[0], I, c_t18a[1], A, c_t18a[2], A2, c_t18a[3], A3));
+                g.put(0, lc<Ops, true>(c_t18a[0], I, c_t18a[1], A, c_t18a[2], A2, c_t18a[3], A3));
 #pragma unroll
                 for (int j = 3; j >= 1; --j)
-                    g.put(4 - j, lc<Ops>(c_t18b[j][0], I, c_t18b[j][1], A, c_t18b[j][2], A2,
-                                         c_t18b[j][3], A3, c_t18b[j][4], A6));
-                const F B2 = lc<Ops>(c_t18b[0][0], I, c_t18b[0][1], A, c_t18b[0][2], A2,
-                                     c_t18b[0][3], A3, c_t18b[0][4], A6);
-                const F A9 = addm<Ops>(g.template mm<Ops>(g.get(0), g.get(1), false), g.get(2));
-                return addm<Ops>(B2, g.template mm<Ops>(addm<Ops>(g.get(3), A9), A9, false));
+                    g.put(4 - j, lc<Ops, true>(c_t18b[j][0], I, c_t18b[j][1], A, c_t18b[j][2], A2,
+                                               c_t18b[j][3], A3, c_t18b[j][4], A6));
+                const F B2 = lc<Ops, true>(c_t18b[0][0], I, c_t18b[0][1], A, c_t18b[0][2], A2,
+                                           c_t18b[0][3], A3, c_t18b[0][4], A6);
+                const F A9 = g.template mm_add<Ops>(g.get(0), g.get(1), false, g.get(2));
+                return g.template mm_add<Ops>(addm<Ops>(g.get(3), A9), A9, false, B2);
             } else {
-                const F B1 = lc<Ops>(c_t18a[0], I, c_t18a[1], A, c_t18a[2], A2, c_t18a[3], A3);
+                const F B1 = lc<Ops, true>(c_t18a[0], I, c_t18a[1], A, c_t18a[2], A2, c_t18a[3], A3);
                 F B[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    B[j] = lc<Ops>(c_t18b[j][0], I, c_t18b[j][1], A, c_t18b[j][2], A2,
-                                   c_t18b[j][3], A3, c_t18b[j][4], A6);
-                const F A9 = addm<Ops>(g.template mm<Ops>(B1, B[3], false), B[2]);
-                return addm<Ops>(B[0], g.template mm<Ops>(addm<Ops>(B[1], A9), A9, false));
+                    B[j] = lc<Ops, true>(c_t18b[j][0], I, c_t18b[j][1], A, c_t18b[j][2], A2,
+                                         c_t18b[j][3], A3, c_t18b[j][4], A6);
+                const F A9 = g.template mm_add<Ops>(B1, B[3], false, B[2]);
+                return g.template mm_add<Ops>(addm<Ops>(B[1], A9), A9, false, B[0]);
             }
         }
     }
@@ -306,7 +321,7 @@ __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename 
 
 // One group of W warps per matrix; GPC groups per CTA; grid-stride over the batch.
 template <int N, int GPC>
-__global__ void __launch_bounds__(32 * TileShape<N>::W * GPC)
+__global__ void __launch_bounds__(32 * TileShape<N>::W * GPC, TileShape<N>::MIN_BLOCKS)
     expm_small_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
                           mexp_selection* __restrict__ sel, int64_t batch, int accuracy,
                           int rounding, int exact_s_min) {

@@ -1,9 +1,308 @@
+// Batched small-n expm in fp32 storage and arithmetic (BASELINE cfg3: 32x32).
+//
+// Products are FFMA on the SIMT pipes (never TF32: the tolerance is
+// 50*n*2^-24 and TF32 rounds operands to 10 bits). One group of W warps per
+// matrix; each lane owns a TR x TC register tile of every matrix variable
+// and a product C = X*Y streams X^T and Y rows out of shared memory
+// (X stored transposed so a lane's TR rows of column k are one vector load,
+// Y's TC columns of row k are TC/4 float4 loads shared by the lanes of a
+// tile column). The exact 1-norm and the (m, s) selection run in fp64 on
+// the fp32 values promoted to double, i.e. exactly the reference's norm of
+// the same data (kernels.cpp:44-53), so (m, s) match bit for bit.
+#include "expm_small.cuh"
 #include "expm_small_f32.cuh"
 
 namespace mexp_b200 {
 
-int run_small_f32(const float*, float*, mexp_selection*, int, int64_t, int, cudaStream_t,
-                  std::atomic<uint64_t>*) {
+struct F32Ops {
+    static constexpr bool kExact = false;
+    __device__ __forceinline__ static float mul(float a, float b) { return a * b; }
+    __device__ __forceinline__ static float add(float a, float b) { return a + b; }
+    __device__ __forceinline__ static float mac(float acc, float a, float b) { return fmaf(a, b, acc); }
+};
+
+template <int N> struct ShapeF32;
+//                                   warps  tile rows  tile cols  stash slots
+template <> struct ShapeF32<8>  { static constexpr int W = 1, TR = 1, TC = 2, STASH = 4; };
+template <> struct ShapeF32<16> { static constexpr int W = 1, TR = 2, TC = 4, STASH = 4; };
+template <> struct ShapeF32<32> { static constexpr int W = 1, TR = 4, TC = 8, STASH = 4; };
+template <> struct ShapeF32<64> { static constexpr int W = 4, TR = 4, TC = 8, STASH = 4; };
+
+template <int N>
+struct GroupF32 {
+    using S = ShapeF32<N>;
+    static constexpr int W = S::W, TR = S::TR, TC = S::TC;
+    static constexpr int THREADS = 32 * W;
+    static constexpr int GC = N / TC;          // tile columns
+    static constexpr int K = TR * TC;          // floats per lane per matrix
+    static_assert((N / TR) * GC == THREADS, "tile cover");
+    static constexpr int LD = N + 4;           // padded row stride (floats)
+    static constexpr int STASH_SLOT = K * THREADS;
+    static constexpr int SMEM_FLOATS = 2 * N * LD + S::STASH * STASH_SLOT + 4 * W + 4;
+
+    struct Frag {
+        using T = float;
+        static constexpr int kCount = K;
+        float v[K];
+    };
+
+    float* sxt;  // X transposed: sxt[k * LD + i] = X[i][k]
+    float* sy;   // Y row-major
+    float* stash;
+    double* scal;  // per-warp partial results (8-byte aligned)
+    int lane, warp, tid, bar_id, ti, tj;
+
+    // element e = r * TC + c of the lane's tile -> (row, col)
+    __device__ __forceinline__ int row_of(int r) const { return ti * TR + r; }
+    __device__ __forceinline__ int col_of(int c) const {
+        if constexpr (TC >= 4)
+            return 4 * tj + (c & 3) + (c >> 2) * (4 * GC);
+        else
+            return TC * tj + c;
+    }
+
+    __device__ __forceinline__ void sync() const {
+        if constexpr (W == 1)
+            __syncwarp();
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(THREADS) : "memory");
+    }
+
+    __device__ __forceinline__ Frag ident() const {
+        Frag f;
+#pragma unroll
+        for (int r = 0; r < TR; ++r)
+#pragma unroll
+            for (int c = 0; c < TC; ++c) f.v[r * TC + c] = (row_of(r) == col_of(c)) ? 1.f : 0.f;
+        return f;
+    }
+
+    __device__ __forceinline__ Frag load_global(const float* m) const {
+        Frag f;
+#pragma unroll
+        for (int r = 0; r < TR; ++r) {
+            if constexpr (TC >= 4) {
+#pragma unroll
+                for (int h = 0; h < TC / 4; ++h) {
+                    const float4 v = ld_stream(reinterpret_cast<const float4*>(m + row_of(r) * N + col_of(4 * h)));
+                    f.v[r * TC + 4 * h] = v.x;
+                    f.v[r * TC + 4 * h + 1] = v.y;
+                    f.v[r * TC + 4 * h + 2] = v.z;
+                    f.v[r * TC + 4 * h + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < TC; ++c) f.v[r * TC + c] = __ldcs(m + row_of(r) * N + col_of(c));
+            }
+        }
+        return f;
+    }
+    __device__ __forceinline__ void store_global(float* m, const Frag& f) const {
+#pragma unroll
+        for (int r = 0; r < TR; ++r) {
+            if constexpr (TC >= 4) {
+#pragma unroll
+                for (int h = 0; h < TC / 4; ++h)
+                    st_stream(reinterpret_cast<float4*>(m + row_of(r) * N + col_of(4 * h)),
+                              make_float4(f.v[r * TC + 4 * h], f.v[r * TC + 4 * h + 1],
+                                          f.v[r * TC + 4 * h + 2], f.v[r * TC + 4 * h + 3]));
+            } else {
+#pragma unroll
+                for (int c = 0; c < TC; ++c) __stcs(m + row_of(r) * N + col_of(c), f.v[r * TC + c]);
+            }
+        }
+    }
+    __device__ __forceinline__ void store_rows(float* s, const Frag& f) const {
+#pragma unroll
+        for (int r = 0; r < TR; ++r)
+#pragma unroll
+            for (int c = 0; c < TC; ++c) s[row_of(r) * LD + col_of(c)] = f.v[r * TC + c];
+    }
+    __device__ __forceinline__ void store_cols(float* s, const Frag& f) const {
+#pragma unroll
+        for (int c = 0; c < TC; ++c)
+#pragma unroll
+            for (int r = 0; r < TR; ++r) s[col_of(c) * LD + row_of(r)] = f.v[r * TC + c];
+    }
+
+    __device__ __forceinline__ void put(int slot, const Frag& f) const {
+        float* p = stash + slot * STASH_SLOT;
+#pragma unroll
+        for (int e = 0; e < K; ++e) p[e * THREADS + tid] = f.v[e];
+    }
+    __device__ __forceinline__ Frag get(int slot) const {
+        const float* p = stash + slot * STASH_SLOT;
+        Frag f;
+#pragma unroll
+        for (int e = 0; e < K; ++e) f.v[e] = p[e * THREADS + tid];
+        return f;
+    }
+
+    template <class Ops>
+    __device__ __forceinline__ Frag mm(const Frag& X, const Frag& Y, bool same) const {
+        return mm_impl(X, Y, nullptr);
+    }
+    template <class Ops>
+    __device__ __forceinline__ Frag mm_add(const Frag& X, const Frag& Y, bool,
+                                           const Frag& B) const {
+        return mm_impl(X, Y, &B);
+    }
+    template <class Ops>
+    __device__ __forceinline__ Frag sq_first(const Frag& A) const {
+        return mm_impl(A, A, nullptr);
+    }
+    __device__ __forceinline__ Frag mm_impl(const Frag& X, const Frag& Y, const Frag* init) const {
+        sync();
+        store_cols(sxt, X);
+        store_rows(sy, Y);
+        sync();
+        Frag C;
+#pragma unroll
+        for (int e = 0; e < K; ++e) C.v[e] = init ? init->v[e] : 0.f;
+#pragma unroll 2
+        for (int k = 0; k < N; ++k) {
+            float a[TR], b[TC];
+            const float* xa = sxt + k * LD + ti * TR;
+#pragma unroll
+            for (int r = 0; r < TR; ++r) a[r] = xa[r];
+            const float* yb = sy + k * LD;
+#pragma unroll
+            for (int c = 0; c < TC; ++c) b[c] = yb[col_of(c)];
+#pragma unroll
+            for (int r = 0; r < TR; ++r)
+#pragma unroll
+                for (int c = 0; c < TC; ++c) C.v[r * TC + c] = fmaf(a[r], b[c], C.v[r * TC + c]);
+        }
+        return C;
+    }
+};
+
+template <int N, int GPC>
+__global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
+    expm_small_f32_kernel(const float* __restrict__ a, float* __restrict__ out,
+                          mexp_selection* __restrict__ sel, int64_t batch, int accuracy) {
+    using G = GroupF32<N>;
+    using F = typename G::Frag;
+    extern __shared__ __align__(16) float smemf[];
+    const int gid = threadIdx.x / G::THREADS;
+    G g;
+    float* base = smemf + gid * G::SMEM_FLOATS;
+    g.sxt = base;
+    g.sy = base + N * G::LD;
+    g.stash = base + 2 * N * G::LD;
+    g.scal = reinterpret_cast<double*>(g.stash + G::S::STASH * G::STASH_SLOT);
+    g.tid = threadIdx.x % G::THREADS;
+    g.lane = g.tid & 31;
+    g.warp = g.tid >> 5;
+    g.bar_id = 1 + gid;
+    g.ti = g.tid / G::GC;
+    g.tj = g.tid % G::GC;
+
+    constexpr int64_t NN = int64_t(N) * N;
+    const int64_t stride = int64_t(gridDim.x) * GPC;
+    for (int64_t m = int64_t(blockIdx.x) * GPC + gid; m < batch; m += stride) {
+        F A = g.load_global(a + m * NN);
+        bool fin = true;
+#pragma unroll
+        for (int e = 0; e < G::K; ++e) fin = fin && isfinite(A.v[e]);
+        g.sync();
+        g.store_rows(g.sy, A);
+        g.sync();
+        // exact 1-norm of the promoted values, rows ascending (kernels.cpp:44-53)
+        double colsum = 0.0;
+        for (int j = g.tid; j < N; j += G::THREADS) {
+            double s = 0.0;
+            for (int i = 0; i < N; ++i) s = __dadd_rn(s, fabs(double(g.sy[i * G::LD + j])));
+            colsum = fmax(colsum, s);
+        }
+        const bool wfin = __all_sync(0xffffffffu, fin);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) colsum = fmax(colsum, __shfl_xor_sync(0xffffffffu, colsum, o));
+        double norm = colsum;
+        bool allfin = wfin;
+        if constexpr (G::W > 1) {
+            if (g.lane == 0) {
+                g.scal[g.warp] = colsum;
+                g.scal[G::W + g.warp] = wfin ? 1.0 : 0.0;
+            }
+            g.sync();
+#pragma unroll
+            for (int w = 0; w < G::W; ++w) {
+                norm = fmax(norm, g.scal[w]);
+                allfin = allfin && (g.scal[G::W + w] != 0.0);
+            }
+        }
+        Sel sl{0, 0, MEXP_OK};
+        if (!allfin)
+            sl.status = MEXP_ERR_NONFINITE;
+        else
+            sl = select_device(norm, accuracy);
+        if (sel && g.tid == 0) {
+            mexp_selection r;
+            r.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
+            r.degree = int16_t(sl.degree);
+            r.s = int16_t(sl.s);
+            r.status = sl.status;
+            sel[m] = r;
+        }
+        F X;
+        if (sl.status != MEXP_OK) {
+#pragma unroll
+            for (int e = 0; e < G::K; ++e) X.v[e] = __int_as_float(0x7fc00000);
+        } else {
+            if (sl.s > 0) {  // exact scaling by 2^-s, rounded once to float
+                const double f = ldexp(1.0, -sl.s);
+#pragma unroll
+                for (int e = 0; e < G::K; ++e) A.v[e] = float(f * double(A.v[e]));
+            }
+            X = eval_taylor_new<F32Ops>(g, sl.degree, A);
+            for (int i = 0; i < sl.s; ++i) X = g.template mm<F32Ops>(X, X, true);
+        }
+        g.store_global(out + m * NN, X);
+    }
+}
+
+namespace {
+int sm_count() {
+    static int v = [] {
+        int dev = 0, s = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+        return s;
+    }();
+    return v;
+}
+
+template <int N, int GPC>
+int launch_f32(const float* a, float* out, mexp_selection* sel, int64_t batch, int accuracy,
+               cudaStream_t st, std::atomic<uint64_t>* launches) {
+    using G = GroupF32<N>;
+    auto kern = expm_small_f32_kernel<N, GPC>;
+    const size_t smem = size_t(G::SMEM_FLOATS) * GPC * sizeof(float);
+    static int bps = [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, G::THREADS * GPC, smem);
+        return b > 0 ? b : 1;
+    }();
+    const int64_t want = (batch + GPC - 1) / GPC;
+    const int64_t cap = int64_t(bps) * sm_count();
+    const int grid = int(want < cap ? want : cap);
+    if (grid == 0) return MEXP_OK;
+    kern<<<grid, G::THREADS * GPC, smem, st>>>(a, out, sel, batch, accuracy);
+    launches->fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? MEXP_OK : MEXP_ERR_CUDA;
+}
+}  // namespace
+
+int run_small_f32(const float* d_a, float* d_out, mexp_selection* d_sel, int np, int64_t batch,
+                  int accuracy, cudaStream_t st, std::atomic<uint64_t>* launches) {
+    switch (np) {
+        case 8: return launch_f32<8, 8>(d_a, d_out, d_sel, batch, accuracy, st, launches);
+        case 16: return launch_f32<16, 4>(d_a, d_out, d_sel, batch, accuracy, st, launches);
+        case 32: return launch_f32<32, 2>(d_a, d_out, d_sel, batch, accuracy, st, launches);
+        case 64: return launch_f32<64, 1>(d_a, d_out, d_sel, batch, accuracy, st, launches);
+    }
     return MEXP_ERR_UNSUPPORTED;
 }
 

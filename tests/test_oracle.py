@@ -182,7 +182,7 @@ def test_device_coefficients_equal_reference(golden):
         assert got == want, name
 
     def block(name):
-        m = re.search(r"__constant__ double " + name + r"\[[^=]*=\s*\{(.*?)\};", src, re.S)
+        m = re.search(r"constexpr double " + name + r"\[[^=]*=\s*\{(.*?)\};", src, re.S)
         return np.array([float(v) for v in re.findall(r"[-+]?\d[\d.e+-]*", m.group(1))])
 
     assert np.array_equal(block("c_t12"), g["t12"].ravel())
