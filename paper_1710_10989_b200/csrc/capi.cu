@@ -307,27 +307,16 @@ int mexp_selection_table(int accuracy, int family, int32_t* degrees, int32_t* pr
     return k;
 }
 
-// mexp::select (expm.cpp:11-29) on the host: pure table arithmetic.
+// mexp::select (expm.cpp:11-29) on the host: pure table arithmetic, the very
+// function the kernels run (select_device is __host__ __device__).
 int mexp_select(double norm, int accuracy, int family, int32_t* degree, int32_t* s) {
     if (accuracy != MEXP_ACCURACY_SINGLE && accuracy != MEXP_ACCURACY_DOUBLE)
         return MEXP_ERR_INVALID_ARGUMENT;
     if (family != MEXP_FAMILY_TAYLOR_NEW) return MEXP_ERR_UNSUPPORTED;
-    const double* th = kThetaHost[accuracy];
-    if (!std::isfinite(norm) || norm < 0) return MEXP_ERR_NORM_NONFINITE;
-    if (norm <= th[5]) {
-        int best = -1;
-        for (int e = 0; e < 6; ++e) {
-            if (th[e] < norm) continue;
-            if (best < 0 || products_of_entry(e) < products_of_entry(best)) best = e;
-        }
-        *degree = degree_of(best);
-        *s = 0;
-        return MEXP_OK;
-    }
-    int k = 0;
-    while (std::ldexp(norm, -k) > th[5]) ++k;
-    *degree = 18;
-    *s = k;
+    const Sel r = select_device(norm, accuracy);
+    if (r.status != MEXP_OK) return r.status;
+    *degree = r.degree;
+    *s = r.s;
     return MEXP_OK;
 }
 

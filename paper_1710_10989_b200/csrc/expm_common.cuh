@@ -3,7 +3,9 @@
 // arithmetic policies (reference-exact and fast).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include "mexp_b200.h"
@@ -88,46 +90,60 @@ struct Sel {
     int status;
 };
 
-__device__ __forceinline__ double theta_of(int accuracy, int e) {
-    double t = c_theta[0][0];
-#pragma unroll
-    for (int k = 0; k < kNumEntries; ++k)
-        if (k == e) t = accuracy ? c_theta[1][k] : c_theta[0][k];
-    return t;
+__host__ __device__ __forceinline__ long long dbits(double x) {
+#ifdef __CUDA_ARCH__
+    return __double_as_longlong(x);
+#else
+    long long b;
+    memcpy(&b, &x, sizeof b);
+    return b;
+#endif
+}
+__host__ __device__ __forceinline__ double dfrom(long long b) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(b);
+#else
+    double x;
+    memcpy(&x, &b, sizeof x);
+    return x;
+#endif
 }
 
-__device__ __forceinline__ Sel select_device(double norm, int accuracy) {
+// One implementation for the kernels and the host-side mexp_select, so the
+// CPU tests of mexp_select exercise the exact logic the kernels run.
+__host__ __device__ __forceinline__ Sel select_device(double norm, int accuracy) {
     Sel r{0, 0, MEXP_OK};
     if (!isfinite(norm) || norm < 0.0) {
         r.status = MEXP_ERR_NORM_NONFINITE;
         return r;
     }
-    const double tmax = theta_of(accuracy, kNumEntries - 1);
+    // the reference's decimal literals (theta_tables.cpp:45-51)
+    const double t0 = accuracy ? 2.22e-16 : 1.19e-7;
+    const double t1 = accuracy ? 2.58e-8 : 5.98e-4;
+    const double t2 = accuracy ? 3.40e-4 : 5.12e-2;
+    const double t3 = accuracy ? 4.99e-2 : 5.80e-1;
+    const double t4 = accuracy ? 2.99e-1 : 1.46;
+    const double tmax = accuracy ? 1.09 : 3.01;
     if (norm <= tmax) {
-        int best = -1;
-#pragma unroll
-        for (int e = kNumEntries - 1; e >= 0; --e) {
-            // skip on theta < norm (expm.cpp:17); products and degrees both
-            // ascend with e, so the first admissible entry is the reference's
-            // (products, degree) minimum
-            if (!(theta_of(accuracy, e) < norm)) best = e;
-        }
-        r.degree = degree_of(best);
+        // entries with theta < norm are skipped (expm.cpp:17); products and
+        // degrees ascend with the entry, so the reference's (products, degree)
+        // minimum is the first admissible entry = the count of skipped ones
+        const int e = int(t0 < norm) + int(t1 < norm) + int(t2 < norm) + int(t3 < norm) +
+                      int(t4 < norm);
+        r.degree = e < 4 ? (1 << e) : (e == 4 ? 12 : 18);
         return r;
     }
-    // least s with ldexp(norm, -s) <= theta_18 (expm.cpp:27). For s >= 1 the
-    // loop only runs while norm * 2^-(s-1) > theta_18, so norm * 2^-s is a
-    // normal number and `ldexp(norm, -s) > t` <=> `norm > t * 2^s` exactly;
-    // doubling t is exact (it can only overflow to +inf, which ends the loop
-    // as ldexp would).
-    int s = 0;
-    double t = tmax;
-    while (norm > t) {
-        t *= 2.0;
-        ++s;
-    }
+    // least s with ldexp(norm, -s) <= theta_18 (expm.cpp:27). With norm =
+    // mn * 2^En and theta = mt * 2^Et (both normal here), theta * 2^k for
+    // k = En - Et has norm's exponent, and the answer is k if norm <= theta *
+    // 2^k else k + 1. Exactly the reference's loop (the halving there is exact
+    // while ldexp(norm, -s) > theta >= 2^-52); checked against it in
+    // tests/test_capi.py::test_closed_form_scaling_exponent.
+    const long long nb = dbits(norm), tb = dbits(tmax);
+    const long long k = (nb >> 52) - (tb >> 52);
+    const double t = dfrom(tb + (k << 52));
     r.degree = 18;
-    r.s = s;
+    r.s = int(k) + int(norm > t);
     return r;
 }
 

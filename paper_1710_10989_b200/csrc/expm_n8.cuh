@@ -152,74 +152,126 @@ struct Group8 {
     }
 };
 
-constexpr int kN8WarpsPerBlock = 8;
+constexpr int kN8WarpsPerBlock = 4;  // 128-thread blocks
+constexpr int kN8Mpw = 4;            // matrices per warp per round
 
-__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 3)
+// One round = 4 consecutive matrices per warp. The prologue (load, finite
+// check, exact 1-norm, selection, selection record) runs for the 4 at once so
+// all 32 lanes work: lane l sums column l&7 of matrix l>>3. Then the schemes
+// run one matrix at a time, each on its own 1 KB tile (which still holds its
+// unscaled A for sq_first).
+__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 5)
     expm8_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
                      mexp_selection* __restrict__ sel, int64_t batch, int accuracy, int rounding,
                      int exact_s_min) {
     using F = Group8::Frag;
-    __shared__ __align__(16) char tiles[kN8WarpsPerBlock][1024];
+    __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     Group8 g;
-    g.init(tiles[wib], lane);
+    g.init(tiles[wib][0], lane);
+    char* const wt = tiles[wib][0];
 
-    const int64_t stride = int64_t(gridDim.x) * kN8WarpsPerBlock;
-    int64_t m = int64_t(blockIdx.x) * kN8WarpsPerBlock + wib;
-    double2 next = make_double2(0.0, 0.0);
-    if (m < batch) next = ld_stream(reinterpret_cast<const double2*>(a + m * 64) + lane);
-    for (; m < batch; m += stride) {
-        F A;
-        A.v[0] = next.x;
-        A.v[1] = next.y;
-        if (m + stride < batch)
-            next = ld_stream(reinterpret_cast<const double2*>(a + (m + stride) * 64) + lane);
+    // 1-norm column reads of lane l: matrix jm = l >> 3, column c8 = l & 7;
+    // element (i, c8) at unit8(i, 0) & ~0x20 plus one of two lane bases
+    const int jm = lane >> 3, c8 = lane & 7, cp = c8 >> 1;
+    const uint32_t half = uint32_t(c8 & 1) << 3;
+    const char* nb0 = wt + jm * 1024 + ((((cp >> 1)) << 5) | ((cp & 1) << 4)) + half;
+    const char* nb1 = wt + jm * 1024 + (((1 ^ (cp >> 1)) << 5) | ((cp & 1) << 4)) + half;
 
-        // all_finite (dense_matrix.cpp:54-58) and the exact 1-norm
-        // (kernels.cpp:44-53): lane j < 8 sums column j over rows 0..7 in order
-        const bool allfin = __all_sync(0xffffffffu, isfinite(A.v[0]) && isfinite(A.v[1]));
-        char* t = g.tile;
-        __syncwarp();  // the previous matrix's last readers are done with the tile
-        *reinterpret_cast<double2*>(t + g.st) = make_double2(A.v[0], A.v[1]);
-        __syncwarp();
-        double colsum = 0.0;
-        if (lane < 8) {
-            const uint32_t half = (lane & 1) << 3;
+    const int64_t rounds = (batch + kN8Mpw - 1) / kN8Mpw;
+    const int64_t rstride = int64_t(gridDim.x) * kN8WarpsPerBlock;
+    int64_t rd = int64_t(blockIdx.x) * kN8WarpsPerBlock + wib;
+
+    auto load4 = [&](int64_t r, double2 (&v)[kN8Mpw]) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                colsum = __dadd_rn(colsum, fabs(*reinterpret_cast<const double*>(t + unit8(i, lane >> 1) + half)));
+        for (int j = 0; j < kN8Mpw; ++j) {
+            const int64_t m = r * kN8Mpw + j;
+            v[j] = (m < batch) ? ld_stream(reinterpret_cast<const double2*>(a + m * 64) + lane)
+                               : make_double2(0.0, 0.0);
         }
+    };
+    double2 nxt[kN8Mpw];
+    if (rd < rounds) load4(rd, nxt);
+    for (; rd < rounds; rd += rstride) {
+        double2 cur[kN8Mpw];
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) colsum = fmax(colsum, __shfl_xor_sync(0xffffffffu, colsum, o));
-        const double norm = __shfl_sync(0xffffffffu, colsum, 0);
+        for (int j = 0; j < kN8Mpw; ++j) cur[j] = nxt[j];
+        if (rd + rstride < rounds) load4(rd + rstride, nxt);
+        const int64_t m0 = rd * kN8Mpw;
 
+        // all_finite (dense_matrix.cpp:54-58), one ballot per matrix
+        uint32_t finbits = 0;
+#pragma unroll
+        for (int j = 0; j < kN8Mpw; ++j)
+            if (__all_sync(0xffffffffu, isfinite(cur[j].x) && isfinite(cur[j].y))) finbits |= 1u << j;
+
+        // stage the 4 (unscaled) matrices, one tile each
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kN8Mpw; ++j) *reinterpret_cast<double2*>(wt + j * 1024 + g.st) = cur[j];
+        __syncwarp();
+
+        // exact 1-norm (kernels.cpp:44-53): column sum over rows 0..7 in order
+        double colsum = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const char* p = (((i >> 1) & 1) ? nb1 : nb0) + (unit8(i, 0) & ~0x20u);
+            colsum = __dadd_rn(colsum, fabs(*reinterpret_cast<const double*>(p)));
+        }
+        // max over the 8 columns: non-negative doubles order like their bits
+        unsigned long long nb = __double_as_longlong(colsum);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const unsigned long long w = __shfl_xor_sync(0xffffffffu, nb, o);
+            nb = w > nb ? w : nb;
+        }
+        const double norm = __longlong_as_double(nb);
+        const bool allfin = (finbits >> jm) & 1u;
         Sel sl{0, 0, MEXP_OK};
         if (!allfin)
             sl.status = MEXP_ERR_NONFINITE;
         else
             sl = select_device(norm, accuracy);
-        if (sel && lane == 0) {
+        if (sel && c8 == 0 && m0 + jm < batch) {
             mexp_selection rec;
             rec.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
             rec.degree = int16_t(sl.degree);
             rec.s = int16_t(sl.s);
             rec.status = sl.status;
-            sel[m] = rec;
+            sel[m0 + jm] = rec;
         }
-        F X;
-        if (sl.status != MEXP_OK) {
-            X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
-        } else {
-            const bool exact = rounding == MEXP_ROUND_REFERENCE ||
-                               (rounding == MEXP_ROUND_AUTO && sl.s >= exact_s_min);
-            g.fscale = ldexp(1.0, -sl.s);
-            if (exact)
-                X = run_expm<ExactOps>(g, A, sl.degree, sl.s);
-            else
-                X = run_expm<FastOps>(g, A, sl.degree, sl.s);
+        const int info = sl.degree | (sl.s << 5) | (sl.status << 20);
+
+#pragma unroll 1
+        for (int j = 0; j < kN8Mpw; ++j) {
+            const int64_t m = m0 + j;
+            if (m >= batch) break;
+            const int inf = __shfl_sync(0xffffffffu, info, 8 * j);
+            const int degree = inf & 31, s = (inf >> 5) & 0x7fff, status = inf >> 20;
+            F A;
+            // cur[j] with a runtime j: select from registers, not local memory
+            double2 v = cur[0];
+#pragma unroll
+            for (int k = 1; k < kN8Mpw; ++k)
+                if (j == k) v = cur[k];
+            A.v[0] = v.x;
+            A.v[1] = v.y;
+            g.tile = wt + j * 1024;
+            F X;
+            if (status != MEXP_OK) {
+                X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
+            } else {
+                const bool exact = rounding == MEXP_ROUND_REFERENCE ||
+                                   (rounding == MEXP_ROUND_AUTO && s >= exact_s_min);
+                g.fscale = ldexp(1.0, -s);
+                if (exact)
+                    X = run_expm<ExactOps>(g, A, degree, s);
+                else
+                    X = run_expm<FastOps>(g, A, degree, s);
+            }
+            st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
         }
-        st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
     }
 }
 

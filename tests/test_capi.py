@@ -72,6 +72,25 @@ def test_host_select_matches_golden(golden):
                     mx.select(float(v), table)
 
 
+def test_closed_form_scaling_exponent(oracle):
+    """mexp_select (= the kernels' select_device, closed-form s from the
+    exponent bits) equals the reference's ldexp loop (restated in the oracle)
+    at every power-of-two boundary of both tables and on random norms."""
+    rng = np.random.default_rng(5)
+    for acc, tmax in ((0, 3.01), (1, 1.09)):
+        table = mx.selection_table(mx.Family.TaylorNew, mx.Accuracy(acc))
+        norms = [np.nextafter(tmax, np.inf), 1.7976931348623157e308, 1e-320, 0.0]
+        for k in range(0, 1030):
+            v = np.ldexp(tmax, k)
+            if np.isfinite(v):
+                norms += [v, np.nextafter(v, 0.0), np.nextafter(v, np.inf)]
+        norms += list(10.0 ** rng.uniform(-20, 308, 20000))
+        for v in norms:
+            st, d, s = oracle.select(float(v), acc)
+            assert st == 0
+            assert mx.select(float(v), table) == (d, s), (v, acc)
+
+
 def test_select_kats():
     t = mx.selection_table(mx.Family.TaylorNew, mx.Accuracy.Double)
     assert mx.select(0.0, t) == (1, 0)
