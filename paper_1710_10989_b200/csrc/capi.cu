@@ -6,6 +6,7 @@
 // block unchanged, since each padded term adds an exact +0 to a sum that is
 // never -0). n > 64 runs the DMMA GEMM engine (expm_large.cu).
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -120,22 +121,77 @@ int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t 
     return MEXP_OK;
 }
 
-int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
-                  int accuracy, int rounding, int smin, cudaStream_t st) {
-    static int blocks_per_sm = [] {
+// 8x8 variant (experiments; default chosen from the measurements in
+// profiles/): bit 0 = split DMMA accumulation, bit 1 = defer reference-rounded
+// matrices to a second kernel. MEXP_N8_VARIANT overrides.
+int n8_variant() {
+    static int v = [] {
+        const char* e = std::getenv("MEXP_N8_VARIANT");
+        // measured (profiles/cfg2_variants_r1.txt): chained DMMAs with the
+        // reference-rounded matrices inline is fastest for AUTO
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <bool kSplit, int kDefer>
+int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t batch,
+                      int accuracy, int rounding, int smin, cudaStream_t st) {
+    auto kern = expm8_f64_kernel<kSplit, kDefer>;
+    static int blocks_per_sm = [&] {
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, expm8_f64_kernel, 32 * kN8WarpsPerBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * kN8WarpsPerBlock, 0);
         return b > 0 ? b : 1;
     }();
-    const int64_t want = (batch + kN8WarpsPerBlock - 1) / kN8WarpsPerBlock;
+    static int exact_bps = [] {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, expm8_exact_kernel, 32 * kN8WarpsPerBlock, 0);
+        return b > 0 ? b : 1;
+    }();
     const int64_t cap = int64_t(blocks_per_sm) * num_sms();
+    if (kDefer && rounding == MEXP_ROUND_REFERENCE) {
+        // every matrix is reference-rounded: the exact kernel alone
+        const int64_t want = (batch + kN8WarpsPerBlock - 1) / kN8WarpsPerBlock;
+        const int64_t ecap = int64_t(exact_bps) * num_sms();
+        const int grid = int(want < ecap ? want : ecap);
+        expm8_exact_kernel<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy,
+                                                                   nullptr, nullptr);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        MEXP_CUDA(cudaGetLastError());
+        return MEXP_OK;
+    }
+    int32_t* work = nullptr;
+    const bool defer = kDefer && rounding == MEXP_ROUND_AUTO;
+    if (defer) {
+        MEXP_CUDA(cudaMallocAsync(&work, sizeof(int32_t) * (batch + 1), st));
+        MEXP_CUDA(cudaMemsetAsync(work + batch, 0, sizeof(int32_t), st));
+    }
+    const int64_t want = (batch + 4 * kN8WarpsPerBlock - 1) / (4 * kN8WarpsPerBlock);
     const int grid = int(want < cap ? want : cap);
-    if (grid == 0) return MEXP_OK;
-    expm8_f64_kernel<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy,
-                                                              rounding, smin);
+    kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding, smin,
+                                                 work, defer ? work + batch : nullptr);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());
+    if (defer) {
+        const int egrid = int(int64_t(exact_bps) * num_sms());
+        expm8_exact_kernel<<<egrid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy,
+                                                                    work, work + batch);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        MEXP_CUDA(cudaGetLastError());
+        MEXP_CUDA(cudaFreeAsync(work, st));
+    }
     return MEXP_OK;
+}
+
+int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
+                  int accuracy, int rounding, int smin, cudaStream_t st) {
+    if (batch == 0) return MEXP_OK;
+    switch (n8_variant()) {
+        case 0: return launch_n8_variant<false, 0>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 1: return launch_n8_variant<true, 0>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 2: return launch_n8_variant<false, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
+        default: return launch_n8_variant<true, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
+    }
 }
 
 int run_small_f64(const double* a, double* out, mexp_selection* sel, int np, int64_t batch,

@@ -39,7 +39,8 @@ __host__ __device__ __forceinline__ constexpr uint32_t unit8(int i, int c) {
            << 4;
 }
 
-struct Group8 {
+template <bool kSplit>
+struct Group8T {
     struct S {
         static constexpr int STASH = 0;
     };
@@ -106,8 +107,16 @@ struct Group8 {
             const double y1 = fscale * *reinterpret_cast<const double*>(tile + ld1);
             Frag C;
             C.v[0] = C.v[1] = 0.0;
-            dmma_8x8x4(C.v[0], C.v[1], A.v[0], y0);
-            dmma_8x8x4(C.v[0], C.v[1], A.v[1], y1);
+            if constexpr (kSplit) {
+                double e0 = 0.0, e1 = 0.0;
+                dmma_8x8x4(C.v[0], C.v[1], A.v[0], y0);
+                dmma_8x8x4(e0, e1, A.v[1], y1);
+                C.v[0] += e0;
+                C.v[1] += e1;
+            } else {
+                dmma_8x8x4(C.v[0], C.v[1], A.v[0], y0);
+                dmma_8x8x4(C.v[0], C.v[1], A.v[1], y1);
+            }
             return C;
         }
     }
@@ -145,8 +154,19 @@ struct Group8 {
             const double y1 = *reinterpret_cast<const double*>(tile + ld1);
             C.v[0] = init ? init->v[0] : 0.0;
             C.v[1] = init ? init->v[1] : 0.0;
-            dmma_8x8x4(C.v[0], C.v[1], X.v[0], y0);
-            dmma_8x8x4(C.v[0], C.v[1], X.v[1], y1);
+            if constexpr (kSplit) {
+                // two independent half-products (even / odd k) summed after:
+                // latency DMMA + DADD instead of two chained DMMAs (26 cycles
+                // each), at the price of 2 DADDs on the shared FP64 pipe
+                double e0 = 0.0, e1 = 0.0;
+                dmma_8x8x4(C.v[0], C.v[1], X.v[0], y0);
+                dmma_8x8x4(e0, e1, X.v[1], y1);
+                C.v[0] += e0;
+                C.v[1] += e1;
+            } else {
+                dmma_8x8x4(C.v[0], C.v[1], X.v[0], y0);
+                dmma_8x8x4(C.v[0], C.v[1], X.v[1], y1);
+            }
         }
         return C;
     }
@@ -160,11 +180,15 @@ constexpr int kN8Mpw = 4;            // matrices per warp per round
 // all 32 lanes work: lane l sums column l&7 of matrix l>>3. Then the schemes
 // run one matrix at a time, each on its own 1 KB tile (which still holds its
 // unscaled A for sq_first).
-__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 5)
+// kExact: 0 = exact-rounded matrices inline; 1 = fast kernel that defers the
+// matrices needing reference rounding to a worklist (expm8_exact_kernel).
+template <bool kSplit, int kDefer>
+__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
     expm8_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
                      mexp_selection* __restrict__ sel, int64_t batch, int accuracy, int rounding,
-                     int exact_s_min) {
-    using F = Group8::Frag;
+                     int exact_s_min, int32_t* __restrict__ worklist, int32_t* __restrict__ wcount) {
+    using Group8 = Group8T<kSplit>;
+    using F = typename Group8::Frag;
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -183,22 +207,16 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 5)
     const int64_t rstride = int64_t(gridDim.x) * kN8WarpsPerBlock;
     int64_t rd = int64_t(blockIdx.x) * kN8WarpsPerBlock + wib;
 
-    auto load4 = [&](int64_t r, double2 (&v)[kN8Mpw]) {
-#pragma unroll
-        for (int j = 0; j < kN8Mpw; ++j) {
-            const int64_t m = r * kN8Mpw + j;
-            v[j] = (m < batch) ? ld_stream(reinterpret_cast<const double2*>(a + m * 64) + lane)
-                               : make_double2(0.0, 0.0);
-        }
-    };
-    double2 nxt[kN8Mpw];
-    if (rd < rounds) load4(rd, nxt);
     for (; rd < rounds; rd += rstride) {
+        const int64_t m0 = rd * kN8Mpw;
+        // 4 coalesced 16-byte loads per lane (2 KB per warp) in flight at once;
+        // with ~8 warps per scheduler the loads of one warp overlap the
+        // schemes of the others
         double2 cur[kN8Mpw];
 #pragma unroll
-        for (int j = 0; j < kN8Mpw; ++j) cur[j] = nxt[j];
-        if (rd + rstride < rounds) load4(rd + rstride, nxt);
-        const int64_t m0 = rd * kN8Mpw;
+        for (int j = 0; j < kN8Mpw; ++j)
+            cur[j] = (m0 + j < batch) ? ld_stream(reinterpret_cast<const double2*>(a + (m0 + j) * 64) + lane)
+                                      : make_double2(0.0, 0.0);
 
         // all_finite (dense_matrix.cpp:54-58), one ballot per matrix
         uint32_t finbits = 0;
@@ -249,15 +267,11 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 5)
             if (m >= batch) break;
             const int inf = __shfl_sync(0xffffffffu, info, 8 * j);
             const int degree = inf & 31, s = (inf >> 5) & 0x7fff, status = inf >> 20;
-            F A;
-            // cur[j] with a runtime j: select from registers, not local memory
-            double2 v = cur[0];
-#pragma unroll
-            for (int k = 1; k < kN8Mpw; ++k)
-                if (j == k) v = cur[k];
+            g.tile = wt + j * 1024;
+            F A;  // back from the staged tile (keeps 16 registers free)
+            const double2 v = *reinterpret_cast<const double2*>(g.tile + g.st);
             A.v[0] = v.x;
             A.v[1] = v.y;
-            g.tile = wt + j * 1024;
             F X;
             if (status != MEXP_OK) {
                 X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
@@ -265,13 +279,86 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 5)
                 const bool exact = rounding == MEXP_ROUND_REFERENCE ||
                                    (rounding == MEXP_ROUND_AUTO && s >= exact_s_min);
                 g.fscale = ldexp(1.0, -s);
-                if (exact)
-                    X = run_expm<ExactOps>(g, A, degree, s);
-                else
+                if constexpr (kDefer) {
+                    if (exact) {
+                        if (lane == 0) worklist[atomicAdd(wcount, 1)] = int32_t(m);
+                        continue;
+                    }
                     X = run_expm<FastOps>(g, A, degree, s);
+                } else {
+                    if (exact)
+                        X = run_expm<ExactOps>(g, A, degree, s);
+                    else
+                        X = run_expm<FastOps>(g, A, degree, s);
+                }
             }
             st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
         }
+    }
+}
+
+// Reference-rounded 8x8 expm for the matrices listed in worklist[0, *wcount)
+// (or, with worklist == nullptr, for all of [0, batch)): one warp per matrix,
+// its own prologue (the selection records were written by the fast kernel).
+__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
+    expm8_exact_kernel(const double* __restrict__ a, double* __restrict__ out,
+                       mexp_selection* __restrict__ sel, int64_t batch, int accuracy,
+                       const int32_t* __restrict__ worklist, const int32_t* __restrict__ wcount) {
+    using Group8 = Group8T<false>;
+    using F = Group8::Frag;
+    __shared__ __align__(16) char tiles[kN8WarpsPerBlock][1024];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    Group8 g;
+    g.init(tiles[wib], lane);
+    const int64_t count = worklist ? int64_t(*wcount) : batch;
+    const int64_t stride = int64_t(gridDim.x) * kN8WarpsPerBlock;
+    for (int64_t w = int64_t(blockIdx.x) * kN8WarpsPerBlock + wib; w < count; w += stride) {
+        const int64_t m = worklist ? int64_t(worklist[w]) : w;
+        F A;
+        const double2 v = ld_stream(reinterpret_cast<const double2*>(a + m * 64) + lane);
+        A.v[0] = v.x;
+        A.v[1] = v.y;
+        const bool allfin = __all_sync(0xffffffffu, isfinite(v.x) && isfinite(v.y));
+        __syncwarp();
+        *reinterpret_cast<double2*>(g.tile + g.st) = v;
+        __syncwarp();
+        double colsum = 0.0;
+        if (lane < 8) {
+            const uint32_t half = (lane & 1) << 3;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                colsum = __dadd_rn(colsum, fabs(*reinterpret_cast<const double*>(
+                                               g.tile + unit8(i, lane >> 1) + half)));
+        }
+        unsigned long long nb = __double_as_longlong(colsum);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, nb, o);
+            nb = x > nb ? x : nb;
+        }
+        const double norm = __longlong_as_double(__shfl_sync(0xffffffffu, nb, 0));
+        Sel sl{0, 0, MEXP_OK};
+        if (!allfin)
+            sl.status = MEXP_ERR_NONFINITE;
+        else
+            sl = select_device(norm, accuracy);
+        if (!worklist && sel && lane == 0) {
+            mexp_selection rec;
+            rec.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
+            rec.degree = int16_t(sl.degree);
+            rec.s = int16_t(sl.s);
+            rec.status = sl.status;
+            sel[m] = rec;
+        }
+        F X;
+        if (sl.status != MEXP_OK) {
+            X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
+        } else {
+            g.fscale = ldexp(1.0, -sl.s);
+            X = run_expm<ExactOps>(g, A, sl.degree, sl.s);
+        }
+        st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
     }
 }
 
