@@ -298,6 +298,30 @@ int oracle_expm(const double* a, int n, int accuracy, double* out, int32_t* degr
     return ORC_OK;
 }
 
+/* T_m(2^-s A) squared s times with a GIVEN (m, s) instead of the selected
+ * one (scale, eval_taylor_new, squarings: expm.cpp:47-61). Used to check a
+ * leading block of a block-triangular matrix, whose (m, s) come from the
+ * norm of the full matrix. Returns the product count or -1. */
+int oracle_expm_forced(const double* a, int n, int degree, int s, double* out) {
+    const size_t nn = (size_t)n * n;
+    double* arg = (double*)malloc(sizeof(double) * nn);
+    double* tmp = (double*)malloc(sizeof(double) * nn);
+    if (s == 0) {
+        memcpy(arg, a, sizeof(double) * nn);
+    } else {
+        const double f = ldexp(1.0, -s);
+        for (size_t e = 0; e < nn; ++e) arg[e] = f * a[e];
+    }
+    const int products = oracle_eval_taylor_new(arg, n, degree, out);
+    for (int i = 0; i < s; ++i) {
+        oracle_matmul(out, out, tmp, n);
+        memcpy(out, tmp, sizeof(double) * nn);
+    }
+    free(arg);
+    free(tmp);
+    return products < 0 ? -1 : products + s;
+}
+
 /* Batched driver over contiguous row-major matrices; per-matrix status. */
 int oracle_expm_batch(const double* a, double* out, int n, int64_t batch, int accuracy,
                       int32_t* degree, int32_t* s, int64_t* cost_thirds, double* norm_in,

@@ -145,6 +145,16 @@ class Oracle:
         self._matmul = L.fn("matmul", None, _P, _P, _P, _I)
         self._eval = L.fn("eval_taylor_new", _I, _P, _I, _I, _P)
         self._coef = L.fn("coefficients", None, _P, _P, _P, _P)
+        self._forced = L.fn("expm_forced", _I, _P, _I, _I, _I, _P)
+
+    def expm_forced(self, a: np.ndarray, degree: int, s: int) -> np.ndarray:
+        """T_degree(2^-s A)^(2^s) with the given (m, s) (oracle_expm_forced)."""
+        a = np.ascontiguousarray(a, np.float64)
+        out = np.empty_like(a)
+        k = self._forced(_ptr(a), a.shape[0], degree, s, _ptr(out))
+        if k < 0:
+            raise ValueError("unsupported degree")
+        return out
 
     def expm_batch(self, a: np.ndarray, accuracy: int = 1) -> ExpmResult:
         batch, n, _ = a.shape

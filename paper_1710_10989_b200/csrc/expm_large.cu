@@ -1,14 +1,555 @@
+// Large-n (n > 64) fp64 expm: batched FP64 tensor-core (DMMA) GEMMs with the
+// schemes' linear combinations fused into the product epilogues.
+//
+// Pipeline per call (all matrices of the batch):
+//   1. norm_cols: one thread per column sums |a_ij| over rows i = 0..n-1 in
+//      order (kernels.cpp:44-53); the max over columns is an atomicMax on the
+//      bits (non-negative doubles order like their bit patterns); a flag
+//      records non-finite entries (dense_matrix.cpp:54-58).
+//   2. select: (m, s) per matrix (expm.cpp:11-29) -> mexp_selection records.
+//   3. one 16-byte-per-matrix device->host read of the records; the host
+//      groups the matrices by degree and by number of squarings.
+//   4. prep: W0 = 2^-s A, zero-padded to np = 128 * ceil(n / 128) (padding
+//      keeps e^A's top-left block: the padded matrix is block diagonal).
+//   5. the degree's scheme as a chain of batched GEMMs whose epilogues form
+//      the y-combinations (taylor_schemes.cpp:104-157), e.g. for T18:
+//        A2 = A*A;  A3 = A2*A;  A6 = A3*A3 -> epilogue writes B1..B5;
+//        B1*B5 -> epilogue A9 = . + B4, L = B3 + A9;  L*A9 -> T = . + B2
+//   6. s squarings (expm.cpp:31-35) as batched GEMMs over the matrices whose
+//      s reaches that step, ping-ponging two buffers;
+//   7. copy-out of each matrix's final buffer to the caller's n x n output.
+//
+// GEMM: 128x128 CTA tile, 8 warps each 64x32 (8x4 DMMA m8n8k4 tiles, 64 fp64
+// accumulators per lane), k-tiles of 16 through a 4-stage cp.async ring in
+// shared memory (rows padded to 4 (mod 16) doubles: conflict-free fragment
+// loads). One DMMA occupies an SM sub-partition's FP64 pipe for 16 cycles, so
+// 32 independent DMMAs per k-step keep all four pipes saturated.
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "expm_common.cuh"
 #include "expm_large.cuh"
 
 namespace mexp_b200 {
 
-int large_expm_f64(const double*, double*, mexp_selection*, int, int64_t, int, cudaStream_t,
-                   std::atomic<uint64_t>*) {
-    return MEXP_ERR_UNSUPPORTED;
+namespace {
+
+thread_local std::string g_err;
+
+#define LCUDA(call)                                                              \
+    do {                                                                         \
+        cudaError_t e_ = (call);                                                 \
+        if (e_ != cudaSuccess) {                                                 \
+            g_err = std::string(#call) + ": " + cudaGetErrorString(e_);          \
+            return MEXP_ERR_CUDA;                                                \
+        }                                                                        \
+    } while (0)
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
+constexpr int LDA = BK + 4;   // 20 doubles: 4 (mod 16)
+constexpr int LDB = BN + 4;   // 132 doubles: 4 (mod 16)
+constexpr int WM = 64, WN = 32, TM = WM / 8, TN = WN / 8;
+constexpr int GEMM_THREADS = 256;
+constexpr size_t STAGE_DOUBLES = size_t(BM) * LDA + size_t(BK) * LDB;
+constexpr size_t GEMM_SMEM = STAGES * STAGE_DOUBLES * sizeof(double);
+
+// Epilogues. c = the product's value at (i, j); id = (i == j); in/out are
+// the step's extra matrices at the same position.
+enum Epi : int {
+    EPI_STORE,    // o0 = c
+    EPI_ADD,      // o0 = c + in0
+    EPI_AL,       // o0 = X = c + in0 ; o1 = in1 + X        (T18: A9, L; T12: A6, L)
+    EPI_T18_B,    // c = A6; in = A, A2, A3 -> o0..o4 = B1, B2, B3, B4, B5
+    EPI_T12_B,    // c = A3; in = A, A2     -> o0..o3 = B1, B2, B3, B4
+    EPI_T8_1,     // c = A2; in = A         -> o0 = A2, o1 = x1 A + x2 A2
+    EPI_T8_2,     // c = A4; in = A, A2     -> o0 = x3 A2 + A4, o1 = x4 I + x5 A + x6 A2 + x7 A4
+    EPI_T8_3,     // c = A8; in = A, A2     -> o0 = y0 I + y1 A + y2 A2 + A8
+    EPI_T4_1,     // c = A2; in = A         -> o0 = A2, o1 = (I/2 + A/6) + A2/24
+    EPI_T4_2,     // c = inner*A2; in = A   -> o0 = (I + A) + c
+    EPI_T2,       // c = A2; in = A         -> o0 = (I + A) + A2/2
+};
+
+struct GemmArgs {
+    const double* X;
+    const double* Y;
+    const double* in[3];
+    double* out[5];
+    const int32_t* list;  // participating matrix indices (blockIdx.z)
+    int np;
+    int64_t mstride;      // np * np
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
-int squarings_f64(double*, int, int64_t, int, int, cudaStream_t, std::atomic<uint64_t>*) {
-    return MEXP_ERR_UNSUPPORTED;
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-const char* large_last_error() { return ""; }
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_pair(const GemmArgs& g, int64_t base, int row, int col,
+                                              double c0, double c1) {
+    const int64_t off = base + int64_t(row) * g.np + col;
+    const double id0 = (row == col) ? 1.0 : 0.0, id1 = (row == col + 1) ? 1.0 : 0.0;
+    auto ld = [&](int k) { return *reinterpret_cast<const double2*>(g.in[k] + off); };
+    auto st = [&](int k, double a, double b) {
+        *reinterpret_cast<double2*>(g.out[k] + off) = make_double2(a, b);
+    };
+    if constexpr (EPI == EPI_STORE) {
+        st(0, c0, c1);
+    } else if constexpr (EPI == EPI_ADD) {
+        const double2 b = ld(0);
+        st(0, c0 + b.x, c1 + b.y);
+    } else if constexpr (EPI == EPI_AL) {
+        const double2 b = ld(0), l = ld(1);
+        const double x0 = c0 + b.x, x1 = c1 + b.y;
+        st(0, x0, x1);
+        st(1, l.x + x0, l.y + x1);
+    } else if constexpr (EPI == EPI_T18_B) {
+        const double2 a = ld(0), a2 = ld(1), a3 = ld(2);
+        st(0, c_t18a[1] * a.x + c_t18a[2] * a2.x + c_t18a[3] * a3.x,
+           c_t18a[1] * a.y + c_t18a[2] * a2.y + c_t18a[3] * a3.y);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            st(1 + j,
+               c_t18b[j][0] * id0 + c_t18b[j][1] * a.x + c_t18b[j][2] * a2.x + c_t18b[j][3] * a3.x +
+                   c_t18b[j][4] * c0,
+               c_t18b[j][0] * id1 + c_t18b[j][1] * a.y + c_t18b[j][2] * a2.y + c_t18b[j][3] * a3.y +
+                   c_t18b[j][4] * c1);
+    } else if constexpr (EPI == EPI_T12_B) {
+        const double2 a = ld(0), a2 = ld(1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            st(j, c_t12[0][j] * id0 + c_t12[1][j] * a.x + c_t12[2][j] * a2.x + c_t12[3][j] * c0,
+               c_t12[0][j] * id1 + c_t12[1][j] * a.y + c_t12[2][j] * a2.y + c_t12[3][j] * c1);
+    } else if constexpr (EPI == EPI_T8_1) {
+        const double2 a = ld(0);
+        st(0, c0, c1);
+        st(1, T8C::x1 * a.x + T8C::x2 * c0, T8C::x1 * a.y + T8C::x2 * c1);
+    } else if constexpr (EPI == EPI_T8_2) {
+        const double2 a = ld(0), a2 = ld(1);
+        st(0, T8C::x3 * a2.x + c0, T8C::x3 * a2.y + c1);
+        st(1, T8C::x4 * id0 + T8C::x5 * a.x + T8C::x6 * a2.x + T8C::x7 * c0,
+           T8C::x4 * id1 + T8C::x5 * a.y + T8C::x6 * a2.y + T8C::x7 * c1);
+    } else if constexpr (EPI == EPI_T8_3) {
+        const double2 a = ld(0), a2 = ld(1);
+        st(0, T8C::y0 * id0 + T8C::y1 * a.x + T8C::y2 * a2.x + c0,
+           T8C::y0 * id1 + T8C::y1 * a.y + T8C::y2 * a2.y + c1);
+    } else if constexpr (EPI == EPI_T4_1) {
+        const double2 a = ld(0);
+        st(0, c0, c1);
+        st(1, (kInvFact2 * id0 + kInvFact3 * a.x) + kInvFact4 * c0,
+           (kInvFact2 * id1 + kInvFact3 * a.y) + kInvFact4 * c1);
+    } else if constexpr (EPI == EPI_T4_2) {
+        const double2 a = ld(0);
+        st(0, (id0 + a.x) + c0, (id1 + a.y) + c1);
+    } else if constexpr (EPI == EPI_T2) {
+        const double2 a = ld(0);
+        st(0, (id0 + a.x) + 0.5 * c0, (id1 + a.y) + 0.5 * c1);
+    }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_dmma_kernel(GemmArgs g) {
+    extern __shared__ __align__(16) double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 2, wn = warp & 3;
+    const int r = lane >> 2, q = lane & 3;
+    const int64_t mat = g.list[blockIdx.z];
+    const int64_t base = mat * g.mstride;
+    const double* X = g.X + base;
+    const double* Y = g.Y + base;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int ktiles = g.np / BK;
+
+    auto stage_a = [&](int s) { return smem + s * STAGE_DOUBLES; };
+    auto stage_b = [&](int s) { return smem + s * STAGE_DOUBLES + BM * LDA; };
+    auto load = [&](int s, int kt) {
+        double* sa = stage_a(s);
+        double* sb = stage_b(s);
+        const int k0 = kt * BK;
+#pragma unroll
+        for (int c = tid; c < BM * BK / 2; c += GEMM_THREADS) {
+            const int row = c >> 3, cc = (c & 7) * 2;
+            cp_async16(sa + row * LDA + cc, X + int64_t(m0 + row) * g.np + k0 + cc);
+        }
+#pragma unroll
+        for (int c = tid; c < BK * BN / 2; c += GEMM_THREADS) {
+            const int row = c >> 6, cc = (c & 63) * 2;
+            cp_async16(sb + row * LDB + cc, Y + int64_t(k0 + row) * g.np + n0 + cc);
+        }
+    };
+
+    double acc[TM][TN][2];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) load(s, s);
+        cp_commit();
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        const int nk = kt + STAGES - 1;
+        if (nk < ktiles) load(nk % STAGES, nk);
+        cp_commit();
+        const double* sa = stage_a(kt % STAGES) + (wm * WM + r) * LDA + q;
+        const double* sb = stage_b(kt % STAGES) + q * LDB + wn * WN + r;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[TM], bf[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) af[i] = sa[i * 8 * LDA + kk];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bf[j] = sb[kk * LDB + j * 8];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    cp_wait<0>();
+
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+            epilogue_pair<EPI>(g, base, m0 + wm * WM + i * 8 + r, n0 + wn * WN + j * 8 + 2 * q,
+                               acc[i][j][0], acc[i][j][1]);
+}
+
+// ---- prologue / epilogue kernels -------------------------------------------
+__global__ void norm_cols_kernel(const double* __restrict__ a, int n, int64_t batch,
+                                 unsigned long long* __restrict__ maxbits,
+                                 int* __restrict__ bad) {
+    const int64_t m = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= batch || j >= n) return;
+    const double* p = a + m * int64_t(n) * n + j;
+    double s = 0.0;
+    bool fin = true;
+    for (int i = 0; i < n; ++i) {
+        const double v = __ldg(p + int64_t(i) * n);
+        fin = fin && isfinite(v);
+        s = __dadd_rn(s, fabs(v));
+    }
+    if (!fin) atomicOr(bad + m, 1);
+    else atomicMax(maxbits + m, static_cast<unsigned long long>(__double_as_longlong(s)));
+}
+
+__global__ void select_kernel(const unsigned long long* __restrict__ maxbits,
+                              const int* __restrict__ bad, int64_t batch, int accuracy,
+                              mexp_selection* __restrict__ sel) {
+    const int64_t m = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (m >= batch) return;
+    mexp_selection r;
+    if (bad[m]) {
+        r.norm_in = __longlong_as_double(0x7ff8000000000000ll);
+        r.degree = 0;
+        r.s = 0;
+        r.status = MEXP_ERR_NONFINITE;
+    } else {
+        const double norm = __longlong_as_double(static_cast<long long>(maxbits[m]));
+        const Sel s = select_device(norm, accuracy);
+        r.norm_in = norm;
+        r.degree = int16_t(s.degree);
+        r.s = int16_t(s.s);
+        r.status = s.status;
+    }
+    sel[m] = r;
+}
+
+// W0[m] = 2^-s A (zero padded), for the listed matrices
+__global__ void prep_kernel(const double* __restrict__ a, double* __restrict__ w, int n, int np,
+                            const int32_t* __restrict__ list, const mexp_selection* __restrict__ sel) {
+    const int64_t m = list[blockIdx.y];
+    const double f = ldexp(1.0, -sel[m].s);
+    const int64_t total = int64_t(np) * np;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / np), j = int(e % np);
+        w[m * total + e] = (i < n && j < n) ? f * a[m * int64_t(n) * n + int64_t(i) * n + j] : 0.0;
+    }
+}
+
+// T1 = I + A (eval_taylor_new degree 1), elementwise
+__global__ void t1_kernel(const double* __restrict__ w0, double* __restrict__ r, int np,
+                          const int32_t* __restrict__ list) {
+    const int64_t m = list[blockIdx.y];
+    const int64_t total = int64_t(np) * np;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / np), j = int(e % np);
+        r[m * total + e] = (i == j ? 1.0 : 0.0) + w0[m * total + e];
+    }
+}
+
+// out[m] = top-left n x n of the final buffer (R if s is even, S if odd);
+// NaN for matrices with a per-matrix error
+__global__ void copy_out_kernel(const double* __restrict__ R, const double* __restrict__ S,
+                                double* __restrict__ out, int n, int np,
+                                const mexp_selection* __restrict__ sel, int64_t batch) {
+    const int64_t m = blockIdx.y;
+    if (m >= batch) return;
+    const mexp_selection r = sel[m];
+    const double* src = (r.s & 1) ? S : R;
+    const int64_t total = int64_t(n) * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / n), j = int(e % n);
+        out[m * total + e] = r.status != MEXP_OK ? __longlong_as_double(0x7ff8000000000000ll)
+                                                 : src[m * int64_t(np) * np + int64_t(i) * np + j];
+    }
+}
+
+template <int EPI>
+int gemm(const double* X, const double* Y, std::initializer_list<const double*> in,
+         std::initializer_list<double*> out, const int32_t* d_list, int count, int np,
+         cudaStream_t st, std::atomic<uint64_t>* launches) {
+    if (count == 0) return MEXP_OK;
+    static bool attr = [] {
+        cudaFuncSetAttribute(gemm_dmma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(GEMM_SMEM));
+        return true;
+    }();
+    (void)attr;
+    GemmArgs g{};
+    g.X = X;
+    g.Y = Y;
+    int k = 0;
+    for (auto p : in) g.in[k++] = p;
+    k = 0;
+    for (auto p : out) g.out[k++] = p;
+    g.list = d_list;
+    g.np = np;
+    g.mstride = int64_t(np) * np;
+    for (int z0 = 0; z0 < count; z0 += 65535) {
+        const int zc = std::min(count - z0, 65535);
+        g.list = d_list + z0;
+        dim3 grid(np / BN, np / BM, zc);
+        gemm_dmma_kernel<EPI><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(g);
+        launches->fetch_add(1, std::memory_order_relaxed);
+    }
+    LCUDA(cudaGetLastError());
+    return MEXP_OK;
+}
+
+struct Workspace {
+    double* buf = nullptr;
+    size_t bytes = 0;
+    int device = -1;
+};
+Workspace& workspace() {
+    static Workspace ws[16];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return ws[dev & 15];
+}
+
+}  // namespace
+
+const char* large_last_error() { return g_err.c_str(); }
+
+int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user, int n,
+                   int64_t batch, int accuracy, cudaStream_t st, std::atomic<uint64_t>* launches) {
+    const int np = (n + BM - 1) / BM * BM;
+    const int64_t mat = int64_t(np) * np;
+    constexpr int kBuffers = 6;
+    // workspace: kBuffers padded matrices per batch entry + per-matrix scratch
+    const size_t need = size_t(kBuffers) * batch * mat * sizeof(double);
+    Workspace& ws = workspace();
+    if (ws.bytes < need) {
+        if (ws.buf) LCUDA(cudaFreeAsync(ws.buf, st));
+        LCUDA(cudaMallocAsync(&ws.buf, need, st));
+        ws.bytes = need;
+    }
+    double* W[kBuffers];
+    for (int k = 0; k < kBuffers; ++k) W[k] = ws.buf + size_t(k) * batch * mat;
+
+    unsigned long long* maxbits = nullptr;
+    int* bad = nullptr;
+    mexp_selection* d_sel = d_sel_user;
+    int32_t* d_lists = nullptr;
+    LCUDA(cudaMallocAsync(&maxbits, sizeof(unsigned long long) * batch + sizeof(int) * batch, st));
+    bad = reinterpret_cast<int*>(maxbits + batch);
+    LCUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long) * batch + sizeof(int) * batch, st));
+    if (!d_sel) LCUDA(cudaMallocAsync(&d_sel, sizeof(mexp_selection) * batch, st));
+
+    norm_cols_kernel<<<dim3((n + 255) / 256, unsigned(batch)), 256, 0, st>>>(d_a, n, batch, maxbits, bad);
+    select_kernel<<<unsigned((batch + 255) / 256), 256, 0, st>>>(maxbits, bad, batch, accuracy, d_sel);
+    launches->fetch_add(2, std::memory_order_relaxed);
+
+    // (m, s) per matrix to the host: the schedule depends on them
+    std::vector<mexp_selection> h_sel(batch);
+    LCUDA(cudaMemcpyAsync(h_sel.data(), d_sel, sizeof(mexp_selection) * batch,
+                          cudaMemcpyDeviceToHost, st));
+    LCUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> by_deg[19];
+    int max_s = 0;
+    for (int64_t m = 0; m < batch; ++m) {
+        if (h_sel[m].status != MEXP_OK) continue;
+        by_deg[h_sel[m].degree].push_back(int32_t(m));
+        max_s = std::max(max_s, int(h_sel[m].s));
+    }
+    // device list layout: all OK matrices (prep), per degree, per squaring step
+    std::vector<int32_t> host_lists;
+    auto append = [&](const std::vector<int32_t>& v) {
+        const size_t off = host_lists.size();
+        host_lists.insert(host_lists.end(), v.begin(), v.end());
+        return off;
+    };
+    std::vector<int32_t> all_ok;
+    for (int d : {1, 2, 4, 8, 12, 18}) all_ok.insert(all_ok.end(), by_deg[d].begin(), by_deg[d].end());
+    const size_t off_all = append(all_ok);
+    size_t off_deg[19] = {};
+    for (int d : {1, 2, 4, 8, 12, 18}) off_deg[d] = append(by_deg[d]);
+    std::vector<size_t> off_sq(max_s + 1);
+    std::vector<int> cnt_sq(max_s + 1);
+    for (int k = 1; k <= max_s; ++k) {
+        std::vector<int32_t> v;
+        for (int32_t m : all_ok)
+            if (h_sel[m].s >= k) v.push_back(m);
+        cnt_sq[k] = int(v.size());
+        off_sq[k] = append(v);
+    }
+    if (!host_lists.empty()) {
+        LCUDA(cudaMallocAsync(&d_lists, sizeof(int32_t) * host_lists.size(), st));
+        LCUDA(cudaMemcpyAsync(d_lists, host_lists.data(), sizeof(int32_t) * host_lists.size(),
+                              cudaMemcpyHostToDevice, st));
+    }
+    auto L = [&](size_t off) { return d_lists + off; };
+    const int ew_grid = int(std::min<int64_t>(1024, (mat + 255) / 256));
+    if (!all_ok.empty()) {
+        prep_kernel<<<dim3(ew_grid, unsigned(all_ok.size())), 256, 0, st>>>(d_a, W[0], n, np,
+                                                                          L(off_all), d_sel);
+        launches->fetch_add(1, std::memory_order_relaxed);
+    }
+    // Schemes; result R of each degree, squarings ping-pong R <-> S.
+    int r;
+    double* R = W[1];
+    double* S = W[2];
+    // the same R/S for every degree so copy-out can pick by s parity: every
+    // scheme below ends in W[1] (R), S = W[2]
+    if (int c = int(by_deg[18].size())) {  // T18 (taylor_schemes.cpp:127-141)
+        const int32_t* l = L(off_deg[18]);
+        if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
+        if ((r = gemm<EPI_STORE>(W[1], W[0], {}, {W[2]}, l, c, np, st, launches))) return r;  // A3
+        // A6 = A3*A3 -> B1 W0, B2 W1, B3 W3, B4 W4, B5 W5 (A, A2 read in place)
+        if ((r = gemm<EPI_T18_B>(W[2], W[2], {W[0], W[1], W[2]}, {W[0], W[1], W[3], W[4], W[5]}, l,
+                                 c, np, st, launches)))
+            return r;
+        // B1*B5: A9 = . + B4 -> W4, L = B3 + A9 -> W3
+        if ((r = gemm<EPI_AL>(W[0], W[5], {W[4], W[3]}, {W[4], W[3]}, l, c, np, st, launches)))
+            return r;
+        // T = L*A9 + B2 -> W1 (R)
+        if ((r = gemm<EPI_ADD>(W[3], W[4], {W[1]}, {W[1]}, l, c, np, st, launches))) return r;
+    }
+    if (int c = int(by_deg[12].size())) {  // T12 (taylor_schemes.cpp:115-125)
+        const int32_t* l = L(off_deg[12]);
+        if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
+        // A3 = A2*A -> B1 W2, B2 W3, B3 W4, B4 W5
+        if ((r = gemm<EPI_T12_B>(W[1], W[0], {W[0], W[1]}, {W[2], W[3], W[4], W[5]}, l, c, np, st,
+                                 launches)))
+            return r;
+        // B4*B4: A6 = . + B3 -> W4, L = B2 + A6 -> W3
+        if ((r = gemm<EPI_AL>(W[5], W[5], {W[4], W[3]}, {W[4], W[3]}, l, c, np, st, launches)))
+            return r;
+        // T = L*A6 + B1 (W2) -> W1
+        if ((r = gemm<EPI_ADD>(W[3], W[4], {W[2]}, {W[1]}, l, c, np, st, launches))) return r;
+    }
+    if (int c = int(by_deg[8].size())) {  // T8 (taylor_schemes.cpp:104-113)
+        const int32_t* l = L(off_deg[8]);
+        // A2 -> W1, U = x1 A + x2 A2 -> W2
+        if ((r = gemm<EPI_T8_1>(W[0], W[0], {W[0]}, {W[1], W[2]}, l, c, np, st, launches))) return r;
+        // A4 = A2*U: V1 -> W3, V2 -> W4
+        if ((r = gemm<EPI_T8_2>(W[1], W[2], {W[0], W[1]}, {W[3], W[4]}, l, c, np, st, launches)))
+            return r;
+        // A8 = V1*V2 -> T -> W1 (A2 read in place)
+        if ((r = gemm<EPI_T8_3>(W[3], W[4], {W[0], W[1]}, {W[1]}, l, c, np, st, launches))) return r;
+    }
+    if (int c = int(by_deg[4].size())) {  // eval_ps(4) (taylor_schemes.cpp:158-165)
+        const int32_t* l = L(off_deg[4]);
+        // A2 -> W3, inner -> W2
+        if ((r = gemm<EPI_T4_1>(W[0], W[0], {W[0]}, {W[3], W[2]}, l, c, np, st, launches))) return r;
+        // T = (I + A) + inner*A2 -> W1
+        if ((r = gemm<EPI_T4_2>(W[2], W[3], {W[0]}, {W[1]}, l, c, np, st, launches))) return r;
+    }
+    if (int c = int(by_deg[2].size())) {  // eval_ps(2)
+        if ((r = gemm<EPI_T2>(W[0], W[0], {W[0]}, {W[1]}, L(off_deg[2]), c, np, st, launches)))
+            return r;
+    }
+    if (int c = int(by_deg[1].size())) {  // I + A
+        t1_kernel<<<dim3(ew_grid, unsigned(c)), 256, 0, st>>>(W[0], W[1], np, L(off_deg[1]));
+        launches->fetch_add(1, std::memory_order_relaxed);
+    }
+    // squarings: step k maps R -> S (k odd) or S -> R (k even)
+    for (int k = 1; k <= max_s; ++k) {
+        const double* src = (k & 1) ? R : S;
+        double* dst = (k & 1) ? S : R;
+        if ((r = gemm<EPI_STORE>(src, src, {}, {dst}, L(off_sq[k]), cnt_sq[k], np, st, launches)))
+            return r;
+    }
+    copy_out_kernel<<<dim3(ew_grid, unsigned(batch)), 256, 0, st>>>(R, S, d_out, n, np, d_sel, batch);
+    launches->fetch_add(1, std::memory_order_relaxed);
+    LCUDA(cudaGetLastError());
+    if (d_lists) LCUDA(cudaFreeAsync(d_lists, st));
+    LCUDA(cudaFreeAsync(maxbits, st));
+    if (!d_sel_user) LCUDA(cudaFreeAsync(d_sel, st));
+    return MEXP_OK;
+}
+
+int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaStream_t st,
+                  std::atomic<uint64_t>* launches) {
+    if (rounding == MEXP_ROUND_REFERENCE) return MEXP_ERR_UNSUPPORTED;
+    const int np = (n + BM - 1) / BM * BM;
+    const int64_t mat = int64_t(np) * np;
+    double* w = nullptr;
+    int32_t* list = nullptr;
+    LCUDA(cudaMallocAsync(&w, sizeof(double) * 2 * batch * mat, st));
+    LCUDA(cudaMallocAsync(&list, sizeof(int32_t) * batch, st));
+    std::vector<int32_t> idx(batch);
+    for (int64_t m = 0; m < batch; ++m) idx[m] = int32_t(m);
+    LCUDA(cudaMemcpyAsync(list, idx.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice, st));
+    // pad into w[0] with s = 0 scaling: reuse prep through a zero selection
+    mexp_selection* sel0 = nullptr;
+    LCUDA(cudaMallocAsync(&sel0, sizeof(mexp_selection) * batch, st));
+    LCUDA(cudaMemsetAsync(sel0, 0, sizeof(mexp_selection) * batch, st));
+    const int ew_grid = int(std::min<int64_t>(1024, (mat + 255) / 256));
+    prep_kernel<<<dim3(ew_grid, unsigned(batch)), 256, 0, st>>>(d_x, w, n, np, list, sel0);
+    launches->fetch_add(1, std::memory_order_relaxed);
+    double* bufs[2] = {w, w + batch * mat};
+    int r;
+    for (int k = 0; k < s; ++k)
+        if ((r = gemm<EPI_STORE>(bufs[k & 1], bufs[k & 1], {}, {bufs[(k + 1) & 1]}, list, int(batch),
+                                 np, st, launches)))
+            return r;
+    // copy back: selection with s parity = s & 1 picks bufs[s & 1] as "S"/"R"
+    LCUDA(cudaMemsetAsync(sel0, 0, sizeof(mexp_selection) * batch, st));
+    std::vector<mexp_selection> hs(batch);
+    for (auto& x : hs) {
+        x.norm_in = 0;
+        x.degree = 1;
+        x.s = int16_t(s & 1);
+        x.status = MEXP_OK;
+    }
+    LCUDA(cudaMemcpyAsync(sel0, hs.data(), sizeof(mexp_selection) * batch, cudaMemcpyHostToDevice, st));
+    copy_out_kernel<<<dim3(ew_grid, unsigned(batch)), 256, 0, st>>>(bufs[0], bufs[1], d_x, n, np,
+                                                                   sel0, batch);
+    launches->fetch_add(1, std::memory_order_relaxed);
+    LCUDA(cudaStreamSynchronize(st));  // hs must outlive the async copy
+    LCUDA(cudaFreeAsync(w, st));
+    LCUDA(cudaFreeAsync(list, st));
+    LCUDA(cudaFreeAsync(sel0, st));
+    return MEXP_OK;
+}
 
 }  // namespace mexp_b200

@@ -258,3 +258,27 @@ def test_oracle_bitwise_equals_reference(oracle, reference):
     r1 = reference.expm_batch(b, accuracy=0)
     r2 = oracle.expm_batch(b, accuracy=0)
     assert np.array_equal(r1.out, r2.out) and np.array_equal(r1.s, r2.s)
+
+
+def test_forced_selection_equals_expm(oracle):
+    from paper_1710_10989_b200 import workloads
+    a = workloads.generate("cfg2", 77, 64)
+    r = oracle.expm_batch(a)
+    for k in range(64):
+        got = oracle.expm_forced(a[k], int(r.degree[k]), int(r.s[k]))
+        assert np.array_equal(got.view(np.uint64), r.out[k].view(np.uint64))
+
+
+def test_leading_block_of_triangular_matrix(oracle):
+    """The size-independent check used for cfg5: for upper-triangular A the
+    leading k x k block of e^A is T_m(2^-s A_k)^(2^s) with the FULL matrix's
+    (m, s); in the reference's arithmetic the extra terms are exact zeros, so
+    the two agree bit for bit."""
+    rng = np.random.default_rng(8)
+    n, k = 48, 12
+    a = np.triu(rng.standard_normal((n, n)) / np.sqrt(n), 1) + np.diag(-5 * rng.uniform(size=n))
+    a *= 30.0 / l1(a)
+    r = oracle.expm_batch(a[None])
+    blk = oracle.expm_forced(a[:k, :k].copy(), int(r.degree[0]), int(r.s[0]))
+    assert np.array_equal(blk.view(np.uint64), r.out[0][:k, :k].copy().view(np.uint64))
+    assert np.all(np.tril(r.out[0], -1) == 0.0)
