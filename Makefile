@@ -14,7 +14,7 @@ OBJDIR   := build/obj
 OBJS := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(CU_SRCS)) \
         $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.cpp.o,$(CXX_SRCS))
 
-all: $(LIB) oracle
+all: $(LIB) oracle tests/cpp/dropin_kats
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -35,3 +35,6 @@ clean:
 	rm -rf build $(PKG)/_lib
 
 .PHONY: all oracle clean
+
+tests/cpp/dropin_kats: tests/cpp/dropin_kats.cpp $(LIB) $(wildcard include/mexp/*.hpp)
+	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/_lib -lmexp_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/_lib'

@@ -47,13 +47,32 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
-def fp64_peak_tflops():
-    """FP64 peak: measured on the box by profiles/fp64_peak.json if present."""
+def compute_peak_tflops(dtype):
+    """FP64 (DMMA) / FP32 (FFMA) peak measured on a B200 of this pool by
+    tools/fp64_peak.cu (profiles/fp64_peak.json); datasheet-class otherwise."""
     p = os.path.join(ROOT, "profiles", "fp64_peak.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        return d.get("dmma_tflops"), "measured"
-    return 37.2, "datasheet-class (148 SM x 64 FMA/clk x 2 x 1.965 GHz)"
+    d = json.load(open(p)) if os.path.exists(p) else {}
+    if dtype == "f64":
+        if "dmma_tflops" in d:
+            return d["dmma_tflops"], "measured (tools/fp64_peak.cu, DMMA m8n8k4)"
+        return 37.2, "datasheet-class (148 SM x 64 FMA/clk x 2 x 1.965 GHz)"
+    if "ffma_tflops" in d:
+        return d["ffma_tflops"], "measured (tools/fp64_peak.cu, FFMA)"
+    return 74.4, "datasheet-class (148 SM x 128 FFMA/clk x 2 x 1.965 GHz)"
+
+
+# Which roofline binds each workload (SURVEY.md section 8(d)): the batched
+# small-n configs are quoted against HBM (BASELINE.json), the large-n ones
+# against the FP64 tensor-core peak.
+ROOFLINE_BOUND = {"cfg1": "tensor", "cfg2": "hbm", "cfg3": "hbm", "cfg4": "tensor",
+                  "cfg5": "tensor"}
+KERNEL_NAME = {
+    "cfg1": "expm_small_f64_kernel<64,1> (1 launch per step)",
+    "cfg2": "expm8_f64_kernel (1 launch per step)",
+    "cfg3": "expm_small_f32_kernel<32,2> (1 launch per step)",
+    "cfg4": "gemm_dmma_kernel<*> chain (all launches of the step; GEMMs dominate)",
+    "cfg5": "gemm_dmma_kernel<*> chain (all launches of the step; GEMMs dominate)",
+}
 
 
 def flops_per_matrix(n, degree, s):
@@ -338,8 +357,18 @@ def run_ours(args):
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             traffic = json.load(open(tpath)).get(f"{args.config}_{args.rounding}")
-        peak64, peak64_src = fp64_peak_tflops()
+        peakc, peakc_src = compute_peak_tflops(cfg.dtype)
         tflops = flops / (ms_step * 1e-3) / 1e12
+        if ROOFLINE_BOUND[args.config] == "hbm":
+            roof = {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": hbm_gbs / peaks["hbm_gbs"], "traffic": traffic,
+                    "peak_source": peaks["source"] + " (MEASURED_PEAKS.json hbm_gbs)"}
+        else:
+            roof = {"bound": "tensor", "achieved": tflops, "peak": peakc, "unit": "TFLOP/s",
+                    "frac": tflops / peakc, "traffic": traffic, "peak_source": peakc_src}
+        roof["kernel"] = KERNEL_NAME[args.config]
+        roof["algorithmic"] = (f"{alg_bytes / 1e6:.1f} MB (A in + e^A out) and "
+                               f"{flops / 1e9:.2f} GFLOP (sum 2 n^3 (pi_m + s)) per step")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
@@ -351,12 +380,10 @@ def run_ours(args):
                        "l2": f"inputs larger than L2 ({pairs} x {2 * B * mat_bytes / 2**20:.0f} MiB "
                              f"in+out, alternating buffers)"},
             "effective_tflops": tflops,
-            "fp64_peak": {"tflops": peak64, "source": peak64_src,
-                          "frac": (tflops / peak64) if peak64 else None},
-            "roofline": {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"],
-                         "unit": "GB/s", "frac": hbm_gbs / peaks["hbm_gbs"], "traffic": traffic,
-                         "peak_source": peaks["source"],
-                         "kernel": "expm_small_f64_kernel<8,8> (1 launch per step)"},
+            "compute_peak": {"tflops": peakc, "source": peakc_src, "frac": tflops / peakc},
+            "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
+                    "frac": hbm_gbs / peaks["hbm_gbs"]},
+            "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": B * mat_bytes,
                     "d2h_bytes_per_step": B * mat_bytes + 16 * B,

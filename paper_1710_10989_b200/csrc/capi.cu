@@ -465,6 +465,23 @@ int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
     return MEXP_OK;
 }
 
+// library-internal helper for the C++ drop-in mexp::squarings (dropin.cpp)
+int mexp_b200_squarings_host(double* x, int n, int s) {
+    const int dv = device_ok();
+    if (dv != MEXP_OK) return dv;
+    double* d = nullptr;
+    const size_t bytes = sizeof(double) * size_t(n) * n;
+    MEXP_CUDA(cudaMalloc(&d, bytes));
+    int r = MEXP_OK;
+    if (cudaMemcpy(d, x, bytes, cudaMemcpyHostToDevice) != cudaSuccess) r = MEXP_ERR_CUDA;
+    if (r == MEXP_OK) r = squarings_f64(d, n, 1, s, MEXP_ROUND_AUTO, nullptr, &g_launches);
+    if (r == MEXP_OK && cudaMemcpy(x, d, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        r = MEXP_ERR_CUDA;
+    cudaFree(d);
+    if (r == MEXP_ERR_CUDA && g_last_cuda_error.empty()) g_last_cuda_error = large_last_error();
+    return r;
+}
+
 int mexp_squarings_batched(double* d_x, int n, int64_t batch, int s, int rounding,
                            void* stream) {
     if (n < 1 || batch < 0 || s < 0 || rounding < 0 || rounding > 2)

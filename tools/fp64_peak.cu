@@ -41,6 +41,21 @@ __global__ void dfma_loop(double* out, double seed) {
     if (s == 12345.0) out[threadIdx.x] = s;
 }
 
+__global__ void ffma_loop(float* out, float seed) {
+    float acc[kChains];
+    const float a = seed + threadIdx.x * 1e-7f, b = 0.999999f;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) acc[c] = c;
+    for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) acc[c] = fmaf(acc[c], b, a);
+    }
+    float s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += acc[c];
+    if (s == 12345.0f) out[threadIdx.x] = s;
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -50,7 +65,7 @@ int main() {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int threads = 256, blocks = sms * 8;
-    float best_mma = 1e30f, best_fma = 1e30f;
+    float best_mma = 1e30f, best_fma = 1e30f, best_ffma = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
         float ms;
         cudaEventRecord(e0);
@@ -65,12 +80,19 @@ int main() {
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
         if (ms < best_fma) best_fma = ms;
+        cudaEventRecord(e0);
+        ffma_loop<<<blocks, threads>>>(reinterpret_cast<float*>(out), 1.0f);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best_ffma) best_ffma = ms;
     }
     const double warps = double(blocks) * threads / 32;
     const double mma_flops = warps * kIters * kChains * 8 * 8 * 4 * 2.0;
     const double fma_flops = double(blocks) * threads * kIters * kChains * 2.0;
-    printf("{\"dmma_tflops\": %.3f, \"dfma_tflops\": %.3f, \"sm_count\": %d, \"err\": \"%s\"}\n",
-           mma_flops / (best_mma * 1e-3) / 1e12, fma_flops / (best_fma * 1e-3) / 1e12, sms,
-           cudaGetErrorString(cudaGetLastError()));
+    printf("{\"dmma_tflops\": %.3f, \"dfma_tflops\": %.3f, \"ffma_tflops\": %.3f, \"sm_count\": %d, "
+           "\"err\": \"%s\"}\n",
+           mma_flops / (best_mma * 1e-3) / 1e12, fma_flops / (best_fma * 1e-3) / 1e12,
+           fma_flops / (best_ffma * 1e-3) / 1e12, sms, cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
