@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_1710_10989_b200 import workloads  # noqa: E402
+from paper_1710_10989_b200.sharding import gather_to_root, max_over_ranks, shard_range  # noqa: E402
 
 METRIC = "matrix exponentials/sec and effective TFLOP/s (fraction of HBM/FP64 roofline)"
 UNIT = "expm/s"
@@ -268,11 +269,9 @@ def run_ours(args):
     cfg = workloads.CONFIGS[args.config]
     n = cfg.n
     B = cfg.batch
-    b0 = rank * B  # weak scaling: each rank owns a full config-sized batch
-    a_host = workloads.generate(args.config, 0, B) if world == 1 else None
-    if a_host is None:
-        # global indices beyond the config batch come from the same generator
-        a_host = _generate_shard(args.config, b0, B)
+    # weak scaling: each rank owns a full config-sized batch of its own matrices
+    shard = shard_range(rank, world, B, weak=True)
+    a_host = workloads.generate(args.config, shard.b0, shard.count)
     torch_dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
     rounding = {"auto": mx.ROUND_AUTO, "reference": mx.ROUND_REFERENCE,
                 "fast": mx.ROUND_FAST}[args.rounding]
@@ -310,9 +309,7 @@ def run_ours(args):
     launches = mx.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
         dist.barrier()
     ms_step = ms / args.steps
     value = world * B / (ms_step * 1e-3)
@@ -329,9 +326,7 @@ def run_ours(args):
         mx.expm_batched_host(h_in, h_out, accuracy=mx.Accuracy(cfg.accuracy), rounding=rounding)
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s, dev)
     e2e_value = world * B / e2e_s
 
     # ---- gather of the results to rank 0 (NCCL), timed separately ----
@@ -340,12 +335,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         dist.barrier()
         g0 = time.perf_counter()
-        if rank == 0:
-            bufs = [torch.empty_like(outs[0]) for _ in range(world)]
-            dist.gather(outs[0], bufs, dst=0)
-        else:
-            dist.gather(outs[0], None, dst=0)
+        gathered = gather_to_root(outs[0], [B] * world)
         torch.cuda.synchronize()
+        del gathered
         gather = {"ms": 1e3 * (time.perf_counter() - g0),
                   "bytes_to_root": (world - 1) * B * mat_bytes, "how": "torch.distributed.gather (NCCL)"}
 
@@ -405,22 +397,6 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def _generate_shard(key, b0, count):
-    """Rows [b0, b0+count) of the counter-based stream; beyond the config batch
-    the same generator continues (weak scaling: rank r owns its own batch)."""
-    cfg = workloads.CONFIGS[key]
-    if b0 + count <= cfg.batch:
-        return workloads.generate(key, b0, count)
-    # the generators index matrices by a 32-bit-shifted counter, so any b0 works
-    old = workloads.CONFIGS[key]
-    workloads.CONFIGS[key] = workloads.Config(old.key, old.n, b0 + count, old.dtype,
-                                              old.accuracy, old.description)
-    try:
-        return workloads.generate(key, b0, count)
-    finally:
-        workloads.CONFIGS[key] = old
 
 
 def main():

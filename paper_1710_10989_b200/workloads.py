@@ -129,7 +129,7 @@ def generate(key: str, b0: int = 0, batch: int | None = None, seed: int = 0) -> 
     if key == "cfg3":
         g = normal(seed, 30, b0, batch, nn).reshape(batch, n, n) / np.sqrt(n)
         idx = np.arange(b0, b0 + batch)
-        skew = idx >= cfg.batch // 2
+        skew = (idx % cfg.batch) >= cfg.batch // 2  # periodic: weak-scaling shards
         g[skew] = g[skew] - np.transpose(g[skew], (0, 2, 1))
         a = rescale(g, log_uniform(seed, 32, b0, batch, 1e-2, 50.0))
         return a.astype(np.float32)
@@ -161,4 +161,4 @@ def generate(key: str, b0: int = 0, batch: int | None = None, seed: int = 0) -> 
 def skew_mask(key: str, b0: int, batch: int) -> np.ndarray:
     """Which matrices of a cfg3 shard are the skew-symmetric half."""
     cfg = CONFIGS[key]
-    return np.arange(b0, b0 + batch) >= cfg.batch // 2
+    return (np.arange(b0, b0 + batch) % cfg.batch) >= cfg.batch // 2
