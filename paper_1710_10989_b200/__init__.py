@@ -244,10 +244,19 @@ def expm_batched_host(a, out=None, accuracy: Accuracy = Accuracy.Double,
         pa, po = a.data_ptr(), out.data_ptr()
         batch, n, _ = a.shape
         dt = _dtype_code(a.dtype)
-    sel = np.zeros(batch, SELECTION_DTYPE)
+    if is_np:
+        sel = np.zeros(batch, SELECTION_DTYPE)
+        psel = sel.ctypes.data
+    else:
+        # pinned like the caller's tensors: the records are DMA'd straight in
+        import torch
+        sel_t = torch.empty(batch * SELECTION_DTYPE.itemsize, dtype=torch.uint8,
+                            pin_memory=a.is_pinned())
+        sel = sel_t.numpy().view(SELECTION_DTYPE)
+        psel = sel_t.data_ptr()
     first = C.c_int64(-1)
     st = library().mexp_expm_batched_host(pa, po, dt, n, batch, int(accuracy), int(family),
-                                          int(rounding), sel.ctypes.data, C.byref(first))
+                                          int(rounding), psel, C.byref(first))
     if st not in (OK, ERR_NONFINITE, ERR_NORM_NONFINITE) or (st != OK and raise_on_error):
         _raise(st)
     return out, sel, st

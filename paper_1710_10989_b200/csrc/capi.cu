@@ -405,32 +405,62 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
     std::lock_guard<std::mutex> lock(p.mu);
     const size_t esz = dtype == MEXP_F64 ? sizeof(double) : sizeof(float);
     const size_t mat_bytes = size_t(n) * n * esz;
-    // ~24 MiB per chunk keeps three chunks in flight (H2D, compute, D2H)
-    int64_t chunk = int64_t((24u << 20) / mat_bytes);
+    // Chunks keep three in flight on three streams (H2D, compute, D2H): 16 MiB
+    // for the small-n kernels (measured best, profiles/e2e_chunks_r1.txt);
+    // 512 MiB for large n, whose ragged squaring steps need enough matrices
+    // per chunk to fill the GPU
+    static const size_t chunk_small = [] {
+        const char* e = std::getenv("MEXP_HOST_CHUNK_MB");
+        return size_t(e ? std::atoi(e) : 16) << 20;
+    }();
+    static const size_t chunk_large = [] {
+        const char* e = std::getenv("MEXP_HOST_CHUNK_MB_LARGE");
+        return size_t(e ? std::atoi(e) : 512) << 20;
+    }();
+    int64_t chunk = int64_t((n > 64 ? chunk_large : chunk_small) / mat_bytes);
     if (chunk < 1) chunk = 1;
-    if (n > 64) chunk = batch;  // the large-n engine wants the whole ragged batch
     if (chunk > batch) chunk = batch;
     int r = ensure_pipe(p, size_t(chunk) * mat_bytes, chunk);
     if (r != MEXP_OK) return r;
-    mexp_selection* hs = h_sel;
-    if (!hs) {
-        if (p.h_sel_cap < batch) {
-            if (p.h_sel_scratch) cudaFreeHost(p.h_sel_scratch);
-            p.h_sel_scratch = nullptr;
-            MEXP_CUDA(cudaMallocHost(&p.h_sel_scratch, sizeof(mexp_selection) * batch));
-            p.h_sel_cap = batch;
-        }
-        hs = p.h_sel_scratch;
+    // selection records always land in pinned scratch: an async copy into a
+    // caller's pageable buffer would block the host thread per chunk and
+    // serialise the copy pipeline; copied to h_sel once at the end
+    bool sel_pinned = false;
+    if (h_sel) {
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, h_sel) == cudaSuccess)
+            sel_pinned = attr.type == cudaMemoryTypeHost;
+        cudaGetLastError();
     }
+    if (!sel_pinned && p.h_sel_cap < batch) {
+        if (p.h_sel_scratch) cudaFreeHost(p.h_sel_scratch);
+        p.h_sel_scratch = nullptr;
+        MEXP_CUDA(cudaMallocHost(&p.h_sel_scratch, sizeof(mexp_selection) * batch));
+        p.h_sel_cap = batch;
+    }
+    mexp_selection* hs = sel_pinned ? h_sel : p.h_sel_scratch;
     const char* src = static_cast<const char*>(h_a);
     char* dst = static_cast<char*>(h_out);
-    int c = 0;
-    for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++c) {
-        const int k = c % HostPipe::kStreams;
+    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    auto h2d = [&](int64_t c) -> int {
+        const int k = int(c % HostPipe::kStreams);
+        const int64_t b0 = c * chunk;
+        const int64_t nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+        MEXP_CUDA(cudaMemcpyAsync(p.d_in[k], src + b0 * mat_bytes, nb * mat_bytes,
+                                  cudaMemcpyHostToDevice, p.st[k]));
+        return MEXP_OK;
+    };
+    // the large-n engine synchronises its stream once per call (it schedules
+    // from the selections), so the next chunk's H2D is issued before it runs
+    const bool prefetch = n > 64;
+    if (prefetch && (r = h2d(0)) != MEXP_OK) return r;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int k = int(c % HostPipe::kStreams);
+        const int64_t b0 = c * chunk;
         const int64_t nb = (batch - b0) < chunk ? (batch - b0) : chunk;
         cudaStream_t st = p.st[k];
-        MEXP_CUDA(cudaMemcpyAsync(p.d_in[k], src + b0 * mat_bytes, nb * mat_bytes,
-                                  cudaMemcpyHostToDevice, st));
+        if (!prefetch && (r = h2d(c)) != MEXP_OK) return r;
+        if (prefetch && c + 1 < nchunks && (r = h2d(c + 1)) != MEXP_OK) return r;
         r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, accuracy, rounding, p.d_sel[k], st);
         if (r != MEXP_OK) return r;
         MEXP_CUDA(cudaMemcpyAsync(dst + b0 * mat_bytes, p.d_out[k], nb * mat_bytes,
@@ -439,6 +469,7 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
                                   cudaMemcpyDeviceToHost, st));
     }
     for (int i = 0; i < HostPipe::kStreams; ++i) MEXP_CUDA(cudaStreamSynchronize(p.st[i]));
+    if (h_sel && !sel_pinned) std::memcpy(h_sel, hs, sizeof(mexp_selection) * batch);
     for (int64_t b = 0; b < batch; ++b) {
         if (hs[b].status != MEXP_OK) {
             if (first_error) *first_error = b;

@@ -17,7 +17,8 @@
 //        B1*B5 -> epilogue A9 = . + B4, L = B3 + A9;  L*A9 -> T = . + B2
 //   6. s squarings (expm.cpp:31-35) as batched GEMMs over the matrices whose
 //      s reaches that step, ping-ponging two buffers;
-//   7. copy-out of each matrix's final buffer to the caller's n x n output.
+//   7. each matrix's last GEMM writes e^A straight into the caller's output
+//      (when n is a multiple of 128; otherwise an unpad copy at the end).
 //
 // GEMM: 128x128 CTA tile, 8 warps each 64x32 (8x4 DMMA m8n8k4 tiles, 64 fp64
 // accumulators per lane), k-tiles of 16 through a 4-stage cp.async ring in
@@ -268,47 +269,47 @@ __global__ void select_kernel(const unsigned long long* __restrict__ maxbits,
     sel[m] = r;
 }
 
-// W0[m] = 2^-s A (zero padded), for the listed matrices
+// W0[m] = 2^-s A (zero padded), for the listed matrices; one block row-strip
+// per (blockIdx.x, matrix), coalesced along rows, no 64-bit divisions
 __global__ void prep_kernel(const double* __restrict__ a, double* __restrict__ w, int n, int np,
                             const int32_t* __restrict__ list, const mexp_selection* __restrict__ sel) {
     const int64_t m = list[blockIdx.y];
     const double f = ldexp(1.0, -sel[m].s);
-    const int64_t total = int64_t(np) * np;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / np), j = int(e % np);
-        w[m * total + e] = (i < n && j < n) ? f * a[m * int64_t(n) * n + int64_t(i) * n + j] : 0.0;
+    for (int i = blockIdx.x; i < np; i += gridDim.x) {
+        double* wr = w + m * int64_t(np) * np + int64_t(i) * np;
+        const double* ar = a + m * int64_t(n) * n + int64_t(i) * n;
+        for (int j = threadIdx.x; j < np; j += blockDim.x)
+            wr[j] = (i < n && j < n) ? f * ar[j] : 0.0;
     }
 }
 
-// T1 = I + A (eval_taylor_new degree 1), elementwise
-__global__ void t1_kernel(const double* __restrict__ w0, double* __restrict__ r, int np,
-                          const int32_t* __restrict__ list) {
+// T1 = I + A (eval_taylor_new degree 1), elementwise; r has row stride ldr
+// (np for the workspace, n when writing the caller's output directly)
+__global__ void t1_kernel(const double* __restrict__ w0, double* __restrict__ r, int n, int np,
+                          int ldr, const int32_t* __restrict__ list) {
     const int64_t m = list[blockIdx.y];
-    const int64_t total = int64_t(np) * np;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / np), j = int(e % np);
-        r[m * total + e] = (i == j ? 1.0 : 0.0) + w0[m * total + e];
-    }
+    for (int i = blockIdx.x; i < n; i += gridDim.x)
+        for (int j = threadIdx.x; j < n; j += blockDim.x)
+            r[m * int64_t(ldr) * ldr + int64_t(i) * ldr + j] =
+                (i == j ? 1.0 : 0.0) + w0[m * int64_t(np) * np + int64_t(i) * np + j];
 }
 
-// out[m] = top-left n x n of the final buffer (R if s is even, S if odd);
-// NaN for matrices with a per-matrix error
-__global__ void copy_out_kernel(const double* __restrict__ R, const double* __restrict__ S,
-                                double* __restrict__ out, int n, int np,
-                                const mexp_selection* __restrict__ sel, int64_t batch) {
-    const int64_t m = blockIdx.y;
-    if (m >= batch) return;
-    const mexp_selection r = sel[m];
-    const double* src = (r.s & 1) ? S : R;
+// out[m] = top-left n x n of src[m] (padded layout), for the listed matrices
+__global__ void unpad_kernel(const double* __restrict__ src, double* __restrict__ out, int n,
+                             int np, const int32_t* __restrict__ list) {
+    const int64_t m = list[blockIdx.y];
+    for (int i = blockIdx.x; i < n; i += gridDim.x)
+        for (int j = threadIdx.x; j < n; j += blockDim.x)
+            out[m * int64_t(n) * n + int64_t(i) * n + j] = src[m * int64_t(np) * np + int64_t(i) * np + j];
+}
+
+// NaN for the listed matrices (per-matrix errors: non-finite input, norm overflow)
+__global__ void nan_kernel(double* __restrict__ out, int n, const int32_t* __restrict__ list) {
+    const int64_t m = list[blockIdx.y];
     const int64_t total = int64_t(n) * n;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int i = int(e / n), j = int(e % n);
-        out[m * total + e] = r.status != MEXP_OK ? __longlong_as_double(0x7ff8000000000000ll)
-                                                 : src[m * int64_t(np) * np + int64_t(i) * np + j];
-    }
+         e += int64_t(gridDim.x) * blockDim.x)
+        out[m * total + e] = __longlong_as_double(0x7ff8000000000000ll);
 }
 
 template <int EPI>
@@ -409,36 +410,84 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     };
     std::vector<int32_t> all_ok;
     for (int d : {1, 2, 4, 8, 12, 18}) all_ok.insert(all_ok.end(), by_deg[d].begin(), by_deg[d].end());
-    const size_t off_all = append(all_ok);
     size_t off_deg[19] = {};
     for (int d : {1, 2, 4, 8, 12, 18}) off_deg[d] = append(by_deg[d]);
-    std::vector<size_t> off_sq(max_s + 1);
-    std::vector<int> cnt_sq(max_s + 1);
+    // Schemes, then squarings. Each matrix's LAST product writes its e^A
+    // straight into the caller's output when no padding is needed (np == n):
+    // the matrices with s == 0 at the scheme's final GEMM, those with s == k
+    // at squaring k. Otherwise the result stays in the workspace (R after an
+    // even number of squarings, S after an odd one) and is unpadded at the end.
+    const bool direct = (np == n);
+    double* R = W[1];
+    double* S = W[2];
+    int r;
+    // split a list into (finishing here, continuing) by s == k
+    auto split = [&](const std::vector<int32_t>& v, int k) {
+        std::vector<int32_t> fin, cont;
+        for (int32_t m : v) (int(h_sel[m].s) == k ? fin : cont).push_back(m);
+        return std::make_pair(fin, cont);
+    };
+    struct Part {
+        size_t off;
+        int count;
+    };
+    // final-step launches go to `out` for the finishing part
+    auto parts = [&](const std::vector<int32_t>& v, int k) {
+        auto fc = split(v, k);
+        if (!direct) {
+            const size_t o = append(v);
+            return std::make_pair(Part{o, 0}, Part{o, int(v.size())});
+        }
+        const size_t of = append(fc.first);
+        const size_t oc = append(fc.second);
+        return std::make_pair(Part{of, int(fc.first.size())}, Part{oc, int(fc.second.size())});
+    };
+    std::vector<std::pair<Part, Part>> deg_parts(19), sq_parts(max_s + 1);
+    for (int d : {1, 2, 4, 8, 12, 18}) deg_parts[d] = parts(by_deg[d], 0);
     for (int k = 1; k <= max_s; ++k) {
         std::vector<int32_t> v;
         for (int32_t m : all_ok)
             if (h_sel[m].s >= k) v.push_back(m);
-        cnt_sq[k] = int(v.size());
-        off_sq[k] = append(v);
+        sq_parts[k] = parts(v, k);
     }
+    std::vector<int32_t> bad_list, all_list;
+    for (int64_t m = 0; m < batch; ++m)
+        if (h_sel[m].status != MEXP_OK) bad_list.push_back(int32_t(m));
+    const size_t off_bad = append(bad_list);
+    const size_t off_all2 = append(all_ok);
     if (!host_lists.empty()) {
         LCUDA(cudaMallocAsync(&d_lists, sizeof(int32_t) * host_lists.size(), st));
         LCUDA(cudaMemcpyAsync(d_lists, host_lists.data(), sizeof(int32_t) * host_lists.size(),
                               cudaMemcpyHostToDevice, st));
     }
     auto L = [&](size_t off) { return d_lists + off; };
-    const int ew_grid = int(std::min<int64_t>(1024, (mat + 255) / 256));
+    const dim3 ew_block(256);
+    const unsigned ew_rows = unsigned(std::min(np, 64));
     if (!all_ok.empty()) {
-        prep_kernel<<<dim3(ew_grid, unsigned(all_ok.size())), 256, 0, st>>>(d_a, W[0], n, np,
-                                                                          L(off_all), d_sel);
+        prep_kernel<<<dim3(ew_rows, unsigned(all_ok.size())), ew_block, 0, st>>>(
+            d_a, W[0], n, np, L(off_all2), d_sel);
         launches->fetch_add(1, std::memory_order_relaxed);
     }
-    // Schemes; result R of each degree, squarings ping-pong R <-> S.
-    int r;
-    double* R = W[1];
-    double* S = W[2];
-    // the same R/S for every degree so copy-out can pick by s parity: every
-    // scheme below ends in W[1] (R), S = W[2]
+    // the scheme's final GEMM of degree d: finishing part -> out, rest -> R
+    auto final_step = [&](auto epi_tag, const double* X, const double* Y,
+                          std::initializer_list<const double*> in, int d) -> int {
+        constexpr int EPI = decltype(epi_tag)::value;
+        const auto& pp = deg_parts[d];
+        int rr;
+        if (pp.first.count &&
+            (rr = gemm<EPI>(X, Y, in, {d_out}, L(pp.first.off), pp.first.count, np, st, launches)))
+            return rr;
+        if (pp.second.count &&
+            (rr = gemm<EPI>(X, Y, in, {R}, L(pp.second.off), pp.second.count, np, st, launches)))
+            return rr;
+        return MEXP_OK;
+    };
+    using EStore = std::integral_constant<int, EPI_STORE>;
+    using EAdd = std::integral_constant<int, EPI_ADD>;
+    using ET8_3 = std::integral_constant<int, EPI_T8_3>;
+    using ET4_2 = std::integral_constant<int, EPI_T4_2>;
+    using ET2 = std::integral_constant<int, EPI_T2>;
+    (void)EStore{};
     if (int c = int(by_deg[18].size())) {  // T18 (taylor_schemes.cpp:127-141)
         const int32_t* l = L(off_deg[18]);
         if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
@@ -450,8 +499,8 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         // B1*B5: A9 = . + B4 -> W4, L = B3 + A9 -> W3
         if ((r = gemm<EPI_AL>(W[0], W[5], {W[4], W[3]}, {W[4], W[3]}, l, c, np, st, launches)))
             return r;
-        // T = L*A9 + B2 -> W1 (R)
-        if ((r = gemm<EPI_ADD>(W[3], W[4], {W[1]}, {W[1]}, l, c, np, st, launches))) return r;
+        // T = L*A9 + B2 (W1) -> R (= W1, read in place) or out
+        if ((r = final_step(EAdd{}, W[3], W[4], {W[1]}, 18))) return r;
     }
     if (int c = int(by_deg[12].size())) {  // T12 (taylor_schemes.cpp:115-125)
         const int32_t* l = L(off_deg[12]);
@@ -463,8 +512,8 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         // B4*B4: A6 = . + B3 -> W4, L = B2 + A6 -> W3
         if ((r = gemm<EPI_AL>(W[5], W[5], {W[4], W[3]}, {W[4], W[3]}, l, c, np, st, launches)))
             return r;
-        // T = L*A6 + B1 (W2) -> W1
-        if ((r = gemm<EPI_ADD>(W[3], W[4], {W[2]}, {W[1]}, l, c, np, st, launches))) return r;
+        // T = L*A6 + B1 (W2)
+        if ((r = final_step(EAdd{}, W[3], W[4], {W[2]}, 12))) return r;
     }
     if (int c = int(by_deg[8].size())) {  // T8 (taylor_schemes.cpp:104-113)
         const int32_t* l = L(off_deg[8]);
@@ -473,34 +522,72 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         // A4 = A2*U: V1 -> W3, V2 -> W4
         if ((r = gemm<EPI_T8_2>(W[1], W[2], {W[0], W[1]}, {W[3], W[4]}, l, c, np, st, launches)))
             return r;
-        // A8 = V1*V2 -> T -> W1 (A2 read in place)
-        if ((r = gemm<EPI_T8_3>(W[3], W[4], {W[0], W[1]}, {W[1]}, l, c, np, st, launches))) return r;
+        // A8 = V1*V2 -> T (A2 read in place)
+        if ((r = final_step(ET8_3{}, W[3], W[4], {W[0], W[1]}, 8))) return r;
     }
     if (int c = int(by_deg[4].size())) {  // eval_ps(4) (taylor_schemes.cpp:158-165)
         const int32_t* l = L(off_deg[4]);
         // A2 -> W3, inner -> W2
         if ((r = gemm<EPI_T4_1>(W[0], W[0], {W[0]}, {W[3], W[2]}, l, c, np, st, launches))) return r;
-        // T = (I + A) + inner*A2 -> W1
-        if ((r = gemm<EPI_T4_2>(W[2], W[3], {W[0]}, {W[1]}, l, c, np, st, launches))) return r;
+        // T = (I + A) + inner*A2
+        if ((r = final_step(ET4_2{}, W[2], W[3], {W[0]}, 4))) return r;
     }
-    if (int c = int(by_deg[2].size())) {  // eval_ps(2)
-        if ((r = gemm<EPI_T2>(W[0], W[0], {W[0]}, {W[1]}, L(off_deg[2]), c, np, st, launches)))
-            return r;
+    if (by_deg[2].size()) {  // eval_ps(2)
+        if ((r = final_step(ET2{}, W[0], W[0], {W[0]}, 2))) return r;
     }
-    if (int c = int(by_deg[1].size())) {  // I + A
-        t1_kernel<<<dim3(ew_grid, unsigned(c)), 256, 0, st>>>(W[0], W[1], np, L(off_deg[1]));
-        launches->fetch_add(1, std::memory_order_relaxed);
+    {  // degree 1: I + A
+        const auto& pp = deg_parts[1];
+        if (pp.first.count) {
+            t1_kernel<<<dim3(ew_rows, unsigned(pp.first.count)), ew_block, 0, st>>>(
+                W[0], d_out, n, np, n, L(pp.first.off));
+            launches->fetch_add(1, std::memory_order_relaxed);
+        }
+        if (pp.second.count) {
+            t1_kernel<<<dim3(ew_rows, unsigned(pp.second.count)), ew_block, 0, st>>>(
+                W[0], R, np, np, np, L(pp.second.off));
+            launches->fetch_add(1, std::memory_order_relaxed);
+        }
     }
     // squarings: step k maps R -> S (k odd) or S -> R (k even)
     for (int k = 1; k <= max_s; ++k) {
         const double* src = (k & 1) ? R : S;
         double* dst = (k & 1) ? S : R;
-        if ((r = gemm<EPI_STORE>(src, src, {}, {dst}, L(off_sq[k]), cnt_sq[k], np, st, launches)))
+        const auto& pp = sq_parts[k];
+        if (pp.first.count &&
+            (r = gemm<EPI_STORE>(src, src, {}, {d_out}, L(pp.first.off), pp.first.count, np, st,
+                                 launches)))
+            return r;
+        if (pp.second.count &&
+            (r = gemm<EPI_STORE>(src, src, {}, {dst}, L(pp.second.off), pp.second.count, np, st,
+                                 launches)))
             return r;
     }
-    copy_out_kernel<<<dim3(ew_grid, unsigned(batch)), 256, 0, st>>>(R, S, d_out, n, np, d_sel, batch);
-    launches->fetch_add(1, std::memory_order_relaxed);
+    if (!direct && !all_ok.empty()) {
+        // unpad from R (even s) / S (odd s)
+        std::vector<int32_t> ev, od;
+        for (int32_t m : all_ok) ((h_sel[m].s & 1) ? od : ev).push_back(m);
+        // these lists were not uploaded: append now needs a second upload
+        int32_t* d_extra = nullptr;
+        std::vector<int32_t> both(ev);
+        both.insert(both.end(), od.begin(), od.end());
+        LCUDA(cudaMallocAsync(&d_extra, sizeof(int32_t) * both.size(), st));
+        LCUDA(cudaMemcpyAsync(d_extra, both.data(), sizeof(int32_t) * both.size(),
+                              cudaMemcpyHostToDevice, st));
+        if (!ev.empty())
+            unpad_kernel<<<dim3(ew_rows, unsigned(ev.size())), ew_block, 0, st>>>(R, d_out, n, np, d_extra);
+        if (!od.empty())
+            unpad_kernel<<<dim3(ew_rows, unsigned(od.size())), ew_block, 0, st>>>(
+                S, d_out, n, np, d_extra + ev.size());
+        launches->fetch_add(2, std::memory_order_relaxed);
+        LCUDA(cudaStreamSynchronize(st));  // `both` must outlive the async copy
+        LCUDA(cudaFreeAsync(d_extra, st));
+    }
+    if (!bad_list.empty()) {
+        nan_kernel<<<dim3(64, unsigned(bad_list.size())), 256, 0, st>>>(d_out, n, L(off_bad));
+        launches->fetch_add(1, std::memory_order_relaxed);
+    }
     LCUDA(cudaGetLastError());
+    LCUDA(cudaStreamSynchronize(st));  // host lists must outlive their async upload
     if (d_lists) LCUDA(cudaFreeAsync(d_lists, st));
     LCUDA(cudaFreeAsync(maxbits, st));
     if (!d_sel_user) LCUDA(cudaFreeAsync(d_sel, st));
@@ -514,17 +601,16 @@ int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaSt
     const int64_t mat = int64_t(np) * np;
     double* w = nullptr;
     int32_t* list = nullptr;
+    mexp_selection* sel0 = nullptr;  // s = 0 records: prep copies without scaling
     LCUDA(cudaMallocAsync(&w, sizeof(double) * 2 * batch * mat, st));
     LCUDA(cudaMallocAsync(&list, sizeof(int32_t) * batch, st));
+    LCUDA(cudaMallocAsync(&sel0, sizeof(mexp_selection) * batch, st));
+    LCUDA(cudaMemsetAsync(sel0, 0, sizeof(mexp_selection) * batch, st));
     std::vector<int32_t> idx(batch);
     for (int64_t m = 0; m < batch; ++m) idx[m] = int32_t(m);
     LCUDA(cudaMemcpyAsync(list, idx.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice, st));
-    // pad into w[0] with s = 0 scaling: reuse prep through a zero selection
-    mexp_selection* sel0 = nullptr;
-    LCUDA(cudaMallocAsync(&sel0, sizeof(mexp_selection) * batch, st));
-    LCUDA(cudaMemsetAsync(sel0, 0, sizeof(mexp_selection) * batch, st));
-    const int ew_grid = int(std::min<int64_t>(1024, (mat + 255) / 256));
-    prep_kernel<<<dim3(ew_grid, unsigned(batch)), 256, 0, st>>>(d_x, w, n, np, list, sel0);
+    const unsigned rows = unsigned(std::min(np, 64));
+    prep_kernel<<<dim3(rows, unsigned(batch)), 256, 0, st>>>(d_x, w, n, np, list, sel0);
     launches->fetch_add(1, std::memory_order_relaxed);
     double* bufs[2] = {w, w + batch * mat};
     int r;
@@ -532,20 +618,10 @@ int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaSt
         if ((r = gemm<EPI_STORE>(bufs[k & 1], bufs[k & 1], {}, {bufs[(k + 1) & 1]}, list, int(batch),
                                  np, st, launches)))
             return r;
-    // copy back: selection with s parity = s & 1 picks bufs[s & 1] as "S"/"R"
-    LCUDA(cudaMemsetAsync(sel0, 0, sizeof(mexp_selection) * batch, st));
-    std::vector<mexp_selection> hs(batch);
-    for (auto& x : hs) {
-        x.norm_in = 0;
-        x.degree = 1;
-        x.s = int16_t(s & 1);
-        x.status = MEXP_OK;
-    }
-    LCUDA(cudaMemcpyAsync(sel0, hs.data(), sizeof(mexp_selection) * batch, cudaMemcpyHostToDevice, st));
-    copy_out_kernel<<<dim3(ew_grid, unsigned(batch)), 256, 0, st>>>(bufs[0], bufs[1], d_x, n, np,
-                                                                   sel0, batch);
+    unpad_kernel<<<dim3(rows, unsigned(batch)), 256, 0, st>>>(bufs[s & 1], d_x, n, np, list);
     launches->fetch_add(1, std::memory_order_relaxed);
-    LCUDA(cudaStreamSynchronize(st));  // hs must outlive the async copy
+    LCUDA(cudaGetLastError());
+    LCUDA(cudaStreamSynchronize(st));  // idx must outlive the async copy
     LCUDA(cudaFreeAsync(w, st));
     LCUDA(cudaFreeAsync(list, st));
     LCUDA(cudaFreeAsync(sel0, st));
