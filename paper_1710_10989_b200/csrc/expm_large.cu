@@ -77,7 +77,9 @@ struct GemmArgs {
     const double* Y;
     const double* in[3];
     double* out[5];
-    const int32_t* list;  // participating matrix indices (blockIdx.z)
+    double* final_out;    // the caller's e^A buffer (list entries with bit 31 set)
+    const int32_t* list;  // participating matrix indices (blockIdx.z); bit 31 set =
+                          // this is the matrix's last product: out[0] -> final_out
     int np;
     int64_t mstride;      // np * np
 };
@@ -93,13 +95,13 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 template <int EPI>
-__device__ __forceinline__ void epilogue_pair(const GemmArgs& g, int64_t base, int row, int col,
-                                              double c0, double c1) {
+__device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, int64_t base,
+                                              int row, int col, double c0, double c1) {
     const int64_t off = base + int64_t(row) * g.np + col;
     const double id0 = (row == col) ? 1.0 : 0.0, id1 = (row == col + 1) ? 1.0 : 0.0;
     auto ld = [&](int k) { return *reinterpret_cast<const double2*>(g.in[k] + off); };
     auto st = [&](int k, double a, double b) {
-        *reinterpret_cast<double2*>(g.out[k] + off) = make_double2(a, b);
+        *reinterpret_cast<double2*>((k == 0 ? out0 : g.out[k]) + off) = make_double2(a, b);
     };
     if constexpr (EPI == EPI_STORE) {
         st(0, c0, c1);
@@ -161,7 +163,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_dmma_kernel(GemmArgs g) 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 2, wn = warp & 3;
     const int r = lane >> 2, q = lane & 3;
-    const int64_t mat = g.list[blockIdx.z];
+    const int32_t entry = g.list[blockIdx.z];
+    const int64_t mat = entry & 0x7fffffff;
+    double* out0 = entry < 0 ? g.final_out : g.out[0];
     const int64_t base = mat * g.mstride;
     const double* X = g.X + base;
     const double* Y = g.Y + base;
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_dmma_kernel(GemmArgs g) 
     for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j)
-            epilogue_pair<EPI>(g, base, m0 + wm * WM + i * 8 + r, n0 + wn * WN + j * 8 + 2 * q,
+            epilogue_pair<EPI>(g, out0, base, m0 + wm * WM + i * 8 + r, n0 + wn * WN + j * 8 + 2 * q,
                                acc[i][j][0], acc[i][j][1]);
 }
 
@@ -315,7 +319,7 @@ __global__ void nan_kernel(double* __restrict__ out, int n, const int32_t* __res
 template <int EPI>
 int gemm(const double* X, const double* Y, std::initializer_list<const double*> in,
          std::initializer_list<double*> out, const int32_t* d_list, int count, int np,
-         cudaStream_t st, std::atomic<uint64_t>* launches) {
+         cudaStream_t st, std::atomic<uint64_t>* launches, double* final_out = nullptr) {
     if (count == 0) return MEXP_OK;
     static bool attr = [] {
         cudaFuncSetAttribute(gemm_dmma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -330,6 +334,7 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
     for (auto p : in) g.in[k++] = p;
     k = 0;
     for (auto p : out) g.out[k++] = p;
+    g.final_out = final_out;
     g.list = d_list;
     g.np = np;
     g.mstride = int64_t(np) * np;
@@ -431,8 +436,17 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         size_t off;
         int count;
     };
-    // final-step launches go to `out` for the finishing part
+    // one list per final step; the matrices finishing there carry bit 31 and
+    // write the caller's output (when no padding is needed)
+    auto flagged = [&](const std::vector<int32_t>& v, int k) {
+        std::vector<int32_t> f(v);
+        if (direct)
+            for (auto& m : f)
+                if (int(h_sel[m].s) == k) m = int32_t(uint32_t(m) | 0x80000000u);
+        return Part{append(f), int(f.size())};
+    };
     auto parts = [&](const std::vector<int32_t>& v, int k) {
+        // (t1 kernel only: finishing and continuing separately)
         auto fc = split(v, k);
         if (!direct) {
             const size_t o = append(v);
@@ -442,13 +456,15 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         const size_t oc = append(fc.second);
         return std::make_pair(Part{of, int(fc.first.size())}, Part{oc, int(fc.second.size())});
     };
-    std::vector<std::pair<Part, Part>> deg_parts(19), sq_parts(max_s + 1);
-    for (int d : {1, 2, 4, 8, 12, 18}) deg_parts[d] = parts(by_deg[d], 0);
+    std::vector<Part> deg_flag(19), sq_flag(max_s + 1);
+    std::vector<std::pair<Part, Part>> deg_parts(19);
+    deg_parts[1] = parts(by_deg[1], 0);
+    for (int d : {2, 4, 8, 12, 18}) deg_flag[d] = flagged(by_deg[d], 0);
     for (int k = 1; k <= max_s; ++k) {
         std::vector<int32_t> v;
         for (int32_t m : all_ok)
             if (h_sel[m].s >= k) v.push_back(m);
-        sq_parts[k] = parts(v, k);
+        sq_flag[k] = flagged(v, k);
     }
     std::vector<int32_t> bad_list, all_list;
     for (int64_t m = 0; m < batch; ++m)
@@ -468,19 +484,12 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
             d_a, W[0], n, np, L(off_all2), d_sel);
         launches->fetch_add(1, std::memory_order_relaxed);
     }
-    // the scheme's final GEMM of degree d: finishing part -> out, rest -> R
+    // the scheme's final GEMM of degree d: finishing matrices -> out, rest -> R
     auto final_step = [&](auto epi_tag, const double* X, const double* Y,
                           std::initializer_list<const double*> in, int d) -> int {
         constexpr int EPI = decltype(epi_tag)::value;
-        const auto& pp = deg_parts[d];
-        int rr;
-        if (pp.first.count &&
-            (rr = gemm<EPI>(X, Y, in, {d_out}, L(pp.first.off), pp.first.count, np, st, launches)))
-            return rr;
-        if (pp.second.count &&
-            (rr = gemm<EPI>(X, Y, in, {R}, L(pp.second.off), pp.second.count, np, st, launches)))
-            return rr;
-        return MEXP_OK;
+        const Part& pp = deg_flag[d];
+        return gemm<EPI>(X, Y, in, {R}, L(pp.off), pp.count, np, st, launches, d_out);
     };
     using EStore = std::integral_constant<int, EPI_STORE>;
     using EAdd = std::integral_constant<int, EPI_ADD>;
@@ -552,14 +561,8 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     for (int k = 1; k <= max_s; ++k) {
         const double* src = (k & 1) ? R : S;
         double* dst = (k & 1) ? S : R;
-        const auto& pp = sq_parts[k];
-        if (pp.first.count &&
-            (r = gemm<EPI_STORE>(src, src, {}, {d_out}, L(pp.first.off), pp.first.count, np, st,
-                                 launches)))
-            return r;
-        if (pp.second.count &&
-            (r = gemm<EPI_STORE>(src, src, {}, {dst}, L(pp.second.off), pp.second.count, np, st,
-                                 launches)))
+        const Part& pp = sq_flag[k];
+        if ((r = gemm<EPI_STORE>(src, src, {}, {dst}, L(pp.off), pp.count, np, st, launches, d_out)))
             return r;
     }
     if (!direct && !all_ok.empty()) {
