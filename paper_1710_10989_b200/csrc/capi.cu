@@ -121,6 +121,24 @@ int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t 
     return MEXP_OK;
 }
 
+// Ring of device counters for kernels that hand out work dynamically; a slot
+// is reused only after 4096 further launches on the device.
+int next_ticket(unsigned long long** out) {
+    constexpr int kSlots = 4096;
+    static unsigned long long* ring[16] = {};
+    static std::atomic<uint32_t> next[16];
+    int dev = 0;
+    MEXP_CUDA(cudaGetDevice(&dev));
+    dev &= 15;
+    if (!ring[dev]) {
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lock(mu);
+        if (!ring[dev]) MEXP_CUDA(cudaMalloc(&ring[dev], sizeof(unsigned long long) * kSlots));
+    }
+    *out = ring[dev] + (next[dev].fetch_add(1) % kSlots);
+    return MEXP_OK;
+}
+
 // 8x8 variant (experiments; default chosen from the measurements in
 // profiles/): bit 0 = split DMMA accumulation, bit 1 = defer reference-rounded
 // matrices to a second kernel. MEXP_N8_VARIANT overrides.
@@ -134,10 +152,10 @@ int n8_variant() {
     return v;
 }
 
-template <bool kSplit, int kDefer>
+template <bool kSplit, int kDefer, int kMinBlocks = 8>
 int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t batch,
                       int accuracy, int rounding, int smin, cudaStream_t st) {
-    auto kern = expm8_f64_kernel<kSplit, kDefer>;
+    auto kern = expm8_f64_kernel<kSplit, kDefer, kMinBlocks>;
     static int blocks_per_sm = [&] {
         int b = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * kN8WarpsPerBlock, 0);
@@ -168,8 +186,16 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
     }
     const int64_t want = (batch + 4 * kN8WarpsPerBlock - 1) / (4 * kN8WarpsPerBlock);
     const int grid = int(want < cap ? want : cap);
+    // work ticket for the dynamically distributed rounds: a slot of a
+    // persistent per-device ring, reset in stream order
+    unsigned long long* ticket = nullptr;
+    {
+        int r = next_ticket(&ticket);
+        if (r != MEXP_OK) return r;
+    }
+    MEXP_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st));
     kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding, smin,
-                                                 work, defer ? work + batch : nullptr);
+                                                 work, defer ? work + batch : nullptr, ticket);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());
     if (defer) {
@@ -190,6 +216,8 @@ int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t bat
         case 0: return launch_n8_variant<false, 0>(a, out, sel, batch, accuracy, rounding, smin, st);
         case 1: return launch_n8_variant<true, 0>(a, out, sel, batch, accuracy, rounding, smin, st);
         case 2: return launch_n8_variant<false, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 4: return launch_n8_variant<false, 0, 6>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 5: return launch_n8_variant<false, 0, 7>(a, out, sel, batch, accuracy, rounding, smin, st);
         default: return launch_n8_variant<true, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
     }
 }

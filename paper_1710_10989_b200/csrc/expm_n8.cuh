@@ -182,11 +182,12 @@ constexpr int kN8Mpw = 4;            // matrices per warp per round
 // unscaled A for sq_first).
 // kExact: 0 = exact-rounded matrices inline; 1 = fast kernel that defers the
 // matrices needing reference rounding to a worklist (expm8_exact_kernel).
-template <bool kSplit, int kDefer>
-__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
+template <bool kSplit, int kDefer, int kMinBlocks = 8>
+__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     expm8_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
                      mexp_selection* __restrict__ sel, int64_t batch, int accuracy, int rounding,
-                     int exact_s_min, int32_t* __restrict__ worklist, int32_t* __restrict__ wcount) {
+                     int exact_s_min, int32_t* __restrict__ worklist, int32_t* __restrict__ wcount,
+                     unsigned long long* __restrict__ ticket) {
     using Group8 = Group8T<kSplit>;
     using F = typename Group8::Frag;
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
@@ -207,7 +208,9 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
     const int64_t rstride = int64_t(gridDim.x) * kN8WarpsPerBlock;
     int64_t rd = int64_t(blockIdx.x) * kN8WarpsPerBlock + wib;
 
-    for (; rd < rounds; rd += rstride) {
+    // rounds are handed out dynamically after the first: per-matrix cost varies
+    // ~5x (degree, s, reference rounding), so a static stride leaves a long tail
+    for (; rd < rounds;) {
         const int64_t m0 = rd * kN8Mpw;
         // 4 coalesced 16-byte loads per lane (2 KB per warp) in flight at once;
         // with ~8 warps per scheduler the loads of one warp overlap the
@@ -294,6 +297,9 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
             }
             st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
         }
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(ticket, 1ull);
+        rd = rstride + int64_t(__shfl_sync(0xffffffffu, t, 0));
     }
 }
 

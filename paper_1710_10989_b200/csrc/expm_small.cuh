@@ -205,6 +205,9 @@ struct Group {
 // evaluated literally (the identity enters as a full matrix, c*0.0 included,
 // as in the reference). The fast path skips zero coefficients and starts an
 // identity term (ID0) from its diagonal value instead of multiplying.
+__device__ __forceinline__ bool nonzero_bits(double x) { return __double_as_longlong(x) != 0; }
+__device__ __forceinline__ bool nonzero_bits(float x) { return __float_as_int(x) != 0; }
+
 template <class Ops, class F>
 __device__ __forceinline__ void lc_rest(F&, int) {}
 template <class Ops, class F, class... R>
@@ -218,8 +221,8 @@ __device__ __forceinline__ F lc(double c0, const F& m0, R... rest) {
     F r;
 #pragma unroll
     for (int e = 0; e < F::kCount; ++e) {
-        if constexpr (!Ops::kExact && ID0)
-            r.v[e] = (m0.v[e] != T(0)) ? T(c0) : T(0);
+        if constexpr (!Ops::kExact && ID0)  // identity entry is 1.0 or +0.0: test the
+            r.v[e] = nonzero_bits(m0.v[e]) ? T(c0) : T(0);  // bits on the ALU, not the FP64 pipe
         else if (!Ops::kExact && c0 == 0.0)
             r.v[e] = T(0);
         else
