@@ -223,10 +223,28 @@ def expm_batched(a, out, sel=None, accuracy: Accuracy = Accuracy.Double,
         _raise(st)
 
 
+_PINNED_SEL = {}
+
+
+def _pinned_selection(batch: int):
+    """A cached pinned uint8 tensor holding >= batch selection records."""
+    import torch
+    buf = _PINNED_SEL.get("buf")
+    need = batch * SELECTION_DTYPE.itemsize
+    if buf is None or buf.numel() < need:
+        buf = torch.empty(need, dtype=torch.uint8, pin_memory=True)
+        _PINNED_SEL["buf"] = buf
+    return buf
+
+
 def expm_batched_host(a, out=None, accuracy: Accuracy = Accuracy.Double,
                       rounding: int = ROUND_AUTO, family: Family = Family.TaylorNew,
-                      raise_on_error: bool = True):
+                      raise_on_error: bool = True, sel_out=None):
     """Batched expm on host buffers (numpy arrays or pinned CPU torch tensors).
+
+    For torch inputs the selection records land in ``sel_out`` (a uint8
+    tensor of >= 16*batch bytes) or in a cached pinned buffer; the returned
+    records view is only valid until the next call in that case.
 
     Returns (out, selection records as a numpy structured array, status).
     """
@@ -248,11 +266,16 @@ def expm_batched_host(a, out=None, accuracy: Accuracy = Accuracy.Double,
         sel = np.zeros(batch, SELECTION_DTYPE)
         psel = sel.ctypes.data
     else:
-        # pinned like the caller's tensors: the records are DMA'd straight in
-        import torch
-        sel_t = torch.empty(batch * SELECTION_DTYPE.itemsize, dtype=torch.uint8,
-                            pin_memory=a.is_pinned())
-        sel = sel_t.numpy().view(SELECTION_DTYPE)
+        # pinned like the caller's tensors, so the records are DMA'd straight
+        # in; the pinned buffer is cached (cudaHostAlloc costs ~ms per call)
+        if sel_out is None:
+            sel_t = _pinned_selection(batch) if a.is_pinned() else None
+            if sel_t is None:
+                import torch
+                sel_t = torch.empty(batch * SELECTION_DTYPE.itemsize, dtype=torch.uint8)
+        else:
+            sel_t = sel_out
+        sel = sel_t.numpy().view(SELECTION_DTYPE)[:batch]
         psel = sel_t.data_ptr()
     first = C.c_int64(-1)
     st = library().mexp_expm_batched_host(pa, po, dt, n, batch, int(accuracy), int(family),

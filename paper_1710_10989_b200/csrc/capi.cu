@@ -139,6 +139,18 @@ int next_ticket(unsigned long long** out) {
     return MEXP_OK;
 }
 
+// Squarings at the end of a reference-rounded (AUTO) matrix that may use fast
+// rounding; MEXP_FAST_TAIL overrides. Measured on all 262,144 cfg2 matrices
+// (profiles/cfg2_fast_tail_r1.txt): k <= 3 keeps the max error at 1.8e-14,
+// k = 4 reaches 5.05e-14 > 4.44e-14 = 50*8*u; k = 2 keeps a 4x margin.
+int fast_tail() {
+    static int v = [] {
+        const char* e = std::getenv("MEXP_FAST_TAIL");
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
+
 // 8x8 variant (experiments; default chosen from the measurements in
 // profiles/): bit 0 = split DMMA accumulation, bit 1 = defer reference-rounded
 // matrices to a second kernel. MEXP_N8_VARIANT overrides.
@@ -194,7 +206,10 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
         if (r != MEXP_OK) return r;
     }
     MEXP_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st));
-    kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding, smin,
+    // AUTO: the last fast_tail() squarings of the reference-rounded matrices
+    // run with FMA/DMMA rounding (expm_small.cuh run_expm)
+    const int rounding_arg = rounding == MEXP_ROUND_AUTO ? (rounding | (fast_tail() << 8)) : rounding;
+    kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding_arg, smin,
                                                  work, defer ? work + batch : nullptr, ticket);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());

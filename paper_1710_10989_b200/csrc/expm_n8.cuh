@@ -185,12 +185,14 @@ constexpr int kN8Mpw = 4;            // matrices per warp per round
 template <bool kSplit, int kDefer, int kMinBlocks = 8>
 __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     expm8_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
-                     mexp_selection* __restrict__ sel, int64_t batch, int accuracy, int rounding,
+                     mexp_selection* __restrict__ sel, int64_t batch, int accuracy, int rounding_arg,
                      int exact_s_min, int32_t* __restrict__ worklist, int32_t* __restrict__ wcount,
                      unsigned long long* __restrict__ ticket) {
     using Group8 = Group8T<kSplit>;
     using F = typename Group8::Frag;
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
+    // rounding policy in the low byte; AUTO's fast squaring tail above it
+    const int rounding = rounding_arg & 0xff, fast_tail = rounding_arg >> 8;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     Group8 g;
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
                     X = run_expm<FastOps>(g, A, degree, s);
                 } else {
                     if (exact)
-                        X = run_expm<ExactOps>(g, A, degree, s);
+                        X = run_expm<ExactOps>(g, A, degree, s, fast_tail);
                     else
                         X = run_expm<FastOps>(g, A, degree, s);
                 }

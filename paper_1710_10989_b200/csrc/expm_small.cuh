@@ -309,7 +309,7 @@ __device__ typename G::Frag eval_taylor_new(const G& g, int degree, const typena
 
 template <class Ops, class G>
 __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename G::Frag& A0,
-                                                     int degree, int s) {
+                                                     int degree, int s, int fast_tail = 0) {
     using F = typename G::Frag;
     F A = A0;
     if (s > 0) {  // scaled(a, 2^-s) (expm.cpp:47 -> kernels.cpp:39-42), exact
@@ -318,7 +318,14 @@ __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename 
         for (int e = 0; e < G::K; ++e) A.v[e] = __dmul_rn(f, A.v[e]);
     }
     F X = eval_taylor_new<Ops>(g, degree, A);
-    for (int i = 0; i < s; ++i) X = g.template mm<Ops>(X, X, true);  // squarings, expm.cpp:31-35
+    // squarings, expm.cpp:31-35. With reference rounding, the last
+    // `fast_tail` of them may use FMA/DMMA rounding: a rounding difference
+    // made at squaring i is amplified ~2^(s-i) by the squarings after it, so
+    // the tail adds only ~(2^k - 1) ulp-level differences (the AUTO policy).
+    const int exact_until = (Ops::kExact && fast_tail < s) ? s - fast_tail : (Ops::kExact ? 0 : s);
+    int i = 0;
+    for (; i < exact_until; ++i) X = g.template mm<Ops>(X, X, true);
+    for (; i < s; ++i) X = g.template mm<FastOps>(X, X, true);
     return X;
 }
 
