@@ -309,7 +309,7 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
 
 // ---- host pipeline state: per-device streams and chunk buffers ------------
 struct HostPipe {
-    static constexpr int kStreams = 3;
+    static constexpr int kStreams = 4;
     int device = -1;
     cudaStream_t st[kStreams] = {};
     void* d_in[kStreams] = {};
@@ -318,6 +318,7 @@ struct HostPipe {
     size_t cap_bytes = 0;   // per-stream matrix buffer capacity
     int64_t cap_sel = 0;
     mexp_selection* h_sel_scratch = nullptr;  // pinned, used when the caller passes none
+    std::vector<cudaEvent_t> ev;  // one per chunk of a call: its records have landed
     int64_t h_sel_cap = 0;
     std::mutex mu;
 };
@@ -484,11 +485,42 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
     mexp_selection* hs = sel_pinned ? h_sel : p.h_sel_scratch;
     const char* src = static_cast<const char*>(h_a);
     char* dst = static_cast<char*>(h_out);
-    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    // Chunk plan. Small n: chunk sizes taper to 1/8 at both ends, so the
+    // pipeline fills (first H2D before any D2H) and drains (last D2H after
+    // the last H2D) in ~1/8 of a chunk's copy time instead of a whole one.
+    std::vector<std::pair<int64_t, int64_t>> plan;  // (b0, count)
+    {
+        std::vector<int64_t> sizes;
+        const bool taper = n <= 64 && batch >= 4 * chunk && chunk >= 8;
+        const int64_t head[3] = {chunk / 8, chunk / 4, chunk / 2};
+        int64_t left = batch;
+        if (taper)
+            for (int64_t h : head) {
+                sizes.push_back(h);
+                left -= 2 * h;  // the same again at the tail
+            }
+        while (left > 0) {
+            const int64_t c = left < chunk ? left : chunk;
+            sizes.push_back(c);
+            left -= c;
+        }
+        if (taper)
+            for (int i = 2; i >= 0; --i) sizes.push_back(head[i]);
+        int64_t b0 = 0;
+        for (int64_t c : sizes) {
+            plan.emplace_back(b0, c);
+            b0 += c;
+        }
+    }
+    const int64_t nchunks = int64_t(plan.size());
+    while (int64_t(p.ev.size()) < nchunks) {
+        cudaEvent_t e;
+        MEXP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p.ev.push_back(e);
+    }
     auto h2d = [&](int64_t c) -> int {
         const int k = int(c % HostPipe::kStreams);
-        const int64_t b0 = c * chunk;
-        const int64_t nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+        const int64_t b0 = plan[c].first, nb = plan[c].second;
         MEXP_CUDA(cudaMemcpyAsync(p.d_in[k], src + b0 * mat_bytes, nb * mat_bytes,
                                   cudaMemcpyHostToDevice, p.st[k]));
         return MEXP_OK;
@@ -499,8 +531,7 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
     if (prefetch && (r = h2d(0)) != MEXP_OK) return r;
     for (int64_t c = 0; c < nchunks; ++c) {
         const int k = int(c % HostPipe::kStreams);
-        const int64_t b0 = c * chunk;
-        const int64_t nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+        const int64_t b0 = plan[c].first, nb = plan[c].second;
         cudaStream_t st = p.st[k];
         if (!prefetch && (r = h2d(c)) != MEXP_OK) return r;
         if (prefetch && c + 1 < nchunks && (r = h2d(c + 1)) != MEXP_OK) return r;
@@ -510,16 +541,25 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
                                   cudaMemcpyDeviceToHost, st));
         MEXP_CUDA(cudaMemcpyAsync(hs + b0, p.d_sel[k], nb * sizeof(mexp_selection),
                                   cudaMemcpyDeviceToHost, st));
+        MEXP_CUDA(cudaEventRecord(p.ev[c], st));
+    }
+    // Host-side work on the records (status scan, copy to a pageable h_sel)
+    // overlaps the pipeline: chunk c is handled as soon as its records land.
+    int first_status = MEXP_OK;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        MEXP_CUDA(cudaEventSynchronize(p.ev[c]));
+        const int64_t b0 = plan[c].first, nb = plan[c].second;
+        if (h_sel && !sel_pinned) std::memcpy(h_sel + b0, hs + b0, sizeof(mexp_selection) * nb);
+        if (first_status == MEXP_OK)
+            for (int64_t b = b0; b < b0 + nb; ++b)
+                if (hs[b].status != MEXP_OK) {
+                    if (first_error) *first_error = b;
+                    first_status = hs[b].status;
+                    break;
+                }
     }
     for (int i = 0; i < HostPipe::kStreams; ++i) MEXP_CUDA(cudaStreamSynchronize(p.st[i]));
-    if (h_sel && !sel_pinned) std::memcpy(h_sel, hs, sizeof(mexp_selection) * batch);
-    for (int64_t b = 0; b < batch; ++b) {
-        if (hs[b].status != MEXP_OK) {
-            if (first_error) *first_error = b;
-            return hs[b].status;
-        }
-    }
-    return MEXP_OK;
+    return first_status;
 }
 
 int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
