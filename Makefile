@@ -14,7 +14,7 @@ OBJDIR   := build/obj
 OBJS := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(CU_SRCS)) \
         $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.cpp.o,$(CXX_SRCS))
 
-all: $(LIB) oracle tests/cpp/dropin_kats
+all: $(LIB) oracle tests/cpp/dropin_kats bin/mexp
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -38,3 +38,7 @@ clean:
 
 tests/cpp/dropin_kats: tests/cpp/dropin_kats.cpp $(LIB) $(wildcard include/mexp/*.hpp)
 	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/_lib -lmexp_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/_lib'
+
+bin/mexp: tools/cli/mexp_cli.cpp $(LIB) $(wildcard include/mexp/*.hpp)
+	@mkdir -p bin
+	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/_lib -lmexp_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)/_lib'

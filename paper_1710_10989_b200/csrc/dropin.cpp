@@ -2,7 +2,9 @@
 // implemented over the C ABI (include/mexp_b200.h). Status codes become the
 // reference's exceptions: std::invalid_argument for bad input (expm.cpp:13,38;
 // dense_matrix.cpp:15,20,30), std::runtime_error for CUDA / device failures.
+#include <charconv>
 #include <cmath>
+#include <istream>
 #include <stdexcept>
 #include <string>
 
@@ -82,6 +84,39 @@ bool DenseMatrix::all_finite() const {
     for (double v : data_)
         if (!std::isfinite(v)) return false;
     return true;
+}
+
+// ---- text I/O (host-side, dense_matrix.hpp:62-67 of the reference) ------
+DenseMatrix parse_matrix(std::istream& in) {
+    int n = 0;
+    if (!(in >> n) || n < 1) throw std::invalid_argument("bad matrix header");
+    DenseMatrix m(n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double v;
+            if (!(in >> v)) throw std::invalid_argument("truncated matrix data");
+            if (!std::isfinite(v)) throw std::invalid_argument("non-finite matrix entry");
+            m.at(i, j) = v;
+        }
+    return m;
+}
+
+std::string shortest_double(double v) {
+    char buf[64];
+    const auto res = std::to_chars(buf, buf + sizeof(buf), v);
+    return std::string(buf, res.ptr);
+}
+
+std::string format_matrix(const DenseMatrix& a) {
+    std::string out = std::to_string(a.dim()) + "\n";
+    for (int i = 0; i < a.dim(); ++i) {
+        for (int j = 0; j < a.dim(); ++j) {
+            if (j) out.push_back(' ');
+            out += shortest_double(a.at(i, j));
+        }
+        out.push_back('\n');
+    }
+    return out;
 }
 
 // ---- theta tables (theta_tables.hpp) ------------------------------------
