@@ -207,6 +207,12 @@ struct Group {
 // identity term (ID0) from its diagonal value instead of multiplying.
 __device__ __forceinline__ bool nonzero_bits(double x) { return __double_as_longlong(x) != 0; }
 __device__ __forceinline__ bool nonzero_bits(float x) { return __float_as_int(x) != 0; }
+// c where the identity entry id is 1, 0 where it is +0 (per component)
+__device__ __forceinline__ double id_term(double id, double c) { return nonzero_bits(id) ? c : 0.0; }
+__device__ __forceinline__ float id_term(float id, double c) { return nonzero_bits(id) ? float(c) : 0.f; }
+__device__ __forceinline__ float2 id_term(float2 id, double c) {
+    return make_float2(nonzero_bits(id.x) ? float(c) : 0.f, nonzero_bits(id.y) ? float(c) : 0.f);
+}
 
 template <class Ops, class F>
 __device__ __forceinline__ void lc_rest(F&, int) {}
@@ -222,9 +228,9 @@ __device__ __forceinline__ F lc(double c0, const F& m0, R... rest) {
 #pragma unroll
     for (int e = 0; e < F::kCount; ++e) {
         if constexpr (!Ops::kExact && ID0)  // identity entry is 1.0 or +0.0: test the
-            r.v[e] = nonzero_bits(m0.v[e]) ? T(c0) : T(0);  // bits on the ALU, not the FP64 pipe
+            r.v[e] = id_term(m0.v[e], c0);  // bits on the ALU, not the FP64 pipe
         else if (!Ops::kExact && c0 == 0.0)
-            r.v[e] = T(0);
+            r.v[e] = id_term(T{}, 0.0);
         else
             r.v[e] = Ops::mul(c0, m0.v[e]);
         lc_rest<Ops>(r, e, rest...);

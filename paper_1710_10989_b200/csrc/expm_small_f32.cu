@@ -1,24 +1,34 @@
 // Batched small-n expm in fp32 storage and arithmetic (BASELINE cfg3: 32x32).
 //
-// Products are FFMA on the SIMT pipes (never TF32: the tolerance is
-// 50*n*2^-24 and TF32 rounds operands to 10 bits). One group of W warps per
-// matrix; each lane owns a TR x TC register tile of every matrix variable
-// and a product C = X*Y streams X^T and Y rows out of shared memory
-// (X stored transposed so a lane's TR rows of column k are one vector load,
-// Y's TC columns of row k are TC/4 float4 loads shared by the lanes of a
-// tile column). The exact 1-norm and the (m, s) selection run in fp64 on
-// the fp32 values promoted to double, i.e. exactly the reference's norm of
-// the same data (kernels.cpp:44-53), so (m, s) match bit for bit.
+// Products are FP32 FMAs on the SIMT pipes (never TF32: the tolerance is
+// 50*n*2^-24 and TF32 rounds operands to 10 bits), issued as packed FFMA2
+// (fma.rn.f32x2, sm_100): two correctly rounded fp32 FMAs per instruction,
+// the same FMA rate as scalar FFMA (measured 71 TF either way) with half the
+// instructions, which is what this kernel is short of (issue slots and
+// instruction cache). One group of W warps per matrix; each lane owns a
+// TR x TC register tile of every matrix variable, kept as TC/2 column pairs.
+// A product C = X*Y streams X^T and Y rows out of shared memory (X stored
+// transposed so a lane's TR rows of column k are one vector load; Y's TC
+// columns of row k are TC/4 float4 loads shared by the lanes of a tile
+// column). The exact 1-norm and the (m, s) selection run in fp64 on the fp32
+// values promoted to double, i.e. exactly the reference's norm of the same
+// data (kernels.cpp:44-53), so (m, s) match bit for bit.
 #include "expm_small.cuh"
 #include "expm_small_f32.cuh"
 
 namespace mexp_b200 {
 
-struct F32Ops {
+struct F32Ops {  // on packed pairs; coefficients rounded once to fp32
     static constexpr bool kExact = false;
-    __device__ __forceinline__ static float mul(float a, float b) { return a * b; }
-    __device__ __forceinline__ static float add(float a, float b) { return a + b; }
-    __device__ __forceinline__ static float mac(float acc, float a, float b) { return fmaf(a, b, acc); }
+    __device__ __forceinline__ static float2 mul(double c, float2 m) {
+        const float cf = float(c);
+        return __fmul2_rn(make_float2(cf, cf), m);
+    }
+    __device__ __forceinline__ static float2 add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+    __device__ __forceinline__ static float2 mac(float2 acc, double c, float2 m) {
+        const float cf = float(c);
+        return __ffma2_rn(make_float2(cf, cf), m, acc);
+    }
 };
 
 template <int N> struct ShapeF32;
@@ -33,19 +43,19 @@ template <> struct ShapeF32<64> { static constexpr int W = 4, TR = 4, TC = 8, ST
 template <int N>
 struct GroupF32 {
     using S = ShapeF32<N>;
-    static constexpr int W = S::W, TR = S::TR, TC = S::TC;
+    static constexpr int W = S::W, TR = S::TR, TC = S::TC, TP = TC / 2;
     static constexpr int THREADS = 32 * W;
     static constexpr int GC = N / TC;          // tile columns
-    static constexpr int K = TR * TC;          // floats per lane per matrix
+    static constexpr int K = TR * TP;          // column pairs per lane per matrix
     static_assert((N / TR) * GC == THREADS, "tile cover");
     static constexpr int LD = N + 4;           // padded row stride (floats)
-    static constexpr int STASH_SLOT = K * THREADS;
+    static constexpr int STASH_SLOT = 2 * K * THREADS;
     static constexpr int SMEM_FLOATS = 2 * N * LD + S::STASH * STASH_SLOT + 4 * W + 4;
 
     struct Frag {
-        using T = float;
+        using T = float2;
         static constexpr int kCount = K;
-        float v[K];
+        float2 v[K];
     };
 
     float* sxt;  // X transposed: sxt[k * LD + i] = X[i][k]
@@ -54,7 +64,7 @@ struct GroupF32 {
     double* scal;  // per-warp partial results (8-byte aligned)
     int lane, warp, tid, bar_id, ti, tj;
 
-    // element e = r * TC + c of the lane's tile -> (row, col)
+    // pair p = r * TP + cp of the lane's tile -> row, first column
     __device__ __forceinline__ int row_of(int r) const { return ti * TR + r; }
     __device__ __forceinline__ int col_of(int c) const {
         if constexpr (TC >= 4)
@@ -75,7 +85,10 @@ struct GroupF32 {
 #pragma unroll
         for (int r = 0; r < TR; ++r)
 #pragma unroll
-            for (int c = 0; c < TC; ++c) f.v[r * TC + c] = (row_of(r) == col_of(c)) ? 1.f : 0.f;
+            for (int cp = 0; cp < TP; ++cp) {
+                const int c = col_of(2 * cp);
+                f.v[r * TP + cp] = make_float2(row_of(r) == c ? 1.f : 0.f, row_of(r) == c + 1 ? 1.f : 0.f);
+            }
         return f;
     }
 
@@ -87,14 +100,13 @@ struct GroupF32 {
 #pragma unroll
                 for (int h = 0; h < TC / 4; ++h) {
                     const float4 v = ld_stream(reinterpret_cast<const float4*>(m + row_of(r) * N + col_of(4 * h)));
-                    f.v[r * TC + 4 * h] = v.x;
-                    f.v[r * TC + 4 * h + 1] = v.y;
-                    f.v[r * TC + 4 * h + 2] = v.z;
-                    f.v[r * TC + 4 * h + 3] = v.w;
+                    f.v[r * TP + 2 * h] = make_float2(v.x, v.y);
+                    f.v[r * TP + 2 * h + 1] = make_float2(v.z, v.w);
                 }
             } else {
 #pragma unroll
-                for (int c = 0; c < TC; ++c) f.v[r * TC + c] = __ldcs(m + row_of(r) * N + col_of(c));
+                for (int cp = 0; cp < TP; ++cp)
+                    f.v[r * TP + cp] = __ldcs(reinterpret_cast<const float2*>(m + row_of(r) * N + col_of(2 * cp)));
             }
         }
         return f;
@@ -104,13 +116,15 @@ struct GroupF32 {
         for (int r = 0; r < TR; ++r) {
             if constexpr (TC >= 4) {
 #pragma unroll
-                for (int h = 0; h < TC / 4; ++h)
+                for (int h = 0; h < TC / 4; ++h) {
+                    const float2 a = f.v[r * TP + 2 * h], b = f.v[r * TP + 2 * h + 1];
                     st_stream(reinterpret_cast<float4*>(m + row_of(r) * N + col_of(4 * h)),
-                              make_float4(f.v[r * TC + 4 * h], f.v[r * TC + 4 * h + 1],
-                                          f.v[r * TC + 4 * h + 2], f.v[r * TC + 4 * h + 3]));
+                              make_float4(a.x, a.y, b.x, b.y));
+                }
             } else {
 #pragma unroll
-                for (int c = 0; c < TC; ++c) __stcs(m + row_of(r) * N + col_of(c), f.v[r * TC + c]);
+                for (int cp = 0; cp < TP; ++cp)
+                    __stcs(reinterpret_cast<float2*>(m + row_of(r) * N + col_of(2 * cp)), f.v[r * TP + cp]);
             }
         }
     }
@@ -118,22 +132,26 @@ struct GroupF32 {
 #pragma unroll
         for (int r = 0; r < TR; ++r)
 #pragma unroll
-            for (int c = 0; c < TC; ++c) s[row_of(r) * LD + col_of(c)] = f.v[r * TC + c];
+            for (int cp = 0; cp < TP; ++cp)
+                *reinterpret_cast<float2*>(s + row_of(r) * LD + col_of(2 * cp)) = f.v[r * TP + cp];
     }
     __device__ __forceinline__ void store_cols(float* s, const Frag& f) const {
 #pragma unroll
-        for (int c = 0; c < TC; ++c)
+        for (int cp = 0; cp < TP; ++cp)
 #pragma unroll
-            for (int r = 0; r < TR; ++r) s[col_of(c) * LD + row_of(r)] = f.v[r * TC + c];
+            for (int r = 0; r < TR; ++r) {
+                s[col_of(2 * cp) * LD + row_of(r)] = f.v[r * TP + cp].x;
+                s[(col_of(2 * cp) + 1) * LD + row_of(r)] = f.v[r * TP + cp].y;
+            }
     }
 
     __device__ __forceinline__ void put(int slot, const Frag& f) const {
-        float* p = stash + slot * STASH_SLOT;
+        float2* p = reinterpret_cast<float2*>(stash + slot * STASH_SLOT);
 #pragma unroll
         for (int e = 0; e < K; ++e) p[e * THREADS + tid] = f.v[e];
     }
     __device__ __forceinline__ Frag get(int slot) const {
-        const float* p = stash + slot * STASH_SLOT;
+        const float2* p = reinterpret_cast<const float2*>(stash + slot * STASH_SLOT);
         Frag f;
 #pragma unroll
         for (int e = 0; e < K; ++e) f.v[e] = p[e * THREADS + tid];
@@ -141,7 +159,7 @@ struct GroupF32 {
     }
 
     template <class Ops>
-    __device__ __forceinline__ Frag mm(const Frag& X, const Frag& Y, bool same) const {
+    __device__ __forceinline__ Frag mm(const Frag& X, const Frag& Y, bool) const {
         return mm_impl(X, Y, nullptr);
     }
     template <class Ops>
@@ -160,20 +178,22 @@ struct GroupF32 {
         sync();
         Frag C;
 #pragma unroll
-        for (int e = 0; e < K; ++e) C.v[e] = init ? init->v[e] : 0.f;
+        for (int e = 0; e < K; ++e) C.v[e] = init ? init->v[e] : make_float2(0.f, 0.f);
 #pragma unroll 2
         for (int k = 0; k < N; ++k) {
-            float a[TR], b[TC];
+            float a[TR];
+            float2 b[TP];
             const float* xa = sxt + k * LD + ti * TR;
 #pragma unroll
             for (int r = 0; r < TR; ++r) a[r] = xa[r];
             const float* yb = sy + k * LD;
 #pragma unroll
-            for (int c = 0; c < TC; ++c) b[c] = yb[col_of(c)];
+            for (int cp = 0; cp < TP; ++cp) b[cp] = *reinterpret_cast<const float2*>(yb + col_of(2 * cp));
 #pragma unroll
             for (int r = 0; r < TR; ++r)
 #pragma unroll
-                for (int c = 0; c < TC; ++c) C.v[r * TC + c] = fmaf(a[r], b[c], C.v[r * TC + c]);
+                for (int cp = 0; cp < TP; ++cp)
+                    C.v[r * TP + cp] = __ffma2_rn(make_float2(a[r], a[r]), b[cp], C.v[r * TP + cp]);
         }
         return C;
     }
@@ -206,7 +226,7 @@ __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
         F A = g.load_global(a + m * NN);
         bool fin = true;
 #pragma unroll
-        for (int e = 0; e < G::K; ++e) fin = fin && isfinite(A.v[e]);
+        for (int e = 0; e < G::K; ++e) fin = fin && isfinite(A.v[e].x) && isfinite(A.v[e].y);
         g.sync();
         g.store_rows(g.sy, A);
         g.sync();
@@ -249,13 +269,15 @@ __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
         }
         F X;
         if (sl.status != MEXP_OK) {
+            const float nan = __int_as_float(0x7fc00000);
 #pragma unroll
-            for (int e = 0; e < G::K; ++e) X.v[e] = __int_as_float(0x7fc00000);
+            for (int e = 0; e < G::K; ++e) X.v[e] = make_float2(nan, nan);
         } else {
             if (sl.s > 0) {  // exact scaling by 2^-s, rounded once to float
                 const double f = ldexp(1.0, -sl.s);
 #pragma unroll
-                for (int e = 0; e < G::K; ++e) A.v[e] = float(f * double(A.v[e]));
+                for (int e = 0; e < G::K; ++e)
+                    A.v[e] = make_float2(float(f * double(A.v[e].x)), float(f * double(A.v[e].y)));
             }
             X = eval_taylor_new<F32Ops>(g, sl.degree, A);
             for (int i = 0; i < sl.s; ++i) X = g.template mm<F32Ops>(X, X, true);
