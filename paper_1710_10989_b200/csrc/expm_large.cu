@@ -48,7 +48,10 @@ thread_local std::string g_err;
         }                                                                        \
     } while (0)
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
+#ifndef MEXP_GEMM_BK
+#define MEXP_GEMM_BK 32
+#endif
+constexpr int BM = 128, BN = 128, BK = MEXP_GEMM_BK, STAGES = BK == 16 ? 4 : 3;
 constexpr int LDA = BK + 4;   // 20 doubles: 4 (mod 16)
 constexpr int LDB = BN + 4;   // 132 doubles: 4 (mod 16)
 constexpr int WM = 64, WN = 32, TM = WM / 8, TN = WN / 8;
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_dmma_kernel(GemmArgs g) 
         const int k0 = kt * BK;
 #pragma unroll
         for (int c = tid; c < BM * BK / 2; c += GEMM_THREADS) {
-            const int row = c >> 3, cc = (c & 7) * 2;
+            const int row = c / (BK / 2), cc = (c % (BK / 2)) * 2;
             cp_async16(sa + row * LDA + cc, X + int64_t(m0 + row) * g.np + k0 + cc);
         }
 #pragma unroll
