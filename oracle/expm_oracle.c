@@ -2,7 +2,8 @@
  * TEST INFRASTRUCTURE ONLY — the CPU oracle. Never linked into the product.
  *
  * Plain-C restatement of the reference's scaling-and-squaring expm for
- * Family::TaylorNew (arXiv 1710.10989, reduced-product Taylor schemes), in the
+ * Family::TaylorNew (arXiv 1710.10989, reduced-product Taylor schemes) and
+ * Family::TaylorPS (Paterson-Stockmeyer Taylor, the paper's baseline), in the
  * exact arithmetic order of the reference so results are bit-identical to it
  * when compiled with -ffp-contract=off (the reference's own flag,
  * proj/CMakeLists.txt:10-11). Pinned against the compiled reference
@@ -23,6 +24,11 @@ static const int kDegrees[6] = {1, 2, 4, 8, 12, 18};
 static const int kProducts[6] = {0, 1, 2, 3, 4, 5};
 static const double kThetaDouble[6] = {2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09};
 static const double kThetaSingle[6] = {1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01};
+/* TaylorPS rows: theta_tables.cpp:53-59 */
+static const int kDegreesPS[6] = {1, 2, 4, 6, 9, 16};
+static const int kProductsPS[6] = {0, 1, 2, 3, 4, 6};
+static const double kThetaPSDouble[6] = {2.22e-16, 2.58e-8, 3.40e-4, 9.07e-3, 8.96e-2, 7.80e-1};
+static const double kThetaPSSingle[6] = {1.19e-7, 5.98e-4, 5.12e-2, 2.50e-1, 7.80e-1, 2.48};
 
 /* ---- scheme coefficients: proj/src/taylor_schemes.cpp:12-27,44-48,62-85 ---- */
 typedef struct { double x1, x2, x3, x4, x5, x6, x7, y0, y1, y2; } t8c;
@@ -121,27 +127,35 @@ static void add(const double* a, const double* b, double* out, size_t len) {
     lincomb(c, m, 2, out, len);
 }
 
-/* ---- selection: proj/src/expm.cpp:11-29 ---- */
-int oracle_select(double norm, int accuracy, int32_t* degree, int32_t* s) {
-    const double* th = accuracy == 0 ? kThetaSingle : kThetaDouble;
+/* ---- selection: proj/src/expm.cpp:11-29; family 0 TaylorNew, 1 TaylorPS ---- */
+int oracle_select_family(double norm, int accuracy, int family, int32_t* degree, int32_t* s) {
+    const int ps = family == 1;
+    const double* th = ps ? (accuracy == 0 ? kThetaPSSingle : kThetaPSDouble)
+                          : (accuracy == 0 ? kThetaSingle : kThetaDouble);
+    const int* kDeg = ps ? kDegreesPS : kDegrees;
+    const int* kProd = ps ? kProductsPS : kProducts;
     if (!isfinite(norm) || norm < 0) return ORC_NORM_NONFINITE;
     if (norm <= th[5]) {
         int best = -1;
         for (int e = 0; e < 6; ++e) {
             if (th[e] < norm) continue; /* expm.cpp:17 */
-            if (best < 0 || kProducts[e] < kProducts[best] ||
-                (kProducts[e] == kProducts[best] && kDegrees[e] < kDegrees[best]))
+            if (best < 0 || kProd[e] < kProd[best] ||
+                (kProd[e] == kProd[best] && kDeg[e] < kDeg[best]))
                 best = e;
         }
-        *degree = kDegrees[best];
+        *degree = kDeg[best];
         *s = 0;
         return ORC_OK;
     }
     int k = 0;
     while (ldexp(norm, -k) > th[5]) ++k; /* expm.cpp:27 */
-    *degree = 18;
+    *degree = kDeg[5];
     *s = k;
     return ORC_OK;
+}
+
+int oracle_select(double norm, int accuracy, int32_t* degree, int32_t* s) {
+    return oracle_select_family(norm, accuracy, 0, degree, s);
 }
 
 int oracle_products(int degree) {
@@ -217,9 +231,43 @@ static void eval_t18(const double* a, int n, double* out, double* ws) {
     add(b[0], p, out, nn); /* taylor_schemes.cpp:127-141 */
 }
 
-/* eval_ps degrees 2 and 4 (taylor_schemes.cpp:146-157). */
+/* Paterson-Stockmeyer with p = 3 (degrees 6, 9) or 4 (16): chunks
+ * g_i = sum_{k<p} A^k / (p i + k)!, t = g_{q-1} + A^p / m!, then
+ * t = g_i + t A^p down to i = 0 (taylor_schemes.cpp:159-191). */
+static void eval_ps_horner(const double* a, int n, int degree, double* out, double* ws) {
+    const size_t nn = (size_t)n * n;
+    const int p = degree == 16 ? 4 : 3, q = degree / p;
+    double* id = ws; double* a2 = ws + nn; double* a3 = ws + 2 * nn; double* a4 = ws + 3 * nn;
+    double* g[4] = {ws + 4 * nn, ws + 5 * nn, ws + 6 * nn, ws + 7 * nn};
+    double* t = ws + 8 * nn; double* prod = ws + 9 * nn; double* t2 = ws + 10 * nn;
+    memset(id, 0, sizeof(double) * nn);
+    for (int i = 0; i < n; ++i) id[(size_t)i * n + i] = 1.0;
+    oracle_matmul(a, a, a2, n);
+    oracle_matmul(a2, a, a3, n);
+    if (p == 4) oracle_matmul(a2, a2, a4, n);
+    const double* pw[4] = {id, a, a2, a3};
+    for (int i = 0; i < q; ++i) {
+        double k[4];
+        for (int j = 0; j < p; ++j) k[j] = inv_factorial(p * i + j);
+        lincomb(k, pw, p, g[i], nn);
+    }
+    const double* ap = p == 4 ? a4 : a3;
+    { const double k[2] = {1.0, inv_factorial(degree)}; const double* m[2] = {g[q - 1], ap};
+      lincomb(k, m, 2, t, nn); }
+    for (int i = q - 2; i >= 0; --i) {
+        oracle_matmul(t, ap, prod, n);
+        add(g[i], prod, i == 0 ? out : t2, nn);
+        memcpy(t, t2, sizeof(double) * nn);
+    }
+}
+
+/* eval_ps degrees 2 and 4 (taylor_schemes.cpp:146-157), 6, 9, 16 (:159-191). */
 static void eval_ps(const double* a, int n, int degree, double* out, double* ws) {
     const size_t nn = (size_t)n * n;
+    if (degree == 6 || degree == 9 || degree == 16) {
+        eval_ps_horner(a, n, degree, out, ws);
+        return;
+    }
     double* id = ws; double* a2 = ws + nn; double* f0 = ws + 2 * nn; double* f1 = ws + 3 * nn;
     double* inner = ws + 4 * nn; double* p = ws + 5 * nn;
     memset(id, 0, sizeof(double) * nn);
@@ -265,16 +313,30 @@ int oracle_eval_taylor_new(const double* a, int n, int degree, double* out) {
     return products;
 }
 
+/* eval_taylor_ps (taylor_schemes.cpp:229-232): I + A, or eval_ps. */
+int oracle_eval_taylor_ps(const double* a, int n, int degree, double* out) {
+    const size_t nn = (size_t)n * n;
+    int products = -1;
+    for (int e = 0; e < 6; ++e)
+        if (kDegreesPS[e] == degree) products = kProductsPS[e];
+    if (products < 0) return -1;
+    if (degree == 1 || degree == 2 || degree == 4) return oracle_eval_taylor_new(a, n, degree, out);
+    double* ws = (double*)malloc(sizeof(double) * nn * 12);
+    eval_ps(a, n, degree, out, ws);
+    free(ws);
+    return products;
+}
+
 /* expm driver (proj/src/expm.cpp:37-74): finite check, norm, select, exact
  * scaling by 2^-s, T_m, s squarings, report. */
-int oracle_expm(const double* a, int n, int accuracy, double* out, int32_t* degree,
-                int32_t* s, int64_t* cost_thirds, double* norm_in) {
+int oracle_expm_family(const double* a, int n, int accuracy, int family, double* out,
+                       int32_t* degree, int32_t* s, int64_t* cost_thirds, double* norm_in) {
     const size_t nn = (size_t)n * n;
     for (size_t e = 0; e < nn; ++e)
         if (!isfinite(a[e])) return ORC_NONFINITE; /* expm.cpp:38 */
     const double norm = oracle_one_norm(a, n);
     int32_t m = 0, k = 0;
-    const int st = oracle_select(norm, accuracy, &m, &k);
+    const int st = oracle_select_family(norm, accuracy, family, &m, &k);
     if (st != ORC_OK) return st;
     double* arg = (double*)malloc(sizeof(double) * nn);
     double* tmp = (double*)malloc(sizeof(double) * nn);
@@ -284,7 +346,8 @@ int oracle_expm(const double* a, int n, int accuracy, double* out, int32_t* degr
         const double f = ldexp(1.0, -k); /* scale: kernels.cpp:39-42 */
         for (size_t e = 0; e < nn; ++e) arg[e] = f * a[e];
     }
-    const int products = oracle_eval_taylor_new(arg, n, m, out);
+    const int products = family == 1 ? oracle_eval_taylor_ps(arg, n, m, out)
+                                     : oracle_eval_taylor_new(arg, n, m, out);
     for (int i = 0; i < k; ++i) { /* squarings: expm.cpp:31-35 */
         oracle_matmul(out, out, tmp, n);
         memcpy(out, tmp, sizeof(double) * nn);
@@ -296,6 +359,11 @@ int oracle_expm(const double* a, int n, int accuracy, double* out, int32_t* degr
     if (cost_thirds) *cost_thirds = 3 * (int64_t)(products + k);
     if (norm_in) *norm_in = norm;
     return ORC_OK;
+}
+
+int oracle_expm(const double* a, int n, int accuracy, double* out, int32_t* degree,
+                int32_t* s, int64_t* cost_thirds, double* norm_in) {
+    return oracle_expm_family(a, n, accuracy, 0, out, degree, s, cost_thirds, norm_in);
 }
 
 /* T_m(2^-s A) squared s times with a GIVEN (m, s) instead of the selected
@@ -323,13 +391,13 @@ int oracle_expm_forced(const double* a, int n, int degree, int s, double* out) {
 }
 
 /* Batched driver over contiguous row-major matrices; per-matrix status. */
-int oracle_expm_batch(const double* a, double* out, int n, int64_t batch, int accuracy,
-                      int32_t* degree, int32_t* s, int64_t* cost_thirds, double* norm_in,
-                      int32_t* status) {
+int oracle_expm_batch_family(const double* a, double* out, int n, int64_t batch, int accuracy,
+                             int family, int32_t* degree, int32_t* s, int64_t* cost_thirds,
+                             double* norm_in, int32_t* status) {
     const size_t nn = (size_t)n * n;
     int worst = ORC_OK;
     for (int64_t b = 0; b < batch; ++b) {
-        const int st = oracle_expm(a + b * nn, n, accuracy, out + b * nn,
+        const int st = oracle_expm_family(a + b * nn, n, accuracy, family, out + b * nn,
                                    degree ? degree + b : NULL, s ? s + b : NULL,
                                    cost_thirds ? cost_thirds + b : NULL,
                                    norm_in ? norm_in + b : NULL);
@@ -344,6 +412,13 @@ int oracle_expm_batch(const double* a, double* out, int n, int64_t batch, int ac
         if (status) status[b] = st;
     }
     return worst;
+}
+
+int oracle_expm_batch(const double* a, double* out, int n, int64_t batch, int accuracy,
+                      int32_t* degree, int32_t* s, int64_t* cost_thirds, double* norm_in,
+                      int32_t* status) {
+    return oracle_expm_batch_family(a, out, n, batch, accuracy, 0, degree, s, cost_thirds,
+                                    norm_in, status);
 }
 
 /* Coefficients as the oracle holds them (same order as ref_coefficients). */

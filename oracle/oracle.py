@@ -139,8 +139,9 @@ class Oracle:
 
     def __init__(self):
         L = _Lib(ORACLE_SO, "oracle_")
-        self._batch = L.fn("expm_batch", _I, _P, _P, _I, _I64, _I, _P, _P, _P, _P, _P)
-        self._select = L.fn("select", _I, _D, _I, _P, _P)
+        self._batch = L.fn("expm_batch_family", _I, _P, _P, _I, _I64, _I, _I, _P, _P, _P, _P, _P)
+        self._select = L.fn("select_family", _I, _D, _I, _I, _P, _P)
+        self._eval_ps = L.fn("eval_taylor_ps", _I, _P, _I, _I, _P)
         self._one_norm = L.fn("one_norm", _D, _P, _I)
         self._matmul = L.fn("matmul", None, _P, _P, _P, _I)
         self._eval = L.fn("eval_taylor_new", _I, _P, _I, _I, _P)
@@ -156,18 +157,24 @@ class Oracle:
             raise ValueError("unsupported degree")
         return out
 
-    def expm_batch(self, a: np.ndarray, accuracy: int = 1) -> ExpmResult:
+    def expm_batch(self, a: np.ndarray, accuracy: int = 1, family: int = 0) -> ExpmResult:
         batch, n, _ = a.shape
         a = np.ascontiguousarray(a.astype(np.float64, copy=False))
         out, deg, s, cost, norm, st = _alloc(batch, n)
-        ret = self._batch(_ptr(a), _ptr(out), n, batch, accuracy, _ptr(deg), _ptr(s),
+        ret = self._batch(_ptr(a), _ptr(out), n, batch, accuracy, family, _ptr(deg), _ptr(s),
                           _ptr(cost), _ptr(norm), _ptr(st))
         return ExpmResult(out, deg, s, cost, norm, st, ret)
 
-    def select(self, norm: float, accuracy: int = 1):
+    def select(self, norm: float, accuracy: int = 1, family: int = 0):
         d, s = C.c_int32(), C.c_int32()
-        st = self._select(norm, accuracy, C.byref(d), C.byref(s))
+        st = self._select(norm, accuracy, family, C.byref(d), C.byref(s))
         return st, d.value, s.value
+
+    def eval_taylor_ps(self, a, degree):
+        a = np.ascontiguousarray(a, np.float64)
+        out = np.empty_like(a)
+        k = self._eval_ps(_ptr(a), a.shape[0], degree, _ptr(out))
+        return k, out
 
     def one_norm(self, a):
         a = np.ascontiguousarray(a, np.float64)

@@ -53,6 +53,9 @@ bool valid_args(int dtype, int n, int64_t batch, int accuracy, int family, int r
            (family >= 0 && family <= 2) && (rounding >= 0 && rounding <= 2);
 }
 
+// the kernels' `acc_arg`: accuracy in the low nibble, family above it
+int acc_arg(int accuracy, int family) { return accuracy | (family << 4); }
+
 // Rounding threshold of the AUTO policy: matrices with s >= this run the
 // reference-exact arithmetic. Each squaring roughly doubles the relative
 // difference between two roundings of T_m, while the tolerance 50*n*u grows
@@ -99,11 +102,11 @@ int num_sms() {
     return sms;
 }
 
-template <int N, int GPC>
+template <int N, int GPC, int kFamily>
 int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
                      int accuracy, int rounding, int smin, cudaStream_t st) {
     using G = Group<N>;
-    auto kern = expm_small_f64_kernel<N, GPC>;
+    auto kern = expm_small_f64_kernel<N, GPC, kFamily>;
     const size_t smem = size_t(G::SMEM_DOUBLES) * GPC * sizeof(double);
     static int blocks_per_sm = [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -164,18 +167,19 @@ int n8_variant() {
     return v;
 }
 
-template <bool kSplit, int kDefer, int kMinBlocks = 8>
+template <bool kSplit, int kDefer, int kMinBlocks = 8, int kFamily = MEXP_FAMILY_TAYLOR_NEW>
 int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t batch,
                       int accuracy, int rounding, int smin, cudaStream_t st) {
-    auto kern = expm8_f64_kernel<kSplit, kDefer, kMinBlocks>;
+    auto kern = expm8_f64_kernel<kSplit, kDefer, kMinBlocks, kFamily>;
+    auto exact_kern = expm8_exact_kernel<kFamily>;
     static int blocks_per_sm = [&] {
         int b = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * kN8WarpsPerBlock, 0);
         return b > 0 ? b : 1;
     }();
-    static int exact_bps = [] {
+    static int exact_bps = [&] {
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, expm8_exact_kernel, 32 * kN8WarpsPerBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, exact_kern, 32 * kN8WarpsPerBlock, 0);
         return b > 0 ? b : 1;
     }();
     const int64_t cap = int64_t(blocks_per_sm) * num_sms();
@@ -184,8 +188,8 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
         const int64_t want = (batch + kN8WarpsPerBlock - 1) / kN8WarpsPerBlock;
         const int64_t ecap = int64_t(exact_bps) * num_sms();
         const int grid = int(want < ecap ? want : ecap);
-        expm8_exact_kernel<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy,
-                                                                   nullptr, nullptr);
+        exact_kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, nullptr,
+                                                           nullptr);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         MEXP_CUDA(cudaGetLastError());
         return MEXP_OK;
@@ -215,8 +219,8 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
     MEXP_CUDA(cudaGetLastError());
     if (defer) {
         const int egrid = int(int64_t(exact_bps) * num_sms());
-        expm8_exact_kernel<<<egrid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy,
-                                                                    work, work + batch);
+        exact_kern<<<egrid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, work,
+                                                            work + batch);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         MEXP_CUDA(cudaGetLastError());
         MEXP_CUDA(cudaFreeAsync(work, st));
@@ -224,9 +228,23 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
     return MEXP_OK;
 }
 
+// `accuracy` here and below is the kernels' acc_arg (mexp_accuracy | family << 4)
+template <int N, int GPC>
+int launch_small_family(const double* a, double* out, mexp_selection* sel, int64_t batch,
+                        int accuracy, int rounding, int smin, cudaStream_t st) {
+    if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)
+        return launch_small_f64<N, GPC, MEXP_FAMILY_TAYLOR_PS>(a, out, sel, batch, accuracy,
+                                                               rounding, smin, st);
+    return launch_small_f64<N, GPC, MEXP_FAMILY_TAYLOR_NEW>(a, out, sel, batch, accuracy, rounding,
+                                                            smin, st);
+}
+
 int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
                   int accuracy, int rounding, int smin, cudaStream_t st) {
     if (batch == 0) return MEXP_OK;
+    if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)  // the default variant only
+        return launch_n8_variant<false, 0, 8, MEXP_FAMILY_TAYLOR_PS>(a, out, sel, batch, accuracy,
+                                                                     rounding, smin, st);
     switch (n8_variant()) {
         case 0: return launch_n8_variant<false, 0>(a, out, sel, batch, accuracy, rounding, smin, st);
         case 1: return launch_n8_variant<true, 0>(a, out, sel, batch, accuracy, rounding, smin, st);
@@ -241,9 +259,9 @@ int run_small_f64(const double* a, double* out, mexp_selection* sel, int np, int
                   int accuracy, int rounding, int smin, cudaStream_t st) {
     switch (np) {
         case 8: return launch_n8_f64(a, out, sel, batch, accuracy, rounding, smin, st);
-        case 16: return launch_small_f64<16, 4>(a, out, sel, batch, accuracy, rounding, smin, st);
-        case 32: return launch_small_f64<32, 2>(a, out, sel, batch, accuracy, rounding, smin, st);
-        case 64: return launch_small_f64<64, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 16: return launch_small_family<16, 4>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 32: return launch_small_family<32, 2>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 64: return launch_small_family<64, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
     }
     return MEXP_ERR_UNSUPPORTED;
 }
@@ -354,11 +372,6 @@ int ensure_pipe(HostPipe& p, size_t bytes, int64_t sels) {
     return MEXP_OK;
 }
 
-const double kThetaHost[2][6] = {
-    {1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01},
-    {2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09},
-};
-
 }  // namespace
 
 extern "C" {
@@ -399,12 +412,14 @@ int mexp_selection_table(int accuracy, int family, int32_t* degrees, int32_t* pr
                          double* thetas, int cap) {
     if (accuracy != MEXP_ACCURACY_SINGLE && accuracy != MEXP_ACCURACY_DOUBLE)
         return -MEXP_ERR_INVALID_ARGUMENT;
-    if (family != MEXP_FAMILY_TAYLOR_NEW) return -MEXP_ERR_UNSUPPORTED;
+    if (family != MEXP_FAMILY_TAYLOR_NEW && family != MEXP_FAMILY_TAYLOR_PS)
+        return -MEXP_ERR_UNSUPPORTED;
+    const bool ps = family == MEXP_FAMILY_TAYLOR_PS;
     int k = 0;
     for (int e = 0; e < kNumEntries && k < cap; ++e, ++k) {
-        degrees[k] = degree_of(e);
-        products[k] = products_of_entry(e);
-        thetas[k] = kThetaHost[accuracy][e];
+        degrees[k] = ps ? ps_degree_of(e) : degree_of(e);
+        products[k] = products_of(family, degrees[k]);
+        thetas[k] = theta_entry(family, accuracy, e);
     }
     return k;
 }
@@ -414,8 +429,9 @@ int mexp_selection_table(int accuracy, int family, int32_t* degrees, int32_t* pr
 int mexp_select(double norm, int accuracy, int family, int32_t* degree, int32_t* s) {
     if (accuracy != MEXP_ACCURACY_SINGLE && accuracy != MEXP_ACCURACY_DOUBLE)
         return MEXP_ERR_INVALID_ARGUMENT;
-    if (family != MEXP_FAMILY_TAYLOR_NEW) return MEXP_ERR_UNSUPPORTED;
-    const Sel r = select_device(norm, accuracy);
+    if (family != MEXP_FAMILY_TAYLOR_NEW && family != MEXP_FAMILY_TAYLOR_PS)
+        return MEXP_ERR_UNSUPPORTED;
+    const Sel r = select_device(norm, accuracy, family);
     if (r.status != MEXP_OK) return r.status;
     *degree = r.degree;
     *s = r.s;
@@ -426,11 +442,11 @@ int mexp_expm_batched(const void* d_a, void* d_out, int dtype, int n, int64_t ba
                       int accuracy, int family, int rounding, mexp_selection* d_sel,
                       void* stream) {
     if (!valid_args(dtype, n, batch, accuracy, family, rounding)) return MEXP_ERR_INVALID_ARGUMENT;
-    if (family != MEXP_FAMILY_TAYLOR_NEW) return MEXP_ERR_UNSUPPORTED;
+    if (family == MEXP_FAMILY_PADE) return MEXP_ERR_UNSUPPORTED;
     if (batch > 0 && (!d_a || !d_out)) return MEXP_ERR_INVALID_ARGUMENT;
     const int dv = device_ok();
     if (dv != MEXP_OK) return dv;
-    return expm_device(d_a, d_out, dtype, n, batch, accuracy, rounding, d_sel,
+    return expm_device(d_a, d_out, dtype, n, batch, acc_arg(accuracy, family), rounding, d_sel,
                        static_cast<cudaStream_t>(stream));
 }
 
@@ -438,7 +454,7 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
                            int accuracy, int family, int rounding, mexp_selection* h_sel,
                            int64_t* first_error) {
     if (!valid_args(dtype, n, batch, accuracy, family, rounding)) return MEXP_ERR_INVALID_ARGUMENT;
-    if (family != MEXP_FAMILY_TAYLOR_NEW) return MEXP_ERR_UNSUPPORTED;
+    if (family == MEXP_FAMILY_PADE) return MEXP_ERR_UNSUPPORTED;
     if (first_error) *first_error = -1;
     if (batch == 0) return MEXP_OK;
     if (!h_a || !h_out) return MEXP_ERR_INVALID_ARGUMENT;
@@ -535,7 +551,8 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
         cudaStream_t st = p.st[k];
         if (!prefetch && (r = h2d(c)) != MEXP_OK) return r;
         if (prefetch && c + 1 < nchunks && (r = h2d(c + 1)) != MEXP_OK) return r;
-        r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, accuracy, rounding, p.d_sel[k], st);
+        r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, acc_arg(accuracy, family), rounding,
+                        p.d_sel[k], st);
         if (r != MEXP_OK) return r;
         MEXP_CUDA(cudaMemcpyAsync(dst + b0 * mat_bytes, p.d_out[k], nb * mat_bytes,
                                   cudaMemcpyDeviceToHost, st));
@@ -573,7 +590,7 @@ int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
         report->degree = sel.degree;
         report->s = sel.s;
         report->reserved = 0;
-        report->cost_thirds = 3 * int64_t(products_of_degree(sel.degree) + sel.s);
+        report->cost_thirds = 3 * int64_t(products_of(family, sel.degree) + sel.s);
         report->norm_in = sel.norm_in;
     }
     return MEXP_OK;

@@ -39,8 +39,8 @@ int checked_dim(int n) {
 }
 
 SelectionTable load_table(Family f, Accuracy u) {
-    if (f != Family::TaylorNew)
-        throw std::invalid_argument("only the taylor-new family runs on the B200 path");
+    if (f == Family::PadeDiagonal)
+        throw std::invalid_argument("the pade family does not run on the B200 path");
     int32_t d[16], p[16];
     double t[16];
     const int k = mexp_selection_table(int(u), int(f), d, p, t, 16);
@@ -142,8 +142,11 @@ bool parse_family(std::string_view name, Family& out) {
 const SelectionTable& selection_table(Family f, Accuracy u) {
     static const SelectionTable single = load_table(Family::TaylorNew, Accuracy::Single);
     static const SelectionTable dbl = load_table(Family::TaylorNew, Accuracy::Double);
-    if (f != Family::TaylorNew)
-        throw std::invalid_argument("only the taylor-new family runs on the B200 path");
+    static const SelectionTable ps_single = load_table(Family::TaylorPS, Accuracy::Single);
+    static const SelectionTable ps_dbl = load_table(Family::TaylorPS, Accuracy::Double);
+    if (f == Family::PadeDiagonal)
+        throw std::invalid_argument("the pade family does not run on the B200 path");
+    if (f == Family::TaylorPS) return u == Accuracy::Single ? ps_single : ps_dbl;
     return u == Accuracy::Single ? single : dbl;
 }
 

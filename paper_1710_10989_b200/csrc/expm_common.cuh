@@ -78,6 +78,14 @@ __device__ constexpr double c_t18b[4][5] = {
 constexpr double kInvFact2 = 0.5;
 constexpr double kInvFact3 = 0x1.5555555555555p-3;  // 1.0 / 6.0
 constexpr double kInvFact4 = 0x1.5555555555555p-5;  // 1.0 / 24.0
+// 1/k! for the Paterson-Stockmeyer family, as the reference computes it: k!
+// accumulated in double (exact for k <= 18), one correctly rounded division
+// (taylor_schemes.cpp:44-48)
+__host__ __device__ constexpr double inv_fact(int k) {
+    double f = 1.0;
+    for (int i = 2; i <= k; ++i) f *= i;
+    return 1.0 / f;
+}
 
 // ---------------------------------------------------------------------------
 // Selection (reference expm.cpp:11-29): the cheapest table entry whose theta
@@ -111,26 +119,62 @@ __host__ __device__ __forceinline__ double dfrom(long long b) {
 
 // One implementation for the kernels and the host-side mexp_select, so the
 // CPU tests of mexp_select exercise the exact logic the kernels run.
-__host__ __device__ __forceinline__ Sel select_device(double norm, int accuracy) {
+// Family::TaylorPS (Paterson-Stockmeyer, theta_tables.cpp:53-59): degrees
+// {1, 2, 4, 6, 9, 16} at {0, 1, 2, 3, 4, 6} products.
+__host__ __device__ constexpr int ps_degree_of(int e) {
+    return e == 0 ? 1 : e == 1 ? 2 : e == 2 ? 4 : e == 3 ? 6 : e == 4 ? 9 : 16;
+}
+__host__ __device__ constexpr int ps_products_of_degree(int m) {
+    return m == 1 ? 0 : m == 2 ? 1 : m == 4 ? 2 : m == 6 ? 3 : m == 9 ? 4 : m == 16 ? 6 : -1;
+}
+__host__ __device__ constexpr int products_of(int family, int m) {
+    return family == MEXP_FAMILY_TAYLOR_PS ? ps_products_of_degree(m) : products_of_degree(m);
+}
+// theta_m of entry e of a family's table: the reference's decimal literals
+// (theta_tables.cpp:45-51 TaylorNew, :53-59 TaylorPS)
+__host__ __device__ __forceinline__ double theta_entry(int family, int accuracy, int e) {
+    if (family == MEXP_FAMILY_TAYLOR_PS) {
+        switch (e) {
+            case 0: return accuracy ? 2.22e-16 : 1.19e-7;
+            case 1: return accuracy ? 2.58e-8 : 5.98e-4;
+            case 2: return accuracy ? 3.40e-4 : 5.12e-2;
+            case 3: return accuracy ? 9.07e-3 : 2.50e-1;
+            case 4: return accuracy ? 8.96e-2 : 7.80e-1;
+            default: return accuracy ? 7.80e-1 : 2.48;
+        }
+    }
+    switch (e) {
+        case 0: return accuracy ? 2.22e-16 : 1.19e-7;
+        case 1: return accuracy ? 2.58e-8 : 5.98e-4;
+        case 2: return accuracy ? 3.40e-4 : 5.12e-2;
+        case 3: return accuracy ? 4.99e-2 : 5.80e-1;
+        case 4: return accuracy ? 2.99e-1 : 1.46;
+        default: return accuracy ? 1.09 : 3.01;
+    }
+}
+
+__host__ __device__ __forceinline__ Sel select_device(double norm, int accuracy,
+                                                      int family = MEXP_FAMILY_TAYLOR_NEW) {
     Sel r{0, 0, MEXP_OK};
     if (!isfinite(norm) || norm < 0.0) {
         r.status = MEXP_ERR_NORM_NONFINITE;
         return r;
     }
-    // the reference's decimal literals (theta_tables.cpp:45-51)
-    const double t0 = accuracy ? 2.22e-16 : 1.19e-7;
-    const double t1 = accuracy ? 2.58e-8 : 5.98e-4;
-    const double t2 = accuracy ? 3.40e-4 : 5.12e-2;
-    const double t3 = accuracy ? 4.99e-2 : 5.80e-1;
-    const double t4 = accuracy ? 2.99e-1 : 1.46;
-    const double tmax = accuracy ? 1.09 : 3.01;
+    const bool ps = family == MEXP_FAMILY_TAYLOR_PS;
+    const double t0 = theta_entry(family, accuracy, 0);
+    const double t1 = theta_entry(family, accuracy, 1);
+    const double t2 = theta_entry(family, accuracy, 2);
+    const double t3 = theta_entry(family, accuracy, 3);
+    const double t4 = theta_entry(family, accuracy, 4);
+    const double tmax = theta_entry(family, accuracy, 5);
     if (norm <= tmax) {
         // entries with theta < norm are skipped (expm.cpp:17); products and
-        // degrees ascend with the entry, so the reference's (products, degree)
-        // minimum is the first admissible entry = the count of skipped ones
+        // degrees ascend with the entry in both tables, so the reference's
+        // (products, degree) minimum is the first admissible entry = the count
+        // of skipped ones
         const int e = int(t0 < norm) + int(t1 < norm) + int(t2 < norm) + int(t3 < norm) +
                       int(t4 < norm);
-        r.degree = e < 4 ? (1 << e) : (e == 4 ? 12 : 18);
+        r.degree = ps ? ps_degree_of(e) : (e < 4 ? (1 << e) : (e == 4 ? 12 : 18));
         return r;
     }
     // least s with ldexp(norm, -s) <= theta_18 (expm.cpp:27). With norm =
@@ -142,7 +186,7 @@ __host__ __device__ __forceinline__ Sel select_device(double norm, int accuracy)
     const long long nb = dbits(norm), tb = dbits(tmax);
     const long long k = (nb >> 52) - (tb >> 52);
     const double t = dfrom(tb + (k << 52));
-    r.degree = 18;
+    r.degree = ps ? 16 : 18;
     r.s = int(k) + int(norm > t);
     return r;
 }

@@ -73,6 +73,8 @@ enum Epi : int {
     EPI_T4_1,     // c = A2; in = A         -> o0 = A2, o1 = (I/2 + A/6) + A2/24
     EPI_T4_2,     // c = inner*A2; in = A   -> o0 = (I + A) + c
     EPI_T2,       // c = A2; in = A         -> o0 = (I + A) + A2/2
+    EPI_PS_B,     // c = A^p; in = A, A2, A3 (or null) -> o0 = A^p,
+                  //   o_j = lc[j-1] . {I, A, A2, A3, A^p} for j = 1..nlc (Paterson-Stockmeyer)
 };
 
 struct GemmArgs {
@@ -80,6 +82,8 @@ struct GemmArgs {
     const double* Y;
     const double* in[3];
     double* out[5];
+    double lc[4][5];      // EPI_PS_B coefficients (runtime: one kernel for every degree)
+    int nlc;
     double* final_out;    // the caller's e^A buffer (list entries with bit 31 set)
     const int32_t* list;  // participating matrix indices (blockIdx.z); bit 31 set =
                           // this is the matrix's last product: out[0] -> final_out
@@ -157,6 +161,17 @@ __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, i
     } else if constexpr (EPI == EPI_T2) {
         const double2 a = ld(0);
         st(0, (id0 + a.x) + 0.5 * c0, (id1 + a.y) + 0.5 * c1);
+    } else if constexpr (EPI == EPI_PS_B) {
+        const double2 a = ld(0), a2 = ld(1);
+        const double2 a3 = g.in[2] ? ld(2) : make_double2(0.0, 0.0);
+        st(0, c0, c1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j >= g.nlc) break;
+            const double* k = g.lc[j];
+            st(1 + j, k[0] * id0 + k[1] * a.x + k[2] * a2.x + k[3] * a3.x + k[4] * c0,
+               k[0] * id1 + k[1] * a.y + k[2] * a2.y + k[3] * a3.y + k[4] * c1);
+        }
     }
 }
 
@@ -255,8 +270,9 @@ __global__ void norm_cols_kernel(const double* __restrict__ a, int n, int64_t ba
 }
 
 __global__ void select_kernel(const unsigned long long* __restrict__ maxbits,
-                              const int* __restrict__ bad, int64_t batch, int accuracy,
+                              const int* __restrict__ bad, int64_t batch, int acc_arg,
                               mexp_selection* __restrict__ sel) {
+    const int accuracy = acc_arg & 15, family = acc_arg >> 4;  // mexp_accuracy | mexp_family << 4
     const int64_t m = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (m >= batch) return;
     mexp_selection r;
@@ -267,7 +283,7 @@ __global__ void select_kernel(const unsigned long long* __restrict__ maxbits,
         r.status = MEXP_ERR_NONFINITE;
     } else {
         const double norm = __longlong_as_double(static_cast<long long>(maxbits[m]));
-        const Sel s = select_device(norm, accuracy);
+        const Sel s = select_device(norm, accuracy, family);
         r.norm_in = norm;
         r.degree = int16_t(s.degree);
         r.s = int16_t(s.s);
@@ -322,7 +338,8 @@ __global__ void nan_kernel(double* __restrict__ out, int n, const int32_t* __res
 template <int EPI>
 int gemm(const double* X, const double* Y, std::initializer_list<const double*> in,
          std::initializer_list<double*> out, const int32_t* d_list, int count, int np,
-         cudaStream_t st, std::atomic<uint64_t>* launches, double* final_out = nullptr) {
+         cudaStream_t st, std::atomic<uint64_t>* launches, double* final_out = nullptr,
+         const double (*lc)[5] = nullptr, int nlc = 0) {
     if (count == 0) return MEXP_OK;
     static bool attr = [] {
         cudaFuncSetAttribute(gemm_dmma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -338,6 +355,9 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
     k = 0;
     for (auto p : out) g.out[k++] = p;
     g.final_out = final_out;
+    for (int j = 0; j < nlc; ++j)
+        for (int t = 0; t < 5; ++t) g.lc[j][t] = lc[j][t];
+    g.nlc = nlc;
     g.list = d_list;
     g.np = np;
     g.mstride = int64_t(np) * np;
@@ -369,7 +389,7 @@ Workspace& workspace() {
 const char* large_last_error() { return g_err.c_str(); }
 
 int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user, int n,
-                   int64_t batch, int accuracy, cudaStream_t st, std::atomic<uint64_t>* launches) {
+                   int64_t batch, int acc_arg, cudaStream_t st, std::atomic<uint64_t>* launches) {
     const int np = (n + BM - 1) / BM * BM;
     const int64_t mat = int64_t(np) * np;
     constexpr int kBuffers = 6;
@@ -394,7 +414,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     if (!d_sel) LCUDA(cudaMallocAsync(&d_sel, sizeof(mexp_selection) * batch, st));
 
     norm_cols_kernel<<<dim3((n + 255) / 256, unsigned(batch)), 256, 0, st>>>(d_a, n, batch, maxbits, bad);
-    select_kernel<<<unsigned((batch + 255) / 256), 256, 0, st>>>(maxbits, bad, batch, accuracy, d_sel);
+    select_kernel<<<unsigned((batch + 255) / 256), 256, 0, st>>>(maxbits, bad, batch, acc_arg, d_sel);
     launches->fetch_add(2, std::memory_order_relaxed);
 
     // (m, s) per matrix to the host: the schedule depends on them
@@ -417,9 +437,9 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         return off;
     };
     std::vector<int32_t> all_ok;
-    for (int d : {1, 2, 4, 8, 12, 18}) all_ok.insert(all_ok.end(), by_deg[d].begin(), by_deg[d].end());
+    for (int d = 1; d <= 18; ++d) all_ok.insert(all_ok.end(), by_deg[d].begin(), by_deg[d].end());
     size_t off_deg[19] = {};
-    for (int d : {1, 2, 4, 8, 12, 18}) off_deg[d] = append(by_deg[d]);
+    for (int d = 1; d <= 18; ++d) off_deg[d] = append(by_deg[d]);
     // Schemes, then squarings. Each matrix's LAST product writes its e^A
     // straight into the caller's output when no padding is needed (np == n):
     // the matrices with s == 0 at the scheme's final GEMM, those with s == k
@@ -462,7 +482,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     std::vector<Part> deg_flag(19), sq_flag(max_s + 1);
     std::vector<std::pair<Part, Part>> deg_parts(19);
     deg_parts[1] = parts(by_deg[1], 0);
-    for (int d : {2, 4, 8, 12, 18}) deg_flag[d] = flagged(by_deg[d], 0);
+    for (int d = 2; d <= 18; ++d) deg_flag[d] = flagged(by_deg[d], 0);
     for (int k = 1; k <= max_s; ++k) {
         std::vector<int32_t> v;
         for (int32_t m : all_ok)
@@ -536,6 +556,52 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
             return r;
         // A8 = V1*V2 -> T (A2 read in place)
         if ((r = final_step(ET8_3{}, W[3], W[4], {W[0], W[1]}, 8))) return r;
+    }
+    // Family::TaylorPS degrees 6, 9, 16 (eval_ps, taylor_schemes.cpp:167-198):
+    // p = 3 (6, 9) or 4 (16) powers, then the Horner chain
+    // T = ((t A^p + g_{q-1}) A^p + ...) A^p + g_0, with the chunks
+    // g_i = sum_k A^k / (p i + k)! formed in the epilogue of the A^p product
+    // (t = g_{q} + A^{pq}/m! seeds the chain).
+    auto ps_chunk = [](int p, int i, double* row) {
+        for (int k = 0; k < 4; ++k) row[k] = k < p ? inv_fact(p * i + k) : 0.0;
+        row[4] = 0.0;
+    };
+    if (int c = int(by_deg[16].size())) {  // p = 4, q = 4
+        const int32_t* l = L(off_deg[16]);
+        double lc[4][5];
+        ps_chunk(4, 3, lc[0]);
+        lc[0][4] = inv_fact(16);               // t = g3 + A4/16!
+        for (int j = 1; j < 4; ++j) ps_chunk(4, 3 - j, lc[j]);  // g2, g1, g0
+        if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
+        if ((r = gemm<EPI_STORE>(W[1], W[0], {}, {W[2]}, l, c, np, st, launches))) return r;  // A3
+        // A4 = A2*A2 -> A4 W3, t W4, g2 W5, g1 W0, g0 W2 (A, A3 read in place)
+        if ((r = gemm<EPI_PS_B>(W[1], W[1], {W[0], W[1], W[2]}, {W[3], W[4], W[5], W[0], W[2]}, l,
+                                c, np, st, launches, nullptr, lc, 4)))
+            return r;
+        if ((r = gemm<EPI_ADD>(W[4], W[3], {W[5]}, {W[5]}, l, c, np, st, launches))) return r;
+        if ((r = gemm<EPI_ADD>(W[5], W[3], {W[0]}, {W[0]}, l, c, np, st, launches))) return r;
+        if ((r = final_step(EAdd{}, W[0], W[3], {W[2]}, 16))) return r;
+    }
+    for (int d : {9, 6}) {  // p = 3, q = 3 / 2
+        const int c = int(by_deg[d].size());
+        if (!c) continue;
+        const int32_t* l = L(off_deg[d]);
+        const int q = d / 3;
+        double lc[4][5];
+        ps_chunk(3, q - 1, lc[0]);
+        lc[0][4] = inv_fact(d);                // t = g_{q-1} + A3/d!
+        for (int j = 1; j < q; ++j) ps_chunk(3, q - 1 - j, lc[j]);
+        if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
+        // A3 = A2*A -> A3 W2, t W3, then g_{q-2}.. g_0 in W4 (, W5)
+        if ((r = gemm<EPI_PS_B>(W[1], W[0], {W[0], W[1], nullptr}, {W[2], W[3], W[4], W[5]}, l, c,
+                                np, st, launches, nullptr, lc, q)))
+            return r;
+        if (q == 3) {
+            if ((r = gemm<EPI_ADD>(W[3], W[2], {W[4]}, {W[4]}, l, c, np, st, launches))) return r;
+            if ((r = final_step(EAdd{}, W[4], W[2], {W[5]}, d))) return r;
+        } else {
+            if ((r = final_step(EAdd{}, W[3], W[2], {W[4]}, d))) return r;
+        }
     }
     if (int c = int(by_deg[4].size())) {  // eval_ps(4) (taylor_schemes.cpp:158-165)
         const int32_t* l = L(off_deg[4]);

@@ -182,10 +182,12 @@ constexpr int kN8Mpw = 4;            // matrices per warp per round
 // unscaled A for sq_first).
 // kExact: 0 = exact-rounded matrices inline; 1 = fast kernel that defers the
 // matrices needing reference rounding to a worklist (expm8_exact_kernel).
-template <bool kSplit, int kDefer, int kMinBlocks = 8>
+// kFamily (mexp_family) is a template parameter: the TaylorNew kernel carries
+// no Paterson-Stockmeyer code.
+template <bool kSplit, int kDefer, int kMinBlocks = 8, int kFamily = MEXP_FAMILY_TAYLOR_NEW>
 __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     expm8_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
-                     mexp_selection* __restrict__ sel, int64_t batch, int accuracy, int rounding_arg,
+                     mexp_selection* __restrict__ sel, int64_t batch, int acc_arg, int rounding_arg,
                      int exact_s_min, int32_t* __restrict__ worklist, int32_t* __restrict__ wcount,
                      unsigned long long* __restrict__ ticket) {
     using Group8 = Group8T<kSplit>;
@@ -193,6 +195,9 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
     // rounding policy in the low byte; AUTO's fast squaring tail above it
     const int rounding = rounding_arg & 0xff, fast_tail = rounding_arg >> 8;
+    // accuracy in the low 4 bits (mexp_accuracy); the family is kFamily
+    const int accuracy = acc_arg & 15;
+    constexpr int family = kFamily;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     Group8 g;
@@ -255,7 +260,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
         if (!allfin)
             sl.status = MEXP_ERR_NONFINITE;
         else
-            sl = select_device(norm, accuracy);
+            sl = select_device(norm, accuracy, family);
         if (sel && c8 == 0 && m0 + jm < batch) {
             mexp_selection rec;
             rec.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
@@ -289,12 +294,12 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
                         if (lane == 0) worklist[atomicAdd(wcount, 1)] = int32_t(m);
                         continue;
                     }
-                    X = run_expm<FastOps>(g, A, degree, s);
+                    X = run_expm<FastOps>(g, A, degree, s, 0, family);
                 } else {
                     if (exact)
-                        X = run_expm<ExactOps>(g, A, degree, s, fast_tail);
+                        X = run_expm<ExactOps>(g, A, degree, s, fast_tail, family);
                     else
-                        X = run_expm<FastOps>(g, A, degree, s);
+                        X = run_expm<FastOps>(g, A, degree, s, 0, family);
                 }
             }
             st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
@@ -308,13 +313,16 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
 // Reference-rounded 8x8 expm for the matrices listed in worklist[0, *wcount)
 // (or, with worklist == nullptr, for all of [0, batch)): one warp per matrix,
 // its own prologue (the selection records were written by the fast kernel).
+template <int kFamily = MEXP_FAMILY_TAYLOR_NEW>
 __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
     expm8_exact_kernel(const double* __restrict__ a, double* __restrict__ out,
-                       mexp_selection* __restrict__ sel, int64_t batch, int accuracy,
+                       mexp_selection* __restrict__ sel, int64_t batch, int acc_arg,
                        const int32_t* __restrict__ worklist, const int32_t* __restrict__ wcount) {
     using Group8 = Group8T<false>;
     using F = Group8::Frag;
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][1024];
+    const int accuracy = acc_arg & 15;
+    constexpr int family = kFamily;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     Group8 g;
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
         if (!allfin)
             sl.status = MEXP_ERR_NONFINITE;
         else
-            sl = select_device(norm, accuracy);
+            sl = select_device(norm, accuracy, family);
         if (!worklist && sel && lane == 0) {
             mexp_selection rec;
             rec.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
@@ -364,7 +372,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
             X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
         } else {
             g.fscale = ldexp(1.0, -sl.s);
-            X = run_expm<ExactOps>(g, A, sl.degree, sl.s);
+            X = run_expm<ExactOps>(g, A, sl.degree, sl.s, 0, family);
         }
         st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
     }

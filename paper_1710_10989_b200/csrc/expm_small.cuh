@@ -313,9 +313,57 @@ __device__ typename G::Frag eval_taylor_new(const G& g, int degree, const typena
     }
 }
 
+// Family::TaylorPS (reference eval_ps, taylor_schemes.cpp:143-198, and
+// eval_taylor_ps :229-232): Paterson-Stockmeyer degrees {1, 2, 4, 6, 9, 16}.
+template <class Ops, class G>
+__device__ typename G::Frag eval_taylor_ps(const G& g, int degree, const typename G::Frag& A) {
+    using F = typename G::Frag;
+    const F I = g.ident();
+    switch (degree) {
+        case 1:
+            return addm<Ops>(I, A);
+        case 2:
+        case 4:
+            return eval_taylor_new<Ops>(g, degree, A);  // the same eval_ps(2), eval_ps(4)
+        case 6: {
+            const F A2 = g.template sq_first<Ops>(A);
+            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F f0 = lc<Ops, true>(1.0, I, 1.0, A, inv_fact(2), A2);
+            const F f1 = lc<Ops, true>(inv_fact(3), I, inv_fact(4), A, inv_fact(5), A2);
+            const F inner = lc<Ops>(1.0, f1, inv_fact(6), A3);
+            return g.template mm_add<Ops>(inner, A3, false, f0);
+        }
+        case 9: {
+            const F A2 = g.template sq_first<Ops>(A);
+            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F f0 = lc<Ops, true>(inv_fact(0), I, inv_fact(1), A, inv_fact(2), A2);
+            const F f1 = lc<Ops, true>(inv_fact(3), I, inv_fact(4), A, inv_fact(5), A2);
+            const F f2 = lc<Ops, true>(inv_fact(6), I, inv_fact(7), A, inv_fact(8), A2);
+            F t = lc<Ops>(1.0, f2, inv_fact(9), A3);
+            t = g.template mm_add<Ops>(t, A3, false, f1);
+            return g.template mm_add<Ops>(t, A3, false, f0);
+        }
+        default: {  // 16
+            const F A2 = g.template sq_first<Ops>(A);
+            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F A4 = g.template mm<Ops>(A2, A2, true);
+            F gk[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                gk[i] = lc<Ops, true>(inv_fact(4 * i), I, inv_fact(4 * i + 1), A, inv_fact(4 * i + 2), A2,
+                                      inv_fact(4 * i + 3), A3);
+            F t = lc<Ops>(1.0, gk[3], inv_fact(16), A4);
+            t = g.template mm_add<Ops>(t, A4, false, gk[2]);
+            t = g.template mm_add<Ops>(t, A4, false, gk[1]);
+            return g.template mm_add<Ops>(t, A4, false, gk[0]);
+        }
+    }
+}
+
 template <class Ops, class G>
 __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename G::Frag& A0,
-                                                     int degree, int s, int fast_tail = 0) {
+                                                     int degree, int s, int fast_tail = 0,
+                                                     int family = MEXP_FAMILY_TAYLOR_NEW) {
     using F = typename G::Frag;
     F A = A0;
     if (s > 0) {  // scaled(a, 2^-s) (expm.cpp:47 -> kernels.cpp:39-42), exact
@@ -323,7 +371,8 @@ __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename 
 #pragma unroll
         for (int e = 0; e < G::K; ++e) A.v[e] = __dmul_rn(f, A.v[e]);
     }
-    F X = eval_taylor_new<Ops>(g, degree, A);
+    F X = family == MEXP_FAMILY_TAYLOR_PS ? eval_taylor_ps<Ops>(g, degree, A)
+                                          : eval_taylor_new<Ops>(g, degree, A);
     // squarings, expm.cpp:31-35. With reference rounding, the last
     // `fast_tail` of them may use FMA/DMMA rounding: a rounding difference
     // made at squaring i is amplified ~2^(s-i) by the squarings after it, so
@@ -336,14 +385,16 @@ __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename 
 }
 
 // One group of W warps per matrix; GPC groups per CTA; grid-stride over the batch.
-template <int N, int GPC>
+template <int N, int GPC, int kFamily = MEXP_FAMILY_TAYLOR_NEW>
 __global__ void __launch_bounds__(32 * TileShape<N>::W * GPC, TileShape<N>::MIN_BLOCKS)
     expm_small_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
-                          mexp_selection* __restrict__ sel, int64_t batch, int accuracy,
+                          mexp_selection* __restrict__ sel, int64_t batch, int acc_arg,
                           int rounding, int exact_s_min) {
     using G = Group<N>;
     using F = typename G::Frag;
     extern __shared__ __align__(16) double smem[];
+    const int accuracy = acc_arg & 15;  // mexp_accuracy (low nibble)
+    constexpr int family = kFamily;
     const int gid = threadIdx.x / G::THREADS;
     G g;
     double* base = smem + gid * G::SMEM_DOUBLES;
@@ -401,7 +452,7 @@ __global__ void __launch_bounds__(32 * TileShape<N>::W * GPC, TileShape<N>::MIN_
         if (!allfin) {
             sl.status = MEXP_ERR_NONFINITE;
         } else {
-            sl = select_device(norm, accuracy);
+            sl = select_device(norm, accuracy, family);
         }
         if (sel && g.tid == 0) {
             mexp_selection r;
@@ -419,9 +470,9 @@ __global__ void __launch_bounds__(32 * TileShape<N>::W * GPC, TileShape<N>::MIN_
             const bool exact = rounding == MEXP_ROUND_REFERENCE ||
                                (rounding == MEXP_ROUND_AUTO && sl.s >= exact_s_min);
             if (exact)
-                X = run_expm<ExactOps>(g, A, sl.degree, sl.s);
+                X = run_expm<ExactOps>(g, A, sl.degree, sl.s, 0, family);
             else
-                X = run_expm<FastOps>(g, A, sl.degree, sl.s);
+                X = run_expm<FastOps>(g, A, sl.degree, sl.s, 0, family);
         }
         g.store_global(out + m * NN, X);
     }

@@ -199,10 +199,12 @@ struct GroupF32 {
     }
 };
 
-template <int N, int GPC>
+template <int N, int GPC, int kFamily = MEXP_FAMILY_TAYLOR_NEW>
 __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
     expm_small_f32_kernel(const float* __restrict__ a, float* __restrict__ out,
-                          mexp_selection* __restrict__ sel, int64_t batch, int accuracy) {
+                          mexp_selection* __restrict__ sel, int64_t batch, int acc_arg) {
+    const int accuracy = acc_arg & 15;  // mexp_accuracy (low nibble)
+    constexpr int family = kFamily;
     using G = GroupF32<N>;
     using F = typename G::Frag;
     extern __shared__ __align__(16) float smemf[];
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
         if (!allfin)
             sl.status = MEXP_ERR_NONFINITE;
         else
-            sl = select_device(norm, accuracy);
+            sl = select_device(norm, accuracy, family);
         if (sel && g.tid == 0) {
             mexp_selection r;
             r.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
@@ -279,7 +281,8 @@ __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
                 for (int e = 0; e < G::K; ++e)
                     A.v[e] = make_float2(float(f * double(A.v[e].x)), float(f * double(A.v[e].y)));
             }
-            X = eval_taylor_new<F32Ops>(g, sl.degree, A);
+            X = family == MEXP_FAMILY_TAYLOR_PS ? eval_taylor_ps<F32Ops>(g, sl.degree, A)
+                                                : eval_taylor_new<F32Ops>(g, sl.degree, A);
             for (int i = 0; i < sl.s; ++i) X = g.template mm<F32Ops>(X, X, true);
         }
         g.store_global(out + m * NN, X);
@@ -297,11 +300,11 @@ int sm_count() {
     return v;
 }
 
-template <int N, int GPC>
+template <int N, int GPC, int kFamily>
 int launch_f32(const float* a, float* out, mexp_selection* sel, int64_t batch, int accuracy,
                cudaStream_t st, std::atomic<uint64_t>* launches) {
     using G = GroupF32<N>;
-    auto kern = expm_small_f32_kernel<N, GPC>;
+    auto kern = expm_small_f32_kernel<N, GPC, kFamily>;
     const size_t smem = size_t(G::SMEM_FLOATS) * GPC * sizeof(float);
     static int bps = [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -319,15 +322,27 @@ int launch_f32(const float* a, float* out, mexp_selection* sel, int64_t batch, i
 }
 }  // namespace
 
-int run_small_f32(const float* d_a, float* d_out, mexp_selection* d_sel, int np, int64_t batch,
-                  int accuracy, cudaStream_t st, std::atomic<uint64_t>* launches) {
+template <int kFamily>
+int run_small_f32_family(const float* d_a, float* d_out, mexp_selection* d_sel, int np,
+                         int64_t batch, int acc_arg, cudaStream_t st,
+                         std::atomic<uint64_t>* launches) {
     switch (np) {
-        case 8: return launch_f32<8, 8>(d_a, d_out, d_sel, batch, accuracy, st, launches);
-        case 16: return launch_f32<16, 4>(d_a, d_out, d_sel, batch, accuracy, st, launches);
-        case 32: return launch_f32<32, 2>(d_a, d_out, d_sel, batch, accuracy, st, launches);
-        case 64: return launch_f32<64, 1>(d_a, d_out, d_sel, batch, accuracy, st, launches);
+        case 8: return launch_f32<8, 8, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
+        case 16: return launch_f32<16, 4, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
+        case 32: return launch_f32<32, 2, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
+        case 64: return launch_f32<64, 1, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
     }
     return MEXP_ERR_UNSUPPORTED;
+}
+
+// acc_arg = mexp_accuracy | mexp_family << 4; one kernel instantiation per family
+int run_small_f32(const float* d_a, float* d_out, mexp_selection* d_sel, int np, int64_t batch,
+                  int acc_arg, cudaStream_t st, std::atomic<uint64_t>* launches) {
+    if ((acc_arg >> 4) == MEXP_FAMILY_TAYLOR_PS)
+        return run_small_f32_family<MEXP_FAMILY_TAYLOR_PS>(d_a, d_out, d_sel, np, batch, acc_arg,
+                                                           st, launches);
+    return run_small_f32_family<MEXP_FAMILY_TAYLOR_NEW>(d_a, d_out, d_sel, np, batch, acc_arg, st,
+                                                        launches);
 }
 
 }  // namespace mexp_b200

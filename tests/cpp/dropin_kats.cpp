@@ -82,6 +82,13 @@ static void host_only() {
     CHECK(tn.entries.size() == 6 && tn.theta_max() == 1.09 && tn.asymptotic().products == 5);
     CHECK(unit_roundoff(Accuracy::Single) == std::ldexp(1.0, -24));
     CHECK(throws<std::invalid_argument>([] { selection_table(Family::PadeDiagonal, Accuracy::Double); }));
+    // Family::TaylorPS (theta_tables.cpp:53-59)
+    const auto& ps = selection_table(Family::TaylorPS, Accuracy::Double);
+    CHECK(ps.entries.size() == 6 && ps.theta_max() == 7.80e-1 && ps.asymptotic().degree == 16 &&
+          ps.asymptotic().products == 6);
+    CHECK(select(0.5, ps).degree == 16 && select(0.05, ps).degree == 9 &&
+          select(0.005, ps).degree == 6 && select(3.0, ps).s == 2);
+    CHECK(selection_table(Family::TaylorPS, Accuracy::Single).theta_max() == 2.48);
     Family f;
     CHECK(parse_family("taylor", f) && f == Family::TaylorNew);
     CHECK(std::strcmp(family_name(Family::TaylorPS), "taylor-ps") == 0);
@@ -108,8 +115,14 @@ static void device_cases() {
     DenseMatrix bad(2);
     bad.at(0, 1) = std::numeric_limits<double>::infinity();
     CHECK(throws<std::invalid_argument>([&] { expm(bad, Accuracy::Double, Family::TaylorNew); }));
-    // other families are not on the B200 path
+    // Pade is not on the B200 path
     CHECK(throws<std::invalid_argument>([] { expm(DenseMatrix(2), Accuracy::Double, Family::PadeDiagonal); }));
+    // Paterson-Stockmeyer family: rotation by pi -> m = 16, s = 3, 6 + 3 products
+    const auto rps = expm(DenseMatrix::from_rows({{0, pi}, {-pi, 0}}), Accuracy::Double,
+                          Family::TaylorPS);
+    CHECK(rps.degree == 16 && rps.s == 3 && rps.cost_thirds == 27 && rps.family == Family::TaylorPS);
+    CHECK(norm1(DenseMatrix::from_rows({{rps.result.at(0, 0) + 1, rps.result.at(0, 1)},
+                                        {rps.result.at(1, 0), rps.result.at(1, 1) + 1}})) <= 1e-12);
     // expm(A) expm(-A) = I (test_expm.cpp:108-120)
     std::mt19937_64 rng(42);
     for (int rep = 0; rep < 34; ++rep) {

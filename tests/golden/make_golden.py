@@ -26,6 +26,9 @@ OUT = os.path.dirname(os.path.abspath(__file__))
 
 THETA = {1: [2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09],
          0: [1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01]}
+# Family::TaylorPS (theta_tables.cpp:53-59)
+THETA_PS = {1: [2.22e-16, 2.58e-8, 3.40e-4, 9.07e-3, 8.96e-2, 7.80e-1],
+            0: [1.19e-7, 5.98e-4, 5.12e-2, 2.50e-1, 7.80e-1, 2.48]}
 
 
 def select_cases():
@@ -66,8 +69,43 @@ def expm_cases():
     return cases
 
 
+def taylor_ps(ref):
+    """tests/golden/taylor_ps.npz: Family::TaylorPS selection at every theta
+    boundary and expm cases covering degrees {1, 2, 4, 6, 9, 16}, s up to 8."""
+    norms = [0.0, 1.0, 10.0, 0.5, 1e-300, 1e300, 3.0, 100.0]
+    for acc in (0, 1):
+        for t in THETA_PS[acc]:
+            norms += [t, np.nextafter(t, 0.0), np.nextafter(t, np.inf)]
+            for k in range(1, 12):
+                v = np.ldexp(t, k)
+                norms += [v, np.nextafter(v, 0.0), np.nextafter(v, np.inf)]
+    norms = np.array(sorted(set(norms)), np.float64)
+    arrays = {"norms": norms}
+    for acc in (0, 1):
+        sel = np.array([ref.select(float(v), acc, 1) for v in norms], np.int32)
+        arrays[f"status_acc{acc}"], arrays[f"degree_acc{acc}"], arrays[f"s_acc{acc}"] = sel.T
+    rng = np.random.default_rng(19)
+    case_norms = [1e-17, 1e-9, 1e-5, 3.40e-4, 5e-3, 9.07e-3, 0.05, 8.96e-2, 0.2, 0.78, 1.5,
+                  2.48, 6.0, 40.0, 150.0]
+    for n in (1, 2, 3, 8, 13, 16, 32, 64):
+        a = np.stack([random_with_norm(rng, n, v) for v in case_norms])
+        arrays[f"n{n}_a"] = a
+        for acc in (0, 1):
+            r = ref.expm_batch(a, accuracy=acc, family=1)
+            arrays[f"n{n}_acc{acc}_out"] = r.out
+            arrays[f"n{n}_acc{acc}_meta"] = np.stack(
+                [r.degree, r.s, r.cost_thirds, r.status], axis=1).astype(np.int64)
+            arrays[f"n{n}_acc{acc}_norm"] = r.norm_in
+    np.savez_compressed(os.path.join(OUT, "taylor_ps.npz"), **arrays)
+    print(f"wrote taylor_ps.npz: {len(norms)} select norms, {len(case_norms)} cases per n")
+
+
 def main():
     ref = Reference()
+    if "--only-ps" in sys.argv:
+        taylor_ps(ref)
+        return
+    taylor_ps(ref)
     # selection
     norms = select_cases()
     sel = {}

@@ -102,14 +102,51 @@ def test_select_kats():
             mx.select(bad, t)
 
 
-def test_other_families_are_refused(lib):
-    # only Family::TaylorNew is on the B200 path; no CPU fallback for the others
+def test_pade_family_is_refused(lib):
+    # Family::PadeDiagonal is not on the B200 path; no CPU fallback for it
     with pytest.raises(ValueError, match="unsupported"):
         mx.selection_table(mx.Family.PadeDiagonal, mx.Accuracy.Double)
     a = np.eye(3)
     out = np.empty_like(a)
-    st = lib.mexp_expm(a.ctypes.data, 3, 1, int(mx.Family.TaylorPS), out.ctypes.data, None)
+    st = lib.mexp_expm(a.ctypes.data, 3, 1, int(mx.Family.PadeDiagonal), out.ctypes.data, None)
     assert st == mx.ERR_UNSUPPORTED
+    d, s = C.c_int32(), C.c_int32()
+    assert lib.mexp_select(1.0, 1, int(mx.Family.PadeDiagonal), C.byref(d),
+                           C.byref(s)) == mx.ERR_UNSUPPORTED
+
+
+def test_ps_selection_table_and_select(golden):
+    """Family::TaylorPS table (theta_tables.cpp:53-59) and mexp_select (the
+    kernels' select_device) against the reference's selections."""
+    for acc, th in ((1, [2.22e-16, 2.58e-8, 3.40e-4, 9.07e-3, 8.96e-2, 7.80e-1]),
+                    (0, [1.19e-7, 5.98e-4, 5.12e-2, 2.50e-1, 7.80e-1, 2.48])):
+        t = mx.selection_table(mx.Family.TaylorPS, mx.Accuracy(acc))
+        assert [e.degree for e in t.entries] == [1, 2, 4, 6, 9, 16]
+        assert [e.products for e in t.entries] == [0, 1, 2, 3, 4, 6]
+        assert [e.theta for e in t.entries] == th
+    g = golden("taylor_ps.npz")
+    for acc in (0, 1):
+        table = mx.selection_table(mx.Family.TaylorPS, mx.Accuracy(acc))
+        for v, d, s, st in zip(g["norms"], g[f"degree_acc{acc}"], g[f"s_acc{acc}"],
+                               g[f"status_acc{acc}"]):
+            if st == 0:
+                assert mx.select(float(v), table) == (d, s), (v, acc)
+
+
+def test_ps_closed_form_scaling_exponent(oracle):
+    rng = np.random.default_rng(6)
+    for acc, tmax in ((0, 2.48), (1, 0.78)):
+        table = mx.selection_table(mx.Family.TaylorPS, mx.Accuracy(acc))
+        norms = [np.nextafter(tmax, np.inf), 1.7976931348623157e308, 1e-320, 0.0]
+        for k in range(0, 1030, 7):
+            v = np.ldexp(tmax, k)
+            if np.isfinite(v):
+                norms += [v, np.nextafter(v, 0.0), np.nextafter(v, np.inf)]
+        norms += list(10.0 ** rng.uniform(-20, 308, 5000))
+        for v in norms:
+            st, d, s = oracle.select(float(v), acc, 1)
+            assert st == 0
+            assert mx.select(float(v), table) == (d, s), (v, acc)
 
 
 def test_invalid_arguments(lib):

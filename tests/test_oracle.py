@@ -282,3 +282,62 @@ def test_leading_block_of_triangular_matrix(oracle):
     blk = oracle.expm_forced(a[:k, :k].copy(), int(r.degree[0]), int(r.s[0]))
     assert np.array_equal(blk.view(np.uint64), r.out[0][:k, :k].copy().view(np.uint64))
     assert np.all(np.tril(r.out[0], -1) == 0.0)
+
+
+# ---- Family::TaylorPS (Paterson-Stockmeyer; §8(f) next row) ---------------
+def test_ps_select_matches_golden(oracle, golden):
+    g = golden("taylor_ps.npz")
+    for acc in (0, 1):
+        for v, d, s, st in zip(g["norms"], g[f"degree_acc{acc}"], g[f"s_acc{acc}"],
+                               g[f"status_acc{acc}"]):
+            got = oracle.select(float(v), acc, 1)
+            assert got[0] == st
+            if st == 0:
+                assert got[1:] == (d, s), (v, acc)
+
+
+def test_ps_expm_matches_golden_bitwise(oracle, golden):
+    g = golden("taylor_ps.npz")
+    degrees = set()
+    for n in (1, 2, 3, 8, 13, 16, 32, 64):
+        a = g[f"n{n}_a"]
+        for acc in (0, 1):
+            r = oracle.expm_batch(a, accuracy=acc, family=1)
+            meta = g[f"n{n}_acc{acc}_meta"]
+            assert np.array_equal(r.degree, meta[:, 0]) and np.array_equal(r.s, meta[:, 1])
+            assert np.array_equal(r.cost_thirds, meta[:, 2])
+            assert np.array_equal(r.norm_in, g[f"n{n}_acc{acc}_norm"])
+            assert np.array_equal(r.out.view(np.uint64), g[f"n{n}_acc{acc}_out"].view(np.uint64)), (n, acc)
+            degrees |= set(int(d) for d in r.degree)
+    assert degrees == {1, 2, 4, 6, 9, 16}
+
+
+def test_ps_eval_matches_horner(oracle):
+    """eval_taylor_ps(m) is the degree-m Taylor polynomial (within rounding)."""
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, (6, 6))
+    a *= 0.3 / l1(a)
+    for m in (1, 2, 4, 6, 9, 16):
+        k, got = oracle.eval_taylor_ps(a, m)
+        want = np.eye(6)
+        term = np.eye(6)
+        for j in range(1, m + 1):
+            term = term @ a / j
+            want = want + term
+        assert k == {1: 0, 2: 1, 4: 2, 6: 3, 9: 4, 16: 6}[m]
+        assert np.abs(got - want).max() < 1e-15, m
+    assert oracle.eval_taylor_ps(a, 8)[0] == -1
+
+
+def test_ps_oracle_bitwise_equals_reference(oracle, reference):
+    rng = np.random.default_rng(11)
+    for n in (4, 8, 20):
+        norms = 10.0 ** rng.uniform(-17, 2.5, 64)
+        a = rng.standard_normal((64, n, n))
+        a *= (norms / np.abs(a).sum(axis=1).max(axis=1))[:, None, None]
+        for acc in (0, 1):
+            r1 = reference.expm_batch(a, accuracy=acc, family=1)
+            r2 = oracle.expm_batch(a, accuracy=acc, family=1)
+            assert np.array_equal(r1.out.view(np.uint64), r2.out.view(np.uint64)), (n, acc)
+            for f in ("degree", "s", "cost_thirds", "norm_in", "status"):
+                assert np.array_equal(getattr(r1, f), getattr(r2, f)), f
