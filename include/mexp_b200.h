@@ -1,7 +1,9 @@
 /*
  * mexp_b200 — C ABI of the B200 (sm_100a) scaling-and-squaring matrix
  * exponential built on the reduced-product Taylor schemes of arXiv 1710.10989
- * (Family::TaylorNew of the reference `mexp` library).
+ * (Family::TaylorNew of the reference `mexp` library), with the reference's
+ * two comparison families: Paterson-Stockmeyer Taylor (TaylorPS) and the
+ * diagonal Pade approximants (PadeDiagonal, n <= 64).
  *
  * The reference has no FFI layer: its operator boundary is the C++ API in
  * namespace mexp (proj/include/mexp/expm.hpp, theta_tables.hpp). Each entry
@@ -26,21 +28,25 @@
 extern "C" {
 #endif
 
-#define MEXP_B200_ABI_VERSION 1
+#define MEXP_B200_ABI_VERSION 2
 
 /* Status codes. The C++ drop-in maps 1-3 to std::invalid_argument with the
- * reference's messages (expm.cpp:13, expm.cpp:38, taylor_schemes.cpp:225). */
+ * reference's messages (expm.cpp:13, expm.cpp:38, taylor_schemes.cpp:225)
+ * and 7 to std::runtime_error (kernels.cpp:72). */
 typedef enum {
     MEXP_OK = 0,
     MEXP_ERR_NONFINITE = 1,       /* "non-finite matrix entry"           expm.cpp:38 */
     MEXP_ERR_NORM_NONFINITE = 2,  /* "norm must be finite and nonnegative" expm.cpp:13 */
     MEXP_ERR_INVALID_ARGUMENT = 3,/* bad n / batch / enum value, dimension errors */
-    MEXP_ERR_UNSUPPORTED = 4,     /* family other than TaylorNew, dtype/n combination */
+    MEXP_ERR_UNSUPPORTED = 4,     /* family/dtype/n/rounding combination not built */
     MEXP_ERR_CUDA = 5,            /* CUDA runtime error (see mexp_last_cuda_error) */
-    MEXP_ERR_NO_DEVICE = 6        /* no CUDA device: there is no CPU fallback */
+    MEXP_ERR_NO_DEVICE = 6,       /* no CUDA device: there is no CPU fallback */
+    MEXP_ERR_SINGULAR = 7         /* "singular denominator" (Pade solve)  kernels.cpp:72 */
 } mexp_status;
 
-/* theta_tables.hpp:8 (enum class Family). Only TaylorNew is implemented. */
+/* theta_tables.hpp:8 (enum class Family). TaylorNew and TaylorPS run for every
+ * n and dtype; PadeDiagonal (scaling and squaring with r_m, m = 2..26 even,
+ * and a batched pivoted LU solve) for n <= 64. */
 typedef enum { MEXP_FAMILY_TAYLOR_NEW = 0, MEXP_FAMILY_TAYLOR_PS = 1, MEXP_FAMILY_PADE = 2 } mexp_family;
 
 /* theta_tables.hpp:9 (enum class Accuracy): selects the theta table, i.e. the
@@ -107,7 +113,8 @@ int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
 /* Batched expm on DEVICE buffers, asynchronous on `stream`. d_a and d_out
  * hold `batch` n x n matrices of `dtype`; d_sel (may be NULL) receives one
  * mexp_selection per matrix. Per-matrix errors (non-finite input, overflowing
- * norm) are reported in d_sel[i].status with d_out[i] filled with NaN; the
+ * norm, singular Pade denominator) are reported in d_sel[i].status with
+ * d_out[i] filled with NaN; the
  * call itself returns MEXP_OK once the work is enqueued. d_a and d_out must
  * not overlap. n may be any value >= 1. */
 int mexp_expm_batched(const void* d_a, void* d_out, int dtype, int n, int64_t batch,

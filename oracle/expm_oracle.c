@@ -3,7 +3,8 @@
  *
  * Plain-C restatement of the reference's scaling-and-squaring expm for
  * Family::TaylorNew (arXiv 1710.10989, reduced-product Taylor schemes) and
- * Family::TaylorPS (Paterson-Stockmeyer Taylor, the paper's baseline), in the
+ * Family::TaylorPS (Paterson-Stockmeyer Taylor, the paper's baseline) and
+ * Family::PadeDiagonal (diagonal Pade r_m with a pivoted LU solve), in the
  * exact arithmetic order of the reference so results are bit-identical to it
  * when compiled with -ffp-contract=off (the reference's own flag,
  * proj/CMakeLists.txt:10-11). Pinned against the compiled reference
@@ -17,7 +18,7 @@
 #include <stdlib.h>
 #include <string.h>
 
-enum { ORC_OK = 0, ORC_NONFINITE = 1, ORC_NORM_NONFINITE = 2, ORC_INVALID = 3 };
+enum { ORC_OK = 0, ORC_NONFINITE = 1, ORC_NORM_NONFINITE = 2, ORC_INVALID = 3, ORC_SINGULAR = 7 };
 
 /* ---- theta tables: proj/src/theta_tables.cpp:45-51 (TaylorNew rows) ---- */
 static const int kDegrees[6] = {1, 2, 4, 8, 12, 18};
@@ -29,6 +30,13 @@ static const int kDegreesPS[6] = {1, 2, 4, 6, 9, 16};
 static const int kProductsPS[6] = {0, 1, 2, 3, 4, 6};
 static const double kThetaPSDouble[6] = {2.22e-16, 2.58e-8, 3.40e-4, 9.07e-3, 8.96e-2, 7.80e-1};
 static const double kThetaPSSingle[6] = {1.19e-7, 5.98e-4, 5.12e-2, 2.50e-1, 7.80e-1, 2.48};
+/* PadeDiagonal rows: theta_tables.cpp:61-73 */
+static const int kDegreesPade[13] = {2, 4, 6, 8, 10, 12, 14, 16, 18, 20, 22, 24, 26};
+static const int kProductsPade[13] = {0, 1, 2, 3, 3, 4, 4, 5, 5, 5, 6, 6, 6};
+static const double kThetaPadeDouble[13] = {3.65e-8, 5.32e-4, 1.50e-2, 8.54e-2, 2.54e-1, 5.41e-1,
+                                            9.50e-1, 1.47, 2.10, 2.81, 3.60, 4.46, 5.37};
+static const double kThetaPadeSingle[13] = {8.46e-4, 8.09e-2, 4.26e-1, 1.05, 1.88, 2.85, 3.93,
+                                            5.06, 6.25, 7.47, 8.71, 9.97, 11.2};
 
 /* ---- scheme coefficients: proj/src/taylor_schemes.cpp:12-27,44-48,62-85 ---- */
 typedef struct { double x1, x2, x3, x4, x5, x6, x7, y0, y1, y2; } t8c;
@@ -129,15 +137,17 @@ static void add(const double* a, const double* b, double* out, size_t len) {
 
 /* ---- selection: proj/src/expm.cpp:11-29; family 0 TaylorNew, 1 TaylorPS ---- */
 int oracle_select_family(double norm, int accuracy, int family, int32_t* degree, int32_t* s) {
-    const int ps = family == 1;
-    const double* th = ps ? (accuracy == 0 ? kThetaPSSingle : kThetaPSDouble)
+    const int ps = family == 1, pade = family == 2;
+    const int ne = pade ? 13 : 6;
+    const double* th = pade ? (accuracy == 0 ? kThetaPadeSingle : kThetaPadeDouble)
+                     : ps ? (accuracy == 0 ? kThetaPSSingle : kThetaPSDouble)
                           : (accuracy == 0 ? kThetaSingle : kThetaDouble);
-    const int* kDeg = ps ? kDegreesPS : kDegrees;
-    const int* kProd = ps ? kProductsPS : kProducts;
+    const int* kDeg = pade ? kDegreesPade : ps ? kDegreesPS : kDegrees;
+    const int* kProd = pade ? kProductsPade : ps ? kProductsPS : kProducts;
     if (!isfinite(norm) || norm < 0) return ORC_NORM_NONFINITE;
-    if (norm <= th[5]) {
+    if (norm <= th[ne - 1]) {
         int best = -1;
-        for (int e = 0; e < 6; ++e) {
+        for (int e = 0; e < ne; ++e) {
             if (th[e] < norm) continue; /* expm.cpp:17 */
             if (best < 0 || kProd[e] < kProd[best] ||
                 (kProd[e] == kProd[best] && kDeg[e] < kDeg[best]))
@@ -148,8 +158,8 @@ int oracle_select_family(double norm, int accuracy, int family, int32_t* degree,
         return ORC_OK;
     }
     int k = 0;
-    while (ldexp(norm, -k) > th[5]) ++k; /* expm.cpp:27 */
-    *degree = kDeg[5];
+    while (ldexp(norm, -k) > th[ne - 1]) ++k; /* expm.cpp:27 */
+    *degree = kDeg[ne - 1];
     *s = k;
     return ORC_OK;
 }
@@ -327,6 +337,184 @@ int oracle_eval_taylor_ps(const double* a, int n, int degree, double* out) {
     return products;
 }
 
+/* ---- Family::PadeDiagonal: proj/src/pade.cpp, kernels.cpp:55-112 ---- */
+
+/* pade_coeffs (pade.cpp:34-48): b_j = (2m-j)! m! / ((2m)! (m-j)! j!) as an
+ * exact __int128 ratio reduced by its gcd, then long double division rounded
+ * to double. */
+static __int128 fact128(int n) {
+    __int128 f = 1;
+    for (int k = 2; k <= n; ++k) f *= k;
+    return f;
+}
+static __int128 gcd128(__int128 a, __int128 b) {
+    while (b != 0) {
+        const __int128 t = a % b;
+        a = b;
+        b = t;
+    }
+    return a < 0 ? -a : a;
+}
+int oracle_pade_coeffs(int m, double* b) {
+    if (m < 1 || m > 13) return -1;
+    for (int j = 0; j <= m; ++j) {
+        __int128 num = fact128(2 * m - j) * fact128(m);
+        __int128 den = fact128(2 * m) * fact128(m - j) * fact128(j);
+        const __int128 g = gcd128(num, den);
+        num /= g;
+        den /= g;
+        b[j] = (double)((long double)num / (long double)den);
+    }
+    return m + 1;
+}
+
+/* lu_factor + lu_apply (kernels.cpp:55-112): partial pivoting with a strict
+ * '>' scan, multipliers l = row[k] / piv, row[j] -= l * prow[j]; solve each
+ * column of rhs gathered through perm. Returns 0, or -1 on a zero pivot. */
+static int lu_solve(const double* m, const double* rhs, double* x, int n) {
+    const size_t nn = (size_t)n * n;
+    double* lu = (double*)malloc(sizeof(double) * nn);
+    int* perm = (int*)malloc(sizeof(int) * n);
+    double* y = (double*)malloc(sizeof(double) * n);
+    memcpy(lu, m, sizeof(double) * nn);
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    int st = 0;
+    for (int k = 0; k < n && st == 0; ++k) {
+        int p = k;
+        double best = fabs(lu[(size_t)k * n + k]);
+        for (int i = k + 1; i < n; ++i) {
+            const double v = fabs(lu[(size_t)i * n + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        if (best == 0.0) { st = -1; break; }
+        if (p != k) {
+            for (int j = 0; j < n; ++j) {
+                const double t = lu[(size_t)k * n + j];
+                lu[(size_t)k * n + j] = lu[(size_t)p * n + j];
+                lu[(size_t)p * n + j] = t;
+            }
+            const int t = perm[k]; perm[k] = perm[p]; perm[p] = t;
+        }
+        const double piv = lu[(size_t)k * n + k];
+        for (int i = k + 1; i < n; ++i) {
+            double* row = lu + (size_t)i * n;
+            const double* prow = lu + (size_t)k * n;
+            const double l = row[k] / piv;
+            row[k] = l;
+            for (int j = k + 1; j < n; ++j) row[j] -= l * prow[j];
+        }
+    }
+    if (st == 0) {
+        for (int col = 0; col < n; ++col) {
+            for (int i = 0; i < n; ++i) y[i] = rhs[(size_t)perm[i] * n + col];
+            for (int i = 1; i < n; ++i) {
+                double s = y[i];
+                const double* row = lu + (size_t)i * n;
+                for (int j = 0; j < i; ++j) s -= row[j] * y[j];
+                y[i] = s;
+            }
+            for (int i = n - 1; i >= 0; --i) {
+                double s = y[i];
+                const double* row = lu + (size_t)i * n;
+                for (int j = i + 1; j < n; ++j) s -= row[j] * y[j];
+                y[i] = s / row[i];
+            }
+            for (int i = 0; i < n; ++i) x[(size_t)i * n + col] = y[i];
+        }
+    }
+    free(lu); free(perm); free(y);
+    return st;
+}
+
+/* pade_solve (pade.cpp:26-28): (V - U)^-1 (V + U). */
+static int pade_solve(const double* u, const double* v, double* out, int n) {
+    const size_t nn = (size_t)n * n;
+    double* p = (double*)malloc(sizeof(double) * nn);
+    double* q = (double*)malloc(sizeof(double) * nn);
+    { const double k[2] = {1.0, -1.0}; const double* mm[2] = {v, u}; lincomb(k, mm, 2, p, nn); }
+    add(v, u, q, nn);
+    const int st = lu_solve(p, q, out, n);
+    free(p); free(q);
+    return st;
+}
+
+/* eval_pade (pade.cpp:50-113). Returns the product count, -1 for an invalid
+ * order, -2 for a singular denominator. */
+int oracle_eval_pade(const double* a, int n, int order, double* out) {
+    if (order < 2 || order > 26 || order % 2 != 0) return -1;
+    const size_t nn = (size_t)n * n;
+    const int m = order / 2;
+    double b[14];
+    oracle_pade_coeffs(m, b);
+    double* ws = (double*)malloc(sizeof(double) * nn * 20);
+    double* id = ws; double* u = ws + nn; double* v = ws + 2 * nn; double* t = ws + 3 * nn;
+    double* t2 = ws + 4 * nn;
+    double* pw = ws + 5 * nn; /* pw + i*nn = A^(2(i+1)), i < 6 */
+    memset(id, 0, sizeof(double) * nn);
+    for (int i = 0; i < n; ++i) id[(size_t)i * n + i] = 1.0;
+    int products = 0;
+    if (order == 10) { /* eval_r10 */
+        double* a2 = pw; double* a4 = pw + nn;
+        oracle_matmul(a, a, a2, n);
+        oracle_matmul(a2, a2, a4, n);
+        { const double k[3] = {b[5], b[3], b[1]}; const double* mm[3] = {a4, a2, id};
+          lincomb(k, mm, 3, t, nn); }
+        oracle_matmul(a, t, u, n);
+        { const double k[3] = {b[4], b[2], b[0]}; const double* mm[3] = {a4, a2, id};
+          lincomb(k, mm, 3, v, nn); }
+        products = 3;
+    } else if (order == 26) { /* eval_r26 */
+        double* a2 = pw; double* a4 = pw + nn; double* a6 = pw + 2 * nn;
+        oracle_matmul(a, a, a2, n);
+        oracle_matmul(a2, a2, a4, n);
+        oracle_matmul(a2, a4, a6, n);
+        { const double k[3] = {b[13], b[11], b[9]}; const double* mm[3] = {a6, a4, a2};
+          lincomb(k, mm, 3, t, nn); }
+        oracle_matmul(a6, t, t2, n);
+        { const double k[5] = {1.0, b[7], b[5], b[3], b[1]}; const double* mm[5] = {t2, a6, a4, a2, id};
+          lincomb(k, mm, 5, t, nn); }
+        oracle_matmul(a, t, u, n);
+        { const double k[3] = {b[12], b[10], b[8]}; const double* mm[3] = {a6, a4, a2};
+          lincomb(k, mm, 3, t, nn); }
+        oracle_matmul(a6, t, t2, n);
+        { const double k[5] = {1.0, b[6], b[4], b[2], b[0]}; const double* mm[5] = {t2, a6, a4, a2, id};
+          lincomb(k, mm, 5, v, nn); }
+        products = 6;
+    } else { /* even-power chain */
+        const int top = m - (m % 2);
+        int np = 0;
+        if (top >= 2) {
+            oracle_matmul(a, a, pw, n);
+            np = 1;
+            products = 1;
+            for (int e = 4; e <= top; e += 2) {
+                oracle_matmul(pw, pw + (size_t)(np - 1) * nn, pw + (size_t)np * nn, n);
+                ++np;
+                ++products;
+            }
+        }
+        double codd[8], ceven[8];
+        const double* modd[8];
+        const double* meven[8];
+        int ko = 0, ke = 0;
+        codd[ko] = b[1]; modd[ko++] = id;
+        ceven[ke] = b[0]; meven[ke++] = id;
+        for (int j = 3; j <= m; j += 2) { codd[ko] = b[j]; modd[ko++] = pw + (size_t)((j - 1) / 2 - 1) * nn; }
+        for (int j = 2; j <= m; j += 2) { ceven[ke] = b[j]; meven[ke++] = pw + (size_t)(j / 2 - 1) * nn; }
+        if (m >= 3) {
+            lincomb(codd, modd, ko, t, nn);
+            oracle_matmul(a, t, u, n);
+            ++products;
+        } else {
+            for (size_t e = 0; e < nn; ++e) u[e] = b[1] * a[e]; /* scaled(a, b1) */
+        }
+        lincomb(ceven, meven, ke, v, nn);
+    }
+    const int st = pade_solve(u, v, out, n);
+    free(ws);
+    return st < 0 ? -2 : products;
+}
+
 /* expm driver (proj/src/expm.cpp:37-74): finite check, norm, select, exact
  * scaling by 2^-s, T_m, s squarings, report. */
 int oracle_expm_family(const double* a, int n, int accuracy, int family, double* out,
@@ -346,8 +534,14 @@ int oracle_expm_family(const double* a, int n, int accuracy, int family, double*
         const double f = ldexp(1.0, -k); /* scale: kernels.cpp:39-42 */
         for (size_t e = 0; e < nn; ++e) arg[e] = f * a[e];
     }
-    const int products = family == 1 ? oracle_eval_taylor_ps(arg, n, m, out)
+    const int products = family == 2 ? oracle_eval_pade(arg, n, m, out)
+                       : family == 1 ? oracle_eval_taylor_ps(arg, n, m, out)
                                      : oracle_eval_taylor_new(arg, n, m, out);
+    if (products == -2) { /* "singular denominator" (kernels.cpp:72) */
+        free(arg);
+        free(tmp);
+        return ORC_SINGULAR;
+    }
     for (int i = 0; i < k; ++i) { /* squarings: expm.cpp:31-35 */
         oracle_matmul(out, out, tmp, n);
         memcpy(out, tmp, sizeof(double) * nn);
@@ -356,7 +550,14 @@ int oracle_expm_family(const double* a, int n, int accuracy, int family, double*
     free(tmp);
     if (degree) *degree = m;
     if (s) *s = k;
-    if (cost_thirds) *cost_thirds = 3 * (int64_t)(products + k);
+    /* table products, + 4/3 for the Pade solve (expm.cpp:70-72) */
+    if (cost_thirds) {
+        int tp = products;
+        if (family == 2)
+            for (int e = 0; e < 13; ++e)
+                if (kDegreesPade[e] == m) tp = kProductsPade[e];
+        *cost_thirds = 3 * (int64_t)(tp + k) + (family == 2 ? 4 : 0);
+    }
     if (norm_in) *norm_in = norm;
     return ORC_OK;
 }

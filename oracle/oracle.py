@@ -81,6 +81,19 @@ class Reference:
         self._eval = L.fn("eval_taylor_new", _I, _P, _I, _I, _P)
         self._horner = L.fn("taylor_oracle", None, _P, _I, _I, _P)
         self._coef = L.fn("coefficients", None, _P, _P, _P, _P)
+        self._pade_b = L.fn("pade_coeffs", _I, _I, _P)
+        self._eval_pade = L.fn("eval_pade", _I, _P, _I, _I, _P)
+
+    def pade_coeffs(self, m: int) -> np.ndarray:
+        b = np.zeros(14)
+        k = self._pade_b(m, _ptr(b))
+        return b[:k]
+
+    def eval_pade(self, a, order):
+        a = np.ascontiguousarray(a, np.float64)
+        out = np.empty_like(a)
+        k = self._eval_pade(_ptr(a), a.shape[0], order, _ptr(out))
+        return k, out
 
     def expm_batch(self, a: np.ndarray, accuracy: int = 1, family: int = 0) -> ExpmResult:
         batch, n, _ = a.shape
@@ -142,11 +155,24 @@ class Oracle:
         self._batch = L.fn("expm_batch_family", _I, _P, _P, _I, _I64, _I, _I, _P, _P, _P, _P, _P)
         self._select = L.fn("select_family", _I, _D, _I, _I, _P, _P)
         self._eval_ps = L.fn("eval_taylor_ps", _I, _P, _I, _I, _P)
+        self._pade_b = L.fn("pade_coeffs", _I, _I, _P)
+        self._eval_pade = L.fn("eval_pade", _I, _P, _I, _I, _P)
         self._one_norm = L.fn("one_norm", _D, _P, _I)
         self._matmul = L.fn("matmul", None, _P, _P, _P, _I)
         self._eval = L.fn("eval_taylor_new", _I, _P, _I, _I, _P)
         self._coef = L.fn("coefficients", None, _P, _P, _P, _P)
         self._forced = L.fn("expm_forced", _I, _P, _I, _I, _I, _P)
+
+    def pade_coeffs(self, m: int) -> np.ndarray:
+        b = np.zeros(14)
+        k = self._pade_b(m, _ptr(b))
+        return b[:k]
+
+    def eval_pade(self, a, order):
+        a = np.ascontiguousarray(a, np.float64)
+        out = np.empty_like(a)
+        k = self._eval_pade(_ptr(a), a.shape[0], order, _ptr(out))
+        return k, out
 
     def expm_forced(self, a: np.ndarray, degree: int, s: int) -> np.ndarray:
         """T_degree(2^-s A)^(2^s) with the given (m, s) (oracle_expm_forced)."""

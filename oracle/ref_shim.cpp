@@ -18,6 +18,7 @@
 #include "mexp/dense_matrix.hpp"
 #include "mexp/expm.hpp"
 #include "mexp/kernels.hpp"
+#include "mexp/pade.hpp"
 #include "mexp/taylor_schemes.hpp"
 #include "mexp/theta_tables.hpp"
 
@@ -28,6 +29,7 @@ constexpr int kOk = 0;
 constexpr int kNonFinite = 1;
 constexpr int kNormNonFinite = 2;
 constexpr int kInvalid = 3;
+constexpr int kSingular = 7;
 
 mexp::Accuracy acc_of(int a) { return a == 0 ? mexp::Accuracy::Single : mexp::Accuracy::Double; }
 
@@ -67,6 +69,13 @@ int expm_one(const T* a, int n, int accuracy, int family, U* out, int32_t* degre
         if (std::strstr(e.what(), "non-finite")) return kNonFinite;
         if (std::strstr(e.what(), "norm")) return kNormNonFinite;
         return kInvalid;
+    } catch (const std::runtime_error&) {  // "singular denominator" (kernels.cpp:72)
+        for (std::size_t k = 0; k < nn; ++k) out[k] = U(NAN);
+        if (degree) *degree = 0;
+        if (s) *s = 0;
+        if (cost_thirds) *cost_thirds = 0;
+        if (norm_in) *norm_in = NAN;
+        return kSingular;
     }
 }
 
@@ -162,6 +171,33 @@ int ref_eval_taylor_new(const double* a, int n, int degree, double* out) {
 void ref_taylor_oracle(const double* a, int n, int degree, double* out) {
     const auto r = mexp::taylor_oracle(to_dense(a, n), degree);
     std::memcpy(out, r.data(), sizeof(double) * std::size_t(n) * n);
+}
+
+// pade_coeffs(m) (src/pade.cpp:34-48): b_0..b_m into b; returns m + 1, or -1.
+int ref_pade_coeffs(int m, double* b) {
+    try {
+        const auto c = mexp::pade_coeffs(m);
+        for (int j = 0; j <= m; ++j) b[j] = c.b[j];
+        return m + 1;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
+// eval_pade (src/pade.cpp:50-113) on one matrix: returns the product count
+// recorded in the CostContext, -1 on an invalid order, -2 on a singular
+// denominator.
+int ref_eval_pade(const double* a, int n, int order, double* out) {
+    try {
+        mexp::CostContext ctx;
+        const auto r = mexp::eval_pade(ctx, to_dense(a, n), order);
+        std::memcpy(out, r.data(), sizeof(double) * std::size_t(n) * n);
+        return int(ctx.products);
+    } catch (const std::invalid_argument&) {
+        return -1;
+    } catch (const std::runtime_error&) {
+        return -2;
+    }
 }
 
 // Scheme coefficients as the library holds them at run time:

@@ -28,7 +28,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libmexp_b200.so")
 
 # mexp_status (include/mexp_b200.h)
 OK, ERR_NONFINITE, ERR_NORM_NONFINITE, ERR_INVALID_ARGUMENT = 0, 1, 2, 3
-ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_DEVICE = 4, 5, 6
+ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_DEVICE, ERR_SINGULAR = 4, 5, 6, 7
 F64, F32 = 0, 1
 ROUND_AUTO, ROUND_REFERENCE, ROUND_FAST = 0, 1, 2
 

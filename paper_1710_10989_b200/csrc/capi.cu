@@ -69,26 +69,28 @@ int exact_s_min(int n) {
     return 3 + l;
 }
 
-template <class T>
-__global__ void pad_kernel(const T* __restrict__ src, T* __restrict__ dst, int n, int np,
+// zero-pad n -> np (and widen float -> double for the fp32 Pade path)
+template <class S, class D>
+__global__ void pad_kernel(const S* __restrict__ src, D* __restrict__ dst, int n, int np,
                            int64_t batch) {
     const int64_t total = batch * int64_t(np) * np;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t b = i / (int64_t(np) * np);
         const int r = int((i / np) % np), c = int(i % np);
-        dst[i] = (r < n && c < n) ? src[b * n * n + r * n + c] : T(0);
+        dst[i] = (r < n && c < n) ? D(src[b * n * n + r * n + c]) : D(0);
     }
 }
-template <class T>
-__global__ void unpad_kernel(const T* __restrict__ src, T* __restrict__ dst, int n, int np,
+// top-left n x n of each np x np block (and narrow double -> float, rounding once)
+template <class S, class D>
+__global__ void unpad_kernel(const S* __restrict__ src, D* __restrict__ dst, int n, int np,
                              int64_t batch) {
     const int64_t total = batch * int64_t(n) * n;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t b = i / (int64_t(n) * n);
         const int r = int((i / n) % n), c = int(i % n);
-        dst[i] = src[b * np * np + r * np + c];
+        dst[i] = D(src[b * np * np + r * np + c]);
     }
 }
 
@@ -235,6 +237,9 @@ int launch_small_family(const double* a, double* out, mexp_selection* sel, int64
     if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)
         return launch_small_f64<N, GPC, MEXP_FAMILY_TAYLOR_PS>(a, out, sel, batch, accuracy,
                                                                rounding, smin, st);
+    if ((accuracy >> 4) == MEXP_FAMILY_PADE)
+        return launch_small_f64<N, GPC, MEXP_FAMILY_PADE>(a, out, sel, batch, accuracy, rounding,
+                                                          smin, st);
     return launch_small_f64<N, GPC, MEXP_FAMILY_TAYLOR_NEW>(a, out, sel, batch, accuracy, rounding,
                                                             smin, st);
 }
@@ -242,6 +247,9 @@ int launch_small_family(const double* a, double* out, mexp_selection* sel, int64
 int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
                   int accuracy, int rounding, int smin, cudaStream_t st) {
     if (batch == 0) return MEXP_OK;
+    if ((accuracy >> 4) == MEXP_FAMILY_PADE)  // the generic engine (its LU solve)
+        return launch_small_f64<8, 8, MEXP_FAMILY_PADE>(a, out, sel, batch, accuracy, rounding,
+                                                       smin, st);
     if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)  // the default variant only
         return launch_n8_variant<false, 0, 8, MEXP_FAMILY_TAYLOR_PS>(a, out, sel, batch, accuracy,
                                                                      rounding, smin, st);
@@ -272,14 +280,38 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
     if (batch == 0) return MEXP_OK;
     if (n > 64) {
         // the large-n engine is tensor-core DMMA only: no reference-rounded
-        // GEMM, and no fp32 path beyond n = 64
-        if (dtype != MEXP_F64 || rounding == MEXP_ROUND_REFERENCE) return MEXP_ERR_UNSUPPORTED;
+        // GEMM, no fp32 path and no Pade solve beyond n = 64
+        if (dtype != MEXP_F64 || rounding == MEXP_ROUND_REFERENCE ||
+            (accuracy >> 4) == MEXP_FAMILY_PADE)
+            return MEXP_ERR_UNSUPPORTED;
         const int r = large_expm_f64(static_cast<const double*>(d_a), static_cast<double*>(d_out),
                                      d_sel, n, batch, accuracy, st, &g_launches);
         if (r == MEXP_ERR_CUDA) g_last_cuda_error = large_last_error();
         return r;
     }
     const int np = padded_n(n);
+    if (dtype == MEXP_F32 && (accuracy >> 4) == MEXP_FAMILY_PADE) {
+        // fp32 storage, fp64 evaluation: the LU solve of a Pade denominator
+        // amplifies fp32 rounding by cond(V - U), which reaches ~1e3 at the
+        // Single table's thetas (up to 11.2), so the fp32 Pade path widens to
+        // the fp64 engine -- the reference's own arithmetic -- and rounds
+        // e^A once to float
+        const size_t bytes = size_t(batch) * np * np * sizeof(double);
+        double *win = nullptr, *wout = nullptr;
+        MEXP_CUDA(cudaMallocAsync(&win, bytes, st));
+        MEXP_CUDA(cudaMallocAsync(&wout, bytes, st));
+        const int grid = 4 * num_sms();
+        pad_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(d_a), win, n, np, batch);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        const int r = run_small_f64(win, wout, d_sel, np, batch, accuracy, rounding, exact_s_min(n), st);
+        if (r != MEXP_OK) return r;
+        unpad_kernel<<<grid, 256, 0, st>>>(wout, static_cast<float*>(d_out), n, np, batch);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        MEXP_CUDA(cudaFreeAsync(win, st));
+        MEXP_CUDA(cudaFreeAsync(wout, st));
+        MEXP_CUDA(cudaGetLastError());
+        return MEXP_OK;
+    }
     const size_t esz = dtype == MEXP_F64 ? sizeof(double) : sizeof(float);
     const void* src = d_a;
     void* dst = d_out;
@@ -393,9 +425,10 @@ const char* mexp_status_string(int status) {
         case MEXP_ERR_NONFINITE: return "non-finite matrix entry";
         case MEXP_ERR_NORM_NONFINITE: return "norm must be finite and nonnegative";
         case MEXP_ERR_INVALID_ARGUMENT: return "invalid argument";
-        case MEXP_ERR_UNSUPPORTED: return "unsupported on the B200 TaylorNew path";
+        case MEXP_ERR_UNSUPPORTED: return "unsupported on the B200 path";
         case MEXP_ERR_CUDA: return "CUDA error";
         case MEXP_ERR_NO_DEVICE: return "no usable CUDA device (there is no CPU fallback)";
+        case MEXP_ERR_SINGULAR: return "singular denominator";
     }
     return "unknown status";
 }
@@ -412,12 +445,10 @@ int mexp_selection_table(int accuracy, int family, int32_t* degrees, int32_t* pr
                          double* thetas, int cap) {
     if (accuracy != MEXP_ACCURACY_SINGLE && accuracy != MEXP_ACCURACY_DOUBLE)
         return -MEXP_ERR_INVALID_ARGUMENT;
-    if (family != MEXP_FAMILY_TAYLOR_NEW && family != MEXP_FAMILY_TAYLOR_PS)
-        return -MEXP_ERR_UNSUPPORTED;
-    const bool ps = family == MEXP_FAMILY_TAYLOR_PS;
+    if (family < MEXP_FAMILY_TAYLOR_NEW || family > MEXP_FAMILY_PADE) return -MEXP_ERR_INVALID_ARGUMENT;
     int k = 0;
-    for (int e = 0; e < kNumEntries && k < cap; ++e, ++k) {
-        degrees[k] = ps ? ps_degree_of(e) : degree_of(e);
+    for (int e = 0; e < num_entries(family) && k < cap; ++e, ++k) {
+        degrees[k] = degree_of_entry(family, e);
         products[k] = products_of(family, degrees[k]);
         thetas[k] = theta_entry(family, accuracy, e);
     }
@@ -429,8 +460,7 @@ int mexp_selection_table(int accuracy, int family, int32_t* degrees, int32_t* pr
 int mexp_select(double norm, int accuracy, int family, int32_t* degree, int32_t* s) {
     if (accuracy != MEXP_ACCURACY_SINGLE && accuracy != MEXP_ACCURACY_DOUBLE)
         return MEXP_ERR_INVALID_ARGUMENT;
-    if (family != MEXP_FAMILY_TAYLOR_NEW && family != MEXP_FAMILY_TAYLOR_PS)
-        return MEXP_ERR_UNSUPPORTED;
+    if (family < MEXP_FAMILY_TAYLOR_NEW || family > MEXP_FAMILY_PADE) return MEXP_ERR_INVALID_ARGUMENT;
     const Sel r = select_device(norm, accuracy, family);
     if (r.status != MEXP_OK) return r.status;
     *degree = r.degree;
@@ -442,7 +472,6 @@ int mexp_expm_batched(const void* d_a, void* d_out, int dtype, int n, int64_t ba
                       int accuracy, int family, int rounding, mexp_selection* d_sel,
                       void* stream) {
     if (!valid_args(dtype, n, batch, accuracy, family, rounding)) return MEXP_ERR_INVALID_ARGUMENT;
-    if (family == MEXP_FAMILY_PADE) return MEXP_ERR_UNSUPPORTED;
     if (batch > 0 && (!d_a || !d_out)) return MEXP_ERR_INVALID_ARGUMENT;
     const int dv = device_ok();
     if (dv != MEXP_OK) return dv;
@@ -454,7 +483,6 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
                            int accuracy, int family, int rounding, mexp_selection* h_sel,
                            int64_t* first_error) {
     if (!valid_args(dtype, n, batch, accuracy, family, rounding)) return MEXP_ERR_INVALID_ARGUMENT;
-    if (family == MEXP_FAMILY_PADE) return MEXP_ERR_UNSUPPORTED;
     if (first_error) *first_error = -1;
     if (batch == 0) return MEXP_OK;
     if (!h_a || !h_out) return MEXP_ERR_INVALID_ARGUMENT;
@@ -590,7 +618,7 @@ int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
         report->degree = sel.degree;
         report->s = sel.s;
         report->reserved = 0;
-        report->cost_thirds = 3 * int64_t(products_of(family, sel.degree) + sel.s);
+        report->cost_thirds = cost_thirds_of(family, sel.degree, sel.s);
         report->norm_in = sel.norm_in;
     }
     return MEXP_OK;

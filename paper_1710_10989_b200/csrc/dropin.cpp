@@ -39,8 +39,6 @@ int checked_dim(int n) {
 }
 
 SelectionTable load_table(Family f, Accuracy u) {
-    if (f == Family::PadeDiagonal)
-        throw std::invalid_argument("the pade family does not run on the B200 path");
     int32_t d[16], p[16];
     double t[16];
     const int k = mexp_selection_table(int(u), int(f), d, p, t, 16);
@@ -144,8 +142,9 @@ const SelectionTable& selection_table(Family f, Accuracy u) {
     static const SelectionTable dbl = load_table(Family::TaylorNew, Accuracy::Double);
     static const SelectionTable ps_single = load_table(Family::TaylorPS, Accuracy::Single);
     static const SelectionTable ps_dbl = load_table(Family::TaylorPS, Accuracy::Double);
-    if (f == Family::PadeDiagonal)
-        throw std::invalid_argument("the pade family does not run on the B200 path");
+    static const SelectionTable pade_single = load_table(Family::PadeDiagonal, Accuracy::Single);
+    static const SelectionTable pade_dbl = load_table(Family::PadeDiagonal, Accuracy::Double);
+    if (f == Family::PadeDiagonal) return u == Accuracy::Single ? pade_single : pade_dbl;
     if (f == Family::TaylorPS) return u == Accuracy::Single ? ps_single : ps_dbl;
     return u == Accuracy::Single ? single : dbl;
 }

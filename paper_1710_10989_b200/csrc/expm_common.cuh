@@ -127,12 +127,67 @@ __host__ __device__ constexpr int ps_degree_of(int e) {
 __host__ __device__ constexpr int ps_products_of_degree(int m) {
     return m == 1 ? 0 : m == 2 ? 1 : m == 4 ? 2 : m == 6 ? 3 : m == 9 ? 4 : m == 16 ? 6 : -1;
 }
-__host__ __device__ constexpr int products_of(int family, int m) {
-    return family == MEXP_FAMILY_TAYLOR_PS ? ps_products_of_degree(m) : products_of_degree(m);
+// Family::PadeDiagonal (theta_tables.cpp:61-73): orders 2, 4, ..., 26 at
+// {0, 1, 2, 3, 3, 4, 4, 5, 5, 5, 6, 6, 6} products (+ one LU solve).
+constexpr int kPadeEntries = 13;
+__host__ __device__ constexpr int pade_products_of_degree(int m) {
+    return m == 2 ? 0 : m == 4 ? 1 : m == 6 ? 2 : (m == 8 || m == 10) ? 3 : (m == 12 || m == 14) ? 4
+         : (m == 16 || m == 18 || m == 20) ? 5 : (m == 22 || m == 24 || m == 26) ? 6 : -1;
 }
+__host__ __device__ constexpr int num_entries(int family) {
+    return family == MEXP_FAMILY_PADE ? kPadeEntries : kNumEntries;
+}
+__host__ __device__ constexpr int degree_of_entry(int family, int e) {
+    return family == MEXP_FAMILY_PADE ? 2 * (e + 1)
+         : family == MEXP_FAMILY_TAYLOR_PS ? ps_degree_of(e) : degree_of(e);
+}
+__host__ __device__ constexpr int products_of(int family, int m) {
+    return family == MEXP_FAMILY_TAYLOR_PS ? ps_products_of_degree(m)
+         : family == MEXP_FAMILY_PADE ? pade_products_of_degree(m) : products_of_degree(m);
+}
+// the reported cost: products + s, plus 4/3 for the Pade solve (expm.cpp:70-72)
+__host__ __device__ constexpr int cost_thirds_of(int family, int m, int s) {
+    return 3 * (products_of(family, m) + s) + (family == MEXP_FAMILY_PADE ? 4 : 0);
+}
+__host__ __device__ __forceinline__ double pade_theta(int accuracy, int e) {
+    switch (e) {
+        case 0: return accuracy ? 3.65e-8 : 8.46e-4;
+        case 1: return accuracy ? 5.32e-4 : 8.09e-2;
+        case 2: return accuracy ? 1.50e-2 : 4.26e-1;
+        case 3: return accuracy ? 8.54e-2 : 1.05;
+        case 4: return accuracy ? 2.54e-1 : 1.88;
+        case 5: return accuracy ? 5.41e-1 : 2.85;
+        case 6: return accuracy ? 9.50e-1 : 3.93;
+        case 7: return accuracy ? 1.47 : 5.06;
+        case 8: return accuracy ? 2.10 : 6.25;
+        case 9: return accuracy ? 2.81 : 7.47;
+        case 10: return accuracy ? 3.60 : 8.71;
+        case 11: return accuracy ? 4.46 : 9.97;
+        default: return accuracy ? 5.37 : 11.2;
+    }
+}
+// pade_coeffs(m).b (pade.cpp:34-48: exact integer ratios, rounded once via
+// long double) as the compiled reference holds them, b_0..b_m for m = 1..13;
+// checked bit for bit by tests/test_oracle.py::test_pade_coefficients.
+__device__ constexpr double c_pade[13][14] = {
+    {1.0, 0x1.0000000000000p-1, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.5555555555555p-4, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.999999999999ap-4, 0x1.1111111111111p-7, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.b6db6db6db6dbp-4, 0x1.8618618618618p-7, 0x1.3813813813814p-11, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.c71c71c71c71cp-4, 0x1.c71c71c71c71cp-7, 0x1.0410410410410p-10, 0x1.1566abc011567p-15, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.d1745d1745d17p-4, 0x1.f07c1f07c1f08p-7, 0x1.4afd6a052bf5bp-10, 0x1.08cabb37565e2p-14, 0x1.937e11175f095p-20, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.d89d89d89d89ep-4, 0x1.0690690690690p-6, 0x1.7de952f2466a4p-10, 0x1.6ea28d118b474p-14, 0x1.b287c3a303e2bp-19, 0x1.f09b28ba4d955p-25, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.ddddddddddddep-4, 0x1.1111111111111p-6, 0x1.a41a41a41a41ap-10, 0x1.c01c01c01c01cp-14, 0x1.45e5d2ba42ea0p-18, 0x1.29f6b20961c00p-23, 0x1.08db48ebe51c7p-29, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.e1e1e1e1e1e1ep-4, 0x1.1919191919192p-6, 0x1.c1c1c1c1c1c1cp-10, 0x1.0101010101010p-13, 0x1.a5c001a5c001ap-18, 0x1.e20001e20001ep-23, 0x1.5e8ba44745d2dp-28, 0x1.f28db670be53bp-35, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.e50d79435e50dp-4, 0x1.1f7047dc11f70p-6, 0x1.d96da388960f5p-10, 0x1.1c0e9551f3a2dp-13, 0x1.f8fd7b3c5bcc1p-18, 0x1.49ca1c3c50d8ep-22, 0x1.306bcb4b5e520p-27, 0x1.68cb9b9bb2285p-33, 0x1.a3d5a71b92cd3p-40, 0.0, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.e79e79e79e79ep-4, 0x1.2492492492492p-6, 0x1.ecc07b301ecc0p-10, 0x1.3299e6401329ap-13, 0x1.2090d8b4c6bdcp-17, 0x1.9c3ca34b650f1p-22, 0x1.b7b825a5c1212p-27, 0x1.4f06351093257p-32, 0x1.49deba27f3581p-38, 0x1.3fdfbc45c52eap-45, 0.0, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.e9bd37a6f4deap-4, 0x1.28cfc4a33f129p-6, 0x1.fcd1e360fe68fp-10, 0x1.45a50c670938fp-13, 0x1.3fee80f4f29acp-17, 0x1.e783d0b234bb0p-22, 0x1.1ec6024ab59b3p-26, 0x1.fdd1cb2f7bbe9p-32, 0x1.4648d3f56deaap-37, 0x1.0f328eed3d6fep-43, 0x1.bd0ac3296b624p-51, 0.0},
+    {1.0, 0x1.0000000000000p-1, 0x1.eb851eb851eb8p-4, 0x1.2c5f92c5f92c6p-6, 0x1.0531b747fa105p-9, 0x1.55ed4d05c9af0p-13, 0x1.5b5ab7e55f2bap-17, 0x1.15e22cb77f562p-21, 0x1.5f02bf38a0d89p-26, 0x1.5aad6134c4c94p-31, 0x1.05070ff78b221p-36, 0x1.1cc1e2df80824p-42, 0x1.94fcfe65b1145p-49, 0x1.1cd3b01a822a6p-56},
+};
 // theta_m of entry e of a family's table: the reference's decimal literals
 // (theta_tables.cpp:45-51 TaylorNew, :53-59 TaylorPS)
 __host__ __device__ __forceinline__ double theta_entry(int family, int accuracy, int e) {
+    if (family == MEXP_FAMILY_PADE) return pade_theta(accuracy, e);
     if (family == MEXP_FAMILY_TAYLOR_PS) {
         switch (e) {
             case 0: return accuracy ? 2.22e-16 : 1.19e-7;
@@ -158,6 +213,24 @@ __host__ __device__ __forceinline__ Sel select_device(double norm, int accuracy,
     Sel r{0, 0, MEXP_OK};
     if (!isfinite(norm) || norm < 0.0) {
         r.status = MEXP_ERR_NORM_NONFINITE;
+        return r;
+    }
+    if (family == MEXP_FAMILY_PADE) {
+        // products are non-decreasing along the Pade table too (orders 8/10,
+        // 12/14, ... tie), so the cheapest admissible entry with ties to the
+        // lower degree is again the first admissible one
+        const double tmax = pade_theta(accuracy, kPadeEntries - 1);
+        if (norm <= tmax) {
+            int e = 0;
+#pragma unroll
+            for (int k = 0; k < kPadeEntries - 1; ++k) e += int(pade_theta(accuracy, k) < norm);
+            r.degree = 2 * (e + 1);
+            return r;
+        }
+        const long long nb = dbits(norm), tb = dbits(tmax);
+        const long long k = (nb >> 52) - (tb >> 52);
+        r.degree = 26;
+        r.s = int(k) + int(norm > dfrom(tb + (k << 52)));
         return r;
     }
     const bool ps = family == MEXP_FAMILY_TAYLOR_PS;

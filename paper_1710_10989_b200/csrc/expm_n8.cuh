@@ -294,12 +294,12 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
                         if (lane == 0) worklist[atomicAdd(wcount, 1)] = int32_t(m);
                         continue;
                     }
-                    X = run_expm<FastOps>(g, A, degree, s, 0, family);
+                    X = run_expm<FastOps, family>(g, A, degree, s, 0);
                 } else {
                     if (exact)
-                        X = run_expm<ExactOps>(g, A, degree, s, fast_tail, family);
+                        X = run_expm<ExactOps, family>(g, A, degree, s, fast_tail);
                     else
-                        X = run_expm<FastOps>(g, A, degree, s, 0, family);
+                        X = run_expm<FastOps, family>(g, A, degree, s, 0);
                 }
             }
             st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
             X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
         } else {
             g.fscale = ldexp(1.0, -sl.s);
-            X = run_expm<ExactOps>(g, A, sl.degree, sl.s, 0, family);
+            X = run_expm<ExactOps, family>(g, A, sl.degree, sl.s, 0);
         }
         st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
     }

@@ -38,6 +38,7 @@ struct Group {
     static constexpr int BLK_R = N / 8 / TR; // warp blocks per tile-row direction
     static_assert((N / 8) * (N / 8) == W * T, "tile cover");
     static constexpr int THREADS = 32 * W;
+    static constexpr int NDIM = N;
     // shared memory per group, in doubles: two operand buffers + stash + scalars
     static constexpr int STASH_SLOT = K * THREADS;
     static constexpr int SMEM_DOUBLES = 2 * N * LD + S::STASH * STASH_SLOT + 2 * W + 2;
@@ -103,6 +104,31 @@ struct Group {
         for (int t = 0; t < T; ++t)
             *reinterpret_cast<double2*>(s + row_of(t) * LD + col_of(t)) =
                 make_double2(f.v[2 * t], f.v[2 * t + 1]);
+    }
+    __device__ __forceinline__ Frag load_smem(const double* s) const {
+        Frag f;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const double2 v = *reinterpret_cast<const double2*>(s + row_of(t) * LD + col_of(t));
+            f.v[2 * t] = v.x;
+            f.v[2 * t + 1] = v.y;
+        }
+        return f;
+    }
+    // Pade solve staging (pade_solve, pade.cpp:26-28): M = V - U -> sx,
+    // R = V + U -> sy (row-major, stride LD)
+    __device__ __forceinline__ double* lu_m() const { return sx; }
+    __device__ __forceinline__ double* lu_r() const { return sy; }
+    __device__ __forceinline__ int* lu_flag() const { return reinterpret_cast<int*>(scal + 2 * W); }
+    __device__ __forceinline__ void stage_solve(const Frag& M, const Frag& R) const {
+        sync();
+        store_smem(sx, M);
+        store_smem(sy, R);
+        sync();
+    }
+    __device__ __forceinline__ Frag solved() const {
+        sync();
+        return load_smem(sy);
     }
 
     // Stash a fragment in a thread-private slot (conflict-free, same layout back).
@@ -360,10 +386,167 @@ __device__ typename G::Frag eval_taylor_ps(const G& g, int degree, const typenam
     }
 }
 
+// ---- Family::PadeDiagonal (reference pade.cpp) -----------------------------
+// r_order(A) = (V - U)^-1 (V + U) with U odd and V even in A.
+template <class Ops, class F>
+__device__ __forceinline__ void acc_term(F& r, double c, const F& m) {
+#pragma unroll
+    for (int e = 0; e < F::kCount; ++e)
+        if (Ops::kExact || c != 0.0) r.v[e] = Ops::mac(r.v[e], c, m.v[e]);
+}
+
+// U and V of eval_pade (pade.cpp:50-113), in the reference's product and
+// lincomb order: eval_r10, eval_r26, or the generic even-power chain.
 template <class Ops, class G>
+__device__ void eval_pade(const G& g, int order, const typename G::Frag& A, typename G::Frag& U,
+                          typename G::Frag& V) {
+    using F = typename G::Frag;
+    const F I = g.ident();
+    if (order == 10) {  // eval_r10 (pade.cpp:50-58), 3 products
+        const double* b = c_pade[4];
+        const F A2 = g.template sq_first<Ops>(A);
+        const F A4 = g.template mm<Ops>(A2, A2, true);
+        U = g.template mm<Ops>(A, lc<Ops>(b[5], A4, b[3], A2, b[1], I), false);
+        V = lc<Ops>(b[4], A4, b[2], A2, b[0], I);
+        return;
+    }
+    if (order == 26) {  // eval_r26 (pade.cpp:60-74), 6 products
+        const double* b = c_pade[12];
+        const F A2 = g.template sq_first<Ops>(A);
+        const F A4 = g.template mm<Ops>(A2, A2, true);
+        const F A6 = g.template mm<Ops>(A2, A4, false);
+        F u = g.template mm<Ops>(A6, lc<Ops>(b[13], A6, b[11], A4, b[9], A2), false);
+        u = lc<Ops>(1.0, u, b[7], A6, b[5], A4, b[3], A2, b[1], I);
+        U = g.template mm<Ops>(A, u, false);
+        const F v = g.template mm<Ops>(A6, lc<Ops>(b[12], A6, b[10], A4, b[8], A2), false);
+        V = lc<Ops>(1.0, v, b[6], A6, b[4], A4, b[2], A2, b[0], I);
+        return;
+    }
+    // any other even order (pade.cpp:82-110): A2, A4 = A2*A2, A6 = A2*A4, ...
+    // up to the largest even power <= m; the odd and even lincombs take the
+    // powers in ascending order, so they accumulate as the chain grows
+    const int m = order / 2;
+    const double* b = c_pade[m - 1];
+    const int top = m - (m % 2);
+    F odd = lc<Ops, true>(b[1], I);
+    V = lc<Ops, true>(b[0], I);
+    if (top >= 2) {
+        const F A2 = g.template sq_first<Ops>(A);
+        F P = A2;
+#pragma unroll 1
+        for (int e = 2; e <= top; e += 2) {
+            if (e > 2) P = g.template mm<Ops>(A2, P, false);  // matmul(pow[0], pow.back())
+            if (e + 1 <= m) acc_term<Ops>(odd, b[e + 1], P);
+            acc_term<Ops>(V, b[e], P);
+        }
+    }
+    if (m >= 3) {
+        U = g.template mm<Ops>(A, odd, false);
+    } else {  // scaled(a, b1)
+#pragma unroll
+        for (int e = 0; e < F::kCount; ++e) U.v[e] = Ops::mul(b[1], A.v[e]);
+    }
+}
+
+// LU with partial pivoting and the solve of pade_solve (lu_solve,
+// dense_matrix.cpp:112-118 -> kernels.cpp:55-112), cooperatively by the
+// group on M (n x n, stride LD, overwritten by its factors) and R (the
+// right-hand sides, overwritten by the solution). Always in the reference's
+// arithmetic: every multiply, subtract and divide rounded separately. The row
+// swaps are applied to R as they happen, which is the reference's
+// rhs[perm[i]] gather. Returns false for a singular denominator (a zero pivot
+// column, kernels.cpp:71-72).
+__device__ __forceinline__ double lu_fms(double a, double l, double p) {
+    return __dsub_rn(a, __dmul_rn(l, p));
+}
+__device__ __forceinline__ double lu_div(double a, double b) { return __ddiv_rn(a, b); }
+
+template <class G, class T>
+__device__ bool lu_solve_group(const G& g, T* M, T* R, int* flag) {
+    constexpr int N = G::NDIM, LD = G::LD, TH = G::THREADS;
+    static_assert(TH % N == 0, "threads cover whole columns");
+    constexpr int RS = TH / N;  // row phases of the trailing update
+    const int j = g.tid % N, r0 = g.tid / N;
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        if (g.warp == 0) {
+            // pivot: the first row holding the largest |M[i][k]|, i >= k, with
+            // the reference's strict '>' scan from |M[k][k]| (NaN never wins;
+            // a NaN diagonal keeps p = k)
+            T best = T(-1);
+            int p = N;
+            for (int i = k + g.lane; i < N; i += 32) {
+                const T v = fabs(M[i * LD + k]);
+                if (v > best) {
+                    best = v;
+                    p = i;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const T ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int op = __shfl_xor_sync(0xffffffffu, p, o);
+                if (ob > best || (ob == best && op < p)) {
+                    best = ob;
+                    p = op;
+                }
+            }
+            const T vk = fabs(M[k * LD + k]);
+            if (vk != vk) p = k;
+            if (g.lane == 0) *flag = (vk == vk && best == T(0)) ? -1 : p;
+        }
+        g.sync();
+        const int p = *flag;
+        if (p < 0) return false;
+        if (p != k && g.tid < N) {  // swap rows k and p of M and R
+            const T m0 = M[k * LD + j], r0v = R[k * LD + j];
+            M[k * LD + j] = M[p * LD + j];
+            R[k * LD + j] = R[p * LD + j];
+            M[p * LD + j] = m0;
+            R[p * LD + j] = r0v;
+        }
+        g.sync();
+        const T piv = M[k * LD + k];
+        for (int i = k + 1 + g.tid; i < N; i += TH) M[i * LD + k] = lu_div(M[i * LD + k], piv);
+        g.sync();
+        if (j > k) {
+            const T pk = M[k * LD + j];
+            for (int i = k + 1 + r0; i < N; i += RS) M[i * LD + j] = lu_fms(M[i * LD + j], M[i * LD + k], pk);
+        }
+        g.sync();
+    }
+    if (g.tid < N) {  // one right-hand-side column per thread (lu_apply)
+        const int c = g.tid;
+#pragma unroll 1
+        for (int i = 1; i < N; ++i) {
+            T s = R[i * LD + c];
+            for (int q = 0; q < i; ++q) s = lu_fms(s, M[i * LD + q], R[q * LD + c]);
+            R[i * LD + c] = s;
+        }
+#pragma unroll 1
+        for (int i = N - 1; i >= 0; --i) {
+            T s = R[i * LD + c];
+            for (int q = i + 1; q < N; ++q) s = lu_fms(s, M[i * LD + q], R[q * LD + c]);
+            R[i * LD + c] = lu_div(s, M[i * LD + i]);
+        }
+    }
+    return true;
+}
+
+// pade_solve (pade.cpp:26-28): X = (V - U)^-1 (V + U); false when singular
+template <class Ops, class G>
+__device__ __forceinline__ bool pade_solve(const G& g, const typename G::Frag& U,
+                                           const typename G::Frag& V, typename G::Frag& X) {
+    g.stage_solve(lc<Ops>(1.0, V, -1.0, U), addm<Ops>(V, U));  // sub(v, u), add(v, u)
+    if (!lu_solve_group(g, g.lu_m(), g.lu_r(), g.lu_flag())) return false;
+    X = g.solved();
+    return true;
+}
+
+template <class Ops, int kFam = MEXP_FAMILY_TAYLOR_NEW, class G>
 __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename G::Frag& A0,
                                                      int degree, int s, int fast_tail = 0,
-                                                     int family = MEXP_FAMILY_TAYLOR_NEW) {
+                                                     bool* singular = nullptr) {
     using F = typename G::Frag;
     F A = A0;
     if (s > 0) {  // scaled(a, 2^-s) (expm.cpp:47 -> kernels.cpp:39-42), exact
@@ -371,8 +554,19 @@ __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename 
 #pragma unroll
         for (int e = 0; e < G::K; ++e) A.v[e] = __dmul_rn(f, A.v[e]);
     }
-    F X = family == MEXP_FAMILY_TAYLOR_PS ? eval_taylor_ps<Ops>(g, degree, A)
-                                          : eval_taylor_new<Ops>(g, degree, A);
+    F X;
+    if constexpr (kFam == MEXP_FAMILY_PADE) {
+        F U, V;
+        eval_pade<Ops>(g, degree, A, U, V);
+        if (!pade_solve<Ops>(g, U, V, X)) {
+            *singular = true;
+            return X;
+        }
+    } else if constexpr (kFam == MEXP_FAMILY_TAYLOR_PS) {
+        X = eval_taylor_ps<Ops>(g, degree, A);
+    } else {
+        X = eval_taylor_new<Ops>(g, degree, A);
+    }
     // squarings, expm.cpp:31-35. With reference rounding, the last
     // `fast_tail` of them may use FMA/DMMA rounding: a rounding difference
     // made at squaring i is amplified ~2^(s-i) by the squarings after it, so
@@ -469,10 +663,16 @@ __global__ void __launch_bounds__(32 * TileShape<N>::W * GPC, TileShape<N>::MIN_
         } else {
             const bool exact = rounding == MEXP_ROUND_REFERENCE ||
                                (rounding == MEXP_ROUND_AUTO && sl.s >= exact_s_min);
+            bool singular = false;
             if (exact)
-                X = run_expm<ExactOps>(g, A, sl.degree, sl.s, 0, family);
+                X = run_expm<ExactOps, family>(g, A, sl.degree, sl.s, 0, &singular);
             else
-                X = run_expm<FastOps>(g, A, sl.degree, sl.s, 0, family);
+                X = run_expm<FastOps, family>(g, A, sl.degree, sl.s, 0, &singular);
+            if (singular) {  // "singular denominator" (kernels.cpp:71-72)
+#pragma unroll
+                for (int e = 0; e < G::K; ++e) X.v[e] = __longlong_as_double(0x7ff8000000000000ll);
+                if (sel && g.tid == 0) sel[m].status = MEXP_ERR_SINGULAR;
+            }
         }
         g.store_global(out + m * NN, X);
     }

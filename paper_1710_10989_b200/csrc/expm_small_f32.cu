@@ -281,8 +281,11 @@ __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
                 for (int e = 0; e < G::K; ++e)
                     A.v[e] = make_float2(float(f * double(A.v[e].x)), float(f * double(A.v[e].y)));
             }
-            X = family == MEXP_FAMILY_TAYLOR_PS ? eval_taylor_ps<F32Ops>(g, sl.degree, A)
-                                                : eval_taylor_new<F32Ops>(g, sl.degree, A);
+            // (the Pade family in fp32 storage runs on the fp64 engine, capi.cu)
+            if constexpr (family == MEXP_FAMILY_TAYLOR_PS)
+                X = eval_taylor_ps<F32Ops>(g, sl.degree, A);
+            else
+                X = eval_taylor_new<F32Ops>(g, sl.degree, A);
             for (int i = 0; i < sl.s; ++i) X = g.template mm<F32Ops>(X, X, true);
         }
         g.store_global(out + m * NN, X);

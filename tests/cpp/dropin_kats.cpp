@@ -81,7 +81,11 @@ static void host_only() {
         CHECK(select(2.0 * norm, tn).s == select(norm, tn).s + 1);
     CHECK(tn.entries.size() == 6 && tn.theta_max() == 1.09 && tn.asymptotic().products == 5);
     CHECK(unit_roundoff(Accuracy::Single) == std::ldexp(1.0, -24));
-    CHECK(throws<std::invalid_argument>([] { selection_table(Family::PadeDiagonal, Accuracy::Double); }));
+    // Family::PadeDiagonal (theta_tables.cpp:61-73)
+    const auto& pd = selection_table(Family::PadeDiagonal, Accuracy::Double);
+    CHECK(pd.entries.size() == 13 && pd.theta_max() == 5.37 && pd.asymptotic().degree == 26);
+    CHECK(select(3.141592653589793, pd).degree == 22 && select(0.5, pd).degree == 12 &&
+          select(10.0, pd).s == 1);
     // Family::TaylorPS (theta_tables.cpp:53-59)
     const auto& ps = selection_table(Family::TaylorPS, Accuracy::Double);
     CHECK(ps.entries.size() == 6 && ps.theta_max() == 7.80e-1 && ps.asymptotic().degree == 16 &&
@@ -115,8 +119,14 @@ static void device_cases() {
     DenseMatrix bad(2);
     bad.at(0, 1) = std::numeric_limits<double>::infinity();
     CHECK(throws<std::invalid_argument>([&] { expm(bad, Accuracy::Double, Family::TaylorNew); }));
-    // Pade is not on the B200 path
-    CHECK(throws<std::invalid_argument>([] { expm(DenseMatrix(2), Accuracy::Double, Family::PadeDiagonal); }));
+    // Pade family: rotation by pi -> r22, no scaling, 6 products + 4/3 for the solve
+    const auto rpd = expm(DenseMatrix::from_rows({{0, pi}, {-pi, 0}}), Accuracy::Double,
+                          Family::PadeDiagonal);
+    CHECK(rpd.degree == 22 && rpd.s == 0 && rpd.cost_thirds == 22);
+    CHECK(norm1(DenseMatrix::from_rows({{rpd.result.at(0, 0) + 1, rpd.result.at(0, 1)},
+                                        {rpd.result.at(1, 0), rpd.result.at(1, 1) + 1}})) <= 1e-12);
+    // Pade beyond n = 64 is not built
+    CHECK(throws<std::invalid_argument>([] { expm(DenseMatrix(65), Accuracy::Double, Family::PadeDiagonal); }));
     // Paterson-Stockmeyer family: rotation by pi -> m = 16, s = 3, 6 + 3 products
     const auto rps = expm(DenseMatrix::from_rows({{0, pi}, {-pi, 0}}), Accuracy::Double,
                           Family::TaylorPS);

@@ -100,12 +100,55 @@ def taylor_ps(ref):
     print(f"wrote taylor_ps.npz: {len(norms)} select norms, {len(case_norms)} cases per n")
 
 
+def pade(ref):
+    """tests/golden/pade.npz: Family::PadeDiagonal selection at every theta
+    boundary, pade_coeffs(1..13), and expm cases covering every order 2..26
+    (both tables) with s up to 7."""
+    theta = {1: [3.65e-8, 5.32e-4, 1.50e-2, 8.54e-2, 2.54e-1, 5.41e-1, 9.50e-1, 1.47, 2.10,
+                 2.81, 3.60, 4.46, 5.37],
+             0: [8.46e-4, 8.09e-2, 4.26e-1, 1.05, 1.88, 2.85, 3.93, 5.06, 6.25, 7.47, 8.71,
+                 9.97, 11.2]}
+    norms = [0.0, 1.0, 10.0, 0.5, 1e-300, 1e300, 3.0, 100.0]
+    for acc in (0, 1):
+        for t in theta[acc]:
+            norms += [t, np.nextafter(t, 0.0), np.nextafter(t, np.inf)]
+            for k in range(1, 8):
+                v = np.ldexp(t, k)
+                norms += [v, np.nextafter(v, 0.0), np.nextafter(v, np.inf)]
+    norms = np.array(sorted(set(norms)), np.float64)
+    arrays = {"norms": norms}
+    for acc in (0, 1):
+        sel = np.array([ref.select(float(v), acc, 2) for v in norms], np.int32)
+        arrays[f"status_acc{acc}"], arrays[f"degree_acc{acc}"], arrays[f"s_acc{acc}"] = sel.T
+    arrays["coeffs"] = np.stack([np.pad(ref.pade_coeffs(m), (0, 13 - m)) for m in range(1, 14)])
+    rng = np.random.default_rng(26)
+    case_norms = sorted(set(theta[1] + [1e-9, 4.0, 20.0, 300.0] +
+                            [0.9 * t for t in theta[0]] + [0.9 * t for t in theta[1]]))
+    for n in (1, 2, 3, 8, 13, 16, 32, 64):
+        # every order of the double table (and s up to 6) at the large sizes
+        nv = case_norms if n <= 16 else [0.9 * t for t in theta[1]] + [20.0, 300.0]
+        a = np.stack([random_with_norm(rng, n, v) for v in nv])
+        arrays[f"n{n}_a"] = a
+        for acc in (0, 1):
+            r = ref.expm_batch(a, accuracy=acc, family=2)
+            arrays[f"n{n}_acc{acc}_out"] = r.out
+            arrays[f"n{n}_acc{acc}_meta"] = np.stack(
+                [r.degree, r.s, r.cost_thirds, r.status], axis=1).astype(np.int64)
+            arrays[f"n{n}_acc{acc}_norm"] = r.norm_in
+    np.savez_compressed(os.path.join(OUT, "pade.npz"), **arrays)
+    print(f"wrote pade.npz: {len(norms)} select norms, {len(case_norms)} cases per n")
+
+
 def main():
     ref = Reference()
     if "--only-ps" in sys.argv:
         taylor_ps(ref)
         return
+    if "--only-pade" in sys.argv:
+        pade(ref)
+        return
     taylor_ps(ref)
+    pade(ref)
     # selection
     norms = select_cases()
     sel = {}

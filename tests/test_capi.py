@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.mexp_abi_version() == 1
+    assert lib.mexp_abi_version() == 2
 
 
 def test_no_torch_types_in_signatures():
@@ -102,17 +102,32 @@ def test_select_kats():
             mx.select(bad, t)
 
 
-def test_pade_family_is_refused(lib):
-    # Family::PadeDiagonal is not on the B200 path; no CPU fallback for it
-    with pytest.raises(ValueError, match="unsupported"):
-        mx.selection_table(mx.Family.PadeDiagonal, mx.Accuracy.Double)
-    a = np.eye(3)
-    out = np.empty_like(a)
-    st = lib.mexp_expm(a.ctypes.data, 3, 1, int(mx.Family.PadeDiagonal), out.ctypes.data, None)
-    assert st == mx.ERR_UNSUPPORTED
+def test_pade_selection_table_and_select(golden, oracle):
+    """Family::PadeDiagonal table (theta_tables.cpp:61-73): 13 orders whose
+    products tie in pairs/triples; mexp_select (the kernels' select_device)
+    against the reference's selections and the restated ldexp loop."""
+    t = mx.selection_table(mx.Family.PadeDiagonal, mx.Accuracy.Double)
+    assert [e.degree for e in t.entries] == list(range(2, 27, 2))
+    assert [e.products for e in t.entries] == [0, 1, 2, 3, 3, 4, 4, 5, 5, 5, 6, 6, 6]
+    assert t.entries[-1].theta == 5.37
+    assert mx.selection_table(mx.Family.PadeDiagonal, mx.Accuracy.Single).entries[-1].theta == 11.2
+    g = golden("pade.npz")
+    rng = np.random.default_rng(7)
+    for acc in (0, 1):
+        table = mx.selection_table(mx.Family.PadeDiagonal, mx.Accuracy(acc))
+        for v, d, s, st in zip(g["norms"], g[f"degree_acc{acc}"], g[f"s_acc{acc}"],
+                               g[f"status_acc{acc}"]):
+            if st == 0:
+                assert mx.select(float(v), table) == (d, s), (v, acc)
+        for v in 10.0 ** rng.uniform(-20, 308, 3000):
+            st, d, s = oracle.select(float(v), acc, 2)
+            assert mx.select(float(v), table) == (d, s), (v, acc)
+
+
+def test_pade_status_and_large_n_refusal(lib):
+    assert lib.mexp_status_string(mx.ERR_SINGULAR) == b"singular denominator"  # kernels.cpp:72
     d, s = C.c_int32(), C.c_int32()
-    assert lib.mexp_select(1.0, 1, int(mx.Family.PadeDiagonal), C.byref(d),
-                           C.byref(s)) == mx.ERR_UNSUPPORTED
+    assert lib.mexp_select(1.0, 1, 7, C.byref(d), C.byref(s)) == mx.ERR_INVALID_ARGUMENT
 
 
 def test_ps_selection_table_and_select(golden):

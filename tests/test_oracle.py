@@ -341,3 +341,90 @@ def test_ps_oracle_bitwise_equals_reference(oracle, reference):
             assert np.array_equal(r1.out.view(np.uint64), r2.out.view(np.uint64)), (n, acc)
             for f in ("degree", "s", "cost_thirds", "norm_in", "status"):
                 assert np.array_equal(getattr(r1, f), getattr(r2, f)), f
+
+
+# ---- Family::PadeDiagonal (§8(f) next row) ---------------------------------
+def test_pade_select_matches_golden(oracle, golden):
+    g = golden("pade.npz")
+    for acc in (0, 1):
+        for v, d, s, st in zip(g["norms"], g[f"degree_acc{acc}"], g[f"s_acc{acc}"],
+                               g[f"status_acc{acc}"]):
+            got = oracle.select(float(v), acc, 2)
+            assert got[0] == st
+            if st == 0:
+                assert got[1:] == (d, s), (v, acc)
+
+
+def test_pade_coefficients(oracle, golden):
+    """pade_coeffs(1..13): the oracle's int128 / long double restatement and
+    the device table (expm_common.cuh c_pade) equal the reference's doubles."""
+    g = golden("pade.npz")["coeffs"]
+    for m in range(1, 14):
+        assert np.array_equal(oracle.pade_coeffs(m).view(np.uint64), g[m - 1, :m + 1].view(np.uint64))
+    src = open(os.path.join(ROOT, "paper_1710_10989_b200", "csrc", "expm_common.cuh")).read()
+    body = src[src.index("constexpr double c_pade[13][14]"):]
+    body = body[body.index("{") + 1:body.index("};")]
+    vals = [float.fromhex(t) if "0x" in t else float(t)
+            for t in re.findall(r"0x[0-9a-fA-Fp.+-]+|\d+\.\d+", body)]
+    dev = np.array(vals).reshape(13, 14)
+    assert np.array_equal(dev.view(np.uint64), g.view(np.uint64))
+
+
+def test_pade_expm_matches_golden_bitwise(oracle, golden):
+    g = golden("pade.npz")
+    degrees = set()
+    for n in (1, 2, 3, 8, 13, 16, 32, 64):
+        a = g[f"n{n}_a"]
+        for acc in (0, 1):
+            r = oracle.expm_batch(a, accuracy=acc, family=2)
+            meta = g[f"n{n}_acc{acc}_meta"]
+            assert np.array_equal(r.status, meta[:, 3])
+            assert np.array_equal(r.degree, meta[:, 0]) and np.array_equal(r.s, meta[:, 1])
+            assert np.array_equal(r.cost_thirds, meta[:, 2])
+            assert np.array_equal(r.norm_in, g[f"n{n}_acc{acc}_norm"])
+            assert np.array_equal(r.out.view(np.uint64), g[f"n{n}_acc{acc}_out"].view(np.uint64)), (n, acc)
+            degrees |= set(int(d) for d in r.degree)
+    assert degrees == set(range(2, 27, 2))
+
+
+def test_pade_approximant_kats(oracle):
+    """r_m(A) approximates exp(A) (pade.hpp); order 2 is (I - A/2)^-1 (I + A/2);
+    invalid orders refuse (pade.cpp:79-80)."""
+    rng = np.random.default_rng(4)
+    a = rng.uniform(-1, 1, (5, 5))
+    a *= 0.2 / l1(a)
+    want = np.eye(5)
+    term = np.eye(5)
+    for j in range(1, 30):
+        term = term @ a / j
+        want = want + term
+    for order in range(2, 27, 2):
+        k, got = oracle.eval_pade(a, order)
+        assert k >= 0
+        if order >= 12:
+            assert np.abs(got - want).max() < 1e-15, order
+    k, r2 = oracle.eval_pade(a, 2)
+    assert k == 0
+    assert np.allclose(r2, np.linalg.solve(np.eye(5) - a / 2, np.eye(5) + a / 2), atol=1e-15)
+    for bad in (0, 3, 28):
+        assert oracle.eval_pade(a, bad)[0] == -1
+
+
+def test_pade_oracle_bitwise_equals_reference(oracle, reference):
+    rng = np.random.default_rng(12)
+    for n in (3, 8, 20):
+        for order in range(2, 27, 2):
+            a = rng.standard_normal((n, n))
+            a *= 0.5 / l1(a)
+            k1, x1 = oracle.eval_pade(a, order)
+            k2, x2 = reference.eval_pade(a, order)
+            assert k1 == k2 and np.array_equal(x1.view(np.uint64), x2.view(np.uint64)), (n, order)
+        norms = 10.0 ** rng.uniform(-9, 2.5, 64)
+        a = rng.standard_normal((64, n, n))
+        a *= (norms / np.abs(a).sum(axis=1).max(axis=1))[:, None, None]
+        for acc in (0, 1):
+            r1 = reference.expm_batch(a, accuracy=acc, family=2)
+            r2 = oracle.expm_batch(a, accuracy=acc, family=2)
+            assert np.array_equal(r1.out.view(np.uint64), r2.out.view(np.uint64)), (n, acc)
+            for f in ("degree", "s", "cost_thirds", "norm_in", "status"):
+                assert np.array_equal(getattr(r1, f), getattr(r2, f)), f
