@@ -76,8 +76,17 @@ KERNEL_NAME = {
 }
 
 
-def flops_per_matrix(n, degree, s):
-    prods = np.vectorize({1: 0, 2: 1, 4: 2, 8: 3, 12: 4, 18: 5}.get)(degree)
+FAMILIES = {"taylor-new": 0, "taylor-ps": 1, "pade": 2}
+# products per degree of each family's table (theta_tables.cpp:45-73); the
+# Pade solve counts 4/3 of a product (expm.cpp:70-72)
+PRODUCTS = {0: {1: 0, 2: 1, 4: 2, 8: 3, 12: 4, 18: 5},
+            1: {1: 0, 2: 1, 4: 2, 6: 3, 9: 4, 16: 6},
+            2: {2: 0, 4: 1, 6: 2, 8: 3, 10: 3, 12: 4, 14: 4, 16: 5, 18: 5, 20: 5, 22: 6, 24: 6,
+                26: 6}}
+
+
+def flops_per_matrix(n, degree, s, family=0):
+    prods = np.vectorize(PRODUCTS[family].get)(degree) + (4.0 / 3.0 if family == 2 else 0.0)
     return 2.0 * n ** 3 * (prods + s)
 
 
@@ -137,7 +146,7 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- CPU arms --
 def _ref_worker(args):
-    key, b0, count, chunk = args
+    key, b0, count, chunk, family = args
     os.environ["OMP_NUM_THREADS"] = "1"
     from oracle.oracle import Reference
     ref = Reference()
@@ -146,16 +155,16 @@ def _ref_worker(args):
     t0 = time.perf_counter()
     done = 0
     for c in range(0, count, chunk):
-        ref.expm_batch(a[c:c + chunk], accuracy=cfg.accuracy)
+        ref.expm_batch(a[c:c + chunk], accuracy=cfg.accuracy, family=family)
         done += min(chunk, count - c)
     return done, time.perf_counter() - t0
 
 
-def cpu_reference_rate(key, matrices_per_worker, workers, pool=None):
+def cpu_reference_rate(key, matrices_per_worker, workers, pool=None, family=0):
     """Aggregate expm/s of the compiled reference over `workers` processes."""
     cfg = workloads.CONFIGS[key]
     tasks = [(key, (w * matrices_per_worker) % max(cfg.batch - matrices_per_worker, 1),
-              matrices_per_worker, 256) for w in range(workers)]
+              matrices_per_worker, 256, family) for w in range(workers)]
     own = pool is None
     if own:
         pool = mp.get_context("spawn").Pool(workers)
@@ -204,6 +213,8 @@ def parse():
     p.add_argument("--config", default="cfg2", choices=sorted(workloads.CONFIGS))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--rounding", default="auto", choices=["auto", "reference", "fast"])
+    p.add_argument("--family", default="taylor-new", choices=sorted(FAMILIES),
+                   help="Family (theta_tables.hpp:8); the headline is taylor-new")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=10)
     return p.parse_args()
@@ -226,11 +237,12 @@ def run_reference_arm(args):
     pool = mp.get_context("spawn").Pool(cores)
     try:
         for _ in range(max(args.warmup, 1)):
-            cpu_reference_rate(args.config, max(per // 8, 1), cores, pool)
+            cpu_reference_rate(args.config, max(per // 8, 1), cores, pool, FAMILIES[args.family])
         rates = []
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            r, done, wall = cpu_reference_rate(args.config, max(per // 8, 1), cores, pool)
+            r, done, wall = cpu_reference_rate(args.config, max(per // 8, 1), cores, pool,
+                                               FAMILIES[args.family])
             rates.append(r)
             if time.perf_counter() - t0 > 120:  # bound the arm to ~2 minutes
                 break
@@ -247,7 +259,7 @@ def run_reference_arm(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": cfg.dtype, "data": "synthetic (seeded, counter-based; see workloads.py)",
         "config": {"workload": args.config, "description": cfg.description, "n": cfg.n,
-                   "batch": cfg.batch, "parallelism": "host processes"},
+                   "batch": cfg.batch, "family": args.family, "parallelism": "host processes"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -275,6 +287,7 @@ def run_ours(args):
     torch_dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
     rounding = {"auto": mx.ROUND_AUTO, "reference": mx.ROUND_REFERENCE,
                 "fast": mx.ROUND_FAST}[args.rounding]
+    fam = FAMILIES[args.family]
     esz = 8 if cfg.dtype == "f64" else 4
     mat_bytes = n * n * esz
     # two input/output buffer pairs alternate so the working set exceeds L2
@@ -286,13 +299,13 @@ def run_ours(args):
 
     def step(i):
         mx.expm_batched(ins[i % pairs], outs[i % pairs], sel, accuracy=mx.Accuracy(cfg.accuracy),
-                        rounding=rounding, stream=stream)
+                        rounding=rounding, stream=stream, family=mx.Family(fam))
 
     for i in range(max(args.warmup, 3)):
         step(i)
     torch.cuda.synchronize()
     sels = sel.cpu().numpy().view(mx.SELECTION_DTYPE)
-    flops = float(flops_per_matrix(n, sels["degree"], sels["s"]).sum())
+    flops = float(flops_per_matrix(n, sels["degree"], sels["s"], fam).sum())
 
     if world > 1:
         dist.barrier()
@@ -318,12 +331,14 @@ def run_ours(args):
     h_in = torch.from_numpy(a_host).pin_memory()
     h_out = torch.empty_like(h_in).pin_memory()
     for _ in range(2):
-        mx.expm_batched_host(h_in, h_out, accuracy=mx.Accuracy(cfg.accuracy), rounding=rounding)
+        mx.expm_batched_host(h_in, h_out, accuracy=mx.Accuracy(cfg.accuracy), rounding=rounding,
+                             family=mx.Family(fam))
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        mx.expm_batched_host(h_in, h_out, accuracy=mx.Accuracy(cfg.accuracy), rounding=rounding)
+        mx.expm_batched_host(h_in, h_out, accuracy=mx.Accuracy(cfg.accuracy), rounding=rounding,
+                             family=mx.Family(fam))
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
         e2e_s = max_over_ranks(e2e_s, dev)
@@ -348,7 +363,8 @@ def run_ours(args):
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
-            traffic = json.load(open(tpath)).get(f"{args.config}_{args.rounding}")
+            key = f"{args.config}_{args.rounding}" + ("" if fam == 0 else f"_{args.family}")
+            traffic = json.load(open(tpath)).get(key)
         peakc, peakc_src = compute_peak_tflops(cfg.dtype)
         tflops = flops / (ms_step * 1e-3) / 1e12
         if ROOFLINE_BOUND[args.config] == "hbm":
@@ -358,7 +374,7 @@ def run_ours(args):
         else:
             roof = {"bound": "tensor", "achieved": tflops, "peak": peakc, "unit": "TFLOP/s",
                     "frac": tflops / peakc, "traffic": traffic, "peak_source": peakc_src}
-        roof["kernel"] = KERNEL_NAME[args.config]
+        roof["kernel"] = KERNEL_NAME[args.config] if fam == 0 else f"{args.family} kernels"
         roof["algorithmic"] = (f"{alg_bytes / 1e6:.1f} MB (A in + e^A out) and "
                                f"{flops / 1e9:.2f} GFLOP (sum 2 n^3 (pi_m + s)) per step")
         line = {
@@ -368,6 +384,7 @@ def run_ours(args):
             "dtype": cfg.dtype, "data": "synthetic (seeded, counter-based; see workloads.py)",
             "config": {"workload": args.config, "description": cfg.description, "n": n,
                        "batch_per_rank": B, "global_batch": world * B, "rounding": args.rounding,
+                       "family": args.family,
                        "parallelism": f"matrix-sharded x{world}",
                        "l2": f"inputs larger than L2 ({pairs} x {2 * B * mat_bytes / 2**20:.0f} MiB "
                              f"in+out, alternating buffers)"},
@@ -388,7 +405,7 @@ def run_ours(args):
         if not args.no_cpu_baseline and world == 1:
             cores = host_cores()
             per = per_worker_sample(args.config)
-            rate, done, wall = cpu_reference_rate(args.config, per, cores)
+            rate, done, wall = cpu_reference_rate(args.config, per, cores, family=fam)
             line["cpu_baseline"] = {
                 "value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
                 "sample": f"{done} matrices of {args.config} ({per} per worker process, "

@@ -3,7 +3,7 @@
  * exponential built on the reduced-product Taylor schemes of arXiv 1710.10989
  * (Family::TaylorNew of the reference `mexp` library), with the reference's
  * two comparison families: Paterson-Stockmeyer Taylor (TaylorPS) and the
- * diagonal Pade approximants (PadeDiagonal, n <= 64).
+ * diagonal Pade approximants (PadeDiagonal).
  *
  * The reference has no FFI layer: its operator boundary is the C++ API in
  * namespace mexp (proj/include/mexp/expm.hpp, theta_tables.hpp). Each entry
@@ -45,8 +45,8 @@ typedef enum {
 } mexp_status;
 
 /* theta_tables.hpp:8 (enum class Family). TaylorNew and TaylorPS run for every
- * n and dtype; PadeDiagonal (scaling and squaring with r_m, m = 2..26 even,
- * and a batched pivoted LU solve) for n <= 64. */
+ * n and dtype; so does PadeDiagonal (scaling and squaring with r_m,
+ * m = 2..26 even, and a batched pivoted LU solve). */
 typedef enum { MEXP_FAMILY_TAYLOR_NEW = 0, MEXP_FAMILY_TAYLOR_PS = 1, MEXP_FAMILY_PADE = 2 } mexp_family;
 
 /* theta_tables.hpp:9 (enum class Accuracy): selects the theta table, i.e. the

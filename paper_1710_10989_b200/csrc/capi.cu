@@ -280,10 +280,8 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
     if (batch == 0) return MEXP_OK;
     if (n > 64) {
         // the large-n engine is tensor-core DMMA only: no reference-rounded
-        // GEMM, no fp32 path and no Pade solve beyond n = 64
-        if (dtype != MEXP_F64 || rounding == MEXP_ROUND_REFERENCE ||
-            (accuracy >> 4) == MEXP_FAMILY_PADE)
-            return MEXP_ERR_UNSUPPORTED;
+        // GEMM and no fp32 path beyond n = 64
+        if (dtype != MEXP_F64 || rounding == MEXP_ROUND_REFERENCE) return MEXP_ERR_UNSUPPORTED;
         const int r = large_expm_f64(static_cast<const double*>(d_a), static_cast<double*>(d_out),
                                      d_sel, n, batch, accuracy, st, &g_launches);
         if (r == MEXP_ERR_CUDA) g_last_cuda_error = large_last_error();

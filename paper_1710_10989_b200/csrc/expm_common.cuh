@@ -169,21 +169,23 @@ __host__ __device__ __forceinline__ double pade_theta(int accuracy, int e) {
 // pade_coeffs(m).b (pade.cpp:34-48: exact integer ratios, rounded once via
 // long double) as the compiled reference holds them, b_0..b_m for m = 1..13;
 // checked bit for bit by tests/test_oracle.py::test_pade_coefficients.
-__device__ constexpr double c_pade[13][14] = {
-    {1.0, 0x1.0000000000000p-1, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.5555555555555p-4, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.999999999999ap-4, 0x1.1111111111111p-7, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.b6db6db6db6dbp-4, 0x1.8618618618618p-7, 0x1.3813813813814p-11, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.c71c71c71c71cp-4, 0x1.c71c71c71c71cp-7, 0x1.0410410410410p-10, 0x1.1566abc011567p-15, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.d1745d1745d17p-4, 0x1.f07c1f07c1f08p-7, 0x1.4afd6a052bf5bp-10, 0x1.08cabb37565e2p-14, 0x1.937e11175f095p-20, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.d89d89d89d89ep-4, 0x1.0690690690690p-6, 0x1.7de952f2466a4p-10, 0x1.6ea28d118b474p-14, 0x1.b287c3a303e2bp-19, 0x1.f09b28ba4d955p-25, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.ddddddddddddep-4, 0x1.1111111111111p-6, 0x1.a41a41a41a41ap-10, 0x1.c01c01c01c01cp-14, 0x1.45e5d2ba42ea0p-18, 0x1.29f6b20961c00p-23, 0x1.08db48ebe51c7p-29, 0.0, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.e1e1e1e1e1e1ep-4, 0x1.1919191919192p-6, 0x1.c1c1c1c1c1c1cp-10, 0x1.0101010101010p-13, 0x1.a5c001a5c001ap-18, 0x1.e20001e20001ep-23, 0x1.5e8ba44745d2dp-28, 0x1.f28db670be53bp-35, 0.0, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.e50d79435e50dp-4, 0x1.1f7047dc11f70p-6, 0x1.d96da388960f5p-10, 0x1.1c0e9551f3a2dp-13, 0x1.f8fd7b3c5bcc1p-18, 0x1.49ca1c3c50d8ep-22, 0x1.306bcb4b5e520p-27, 0x1.68cb9b9bb2285p-33, 0x1.a3d5a71b92cd3p-40, 0.0, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.e79e79e79e79ep-4, 0x1.2492492492492p-6, 0x1.ecc07b301ecc0p-10, 0x1.3299e6401329ap-13, 0x1.2090d8b4c6bdcp-17, 0x1.9c3ca34b650f1p-22, 0x1.b7b825a5c1212p-27, 0x1.4f06351093257p-32, 0x1.49deba27f3581p-38, 0x1.3fdfbc45c52eap-45, 0.0, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.e9bd37a6f4deap-4, 0x1.28cfc4a33f129p-6, 0x1.fcd1e360fe68fp-10, 0x1.45a50c670938fp-13, 0x1.3fee80f4f29acp-17, 0x1.e783d0b234bb0p-22, 0x1.1ec6024ab59b3p-26, 0x1.fdd1cb2f7bbe9p-32, 0x1.4648d3f56deaap-37, 0x1.0f328eed3d6fep-43, 0x1.bd0ac3296b624p-51, 0.0},
-    {1.0, 0x1.0000000000000p-1, 0x1.eb851eb851eb8p-4, 0x1.2c5f92c5f92c6p-6, 0x1.0531b747fa105p-9, 0x1.55ed4d05c9af0p-13, 0x1.5b5ab7e55f2bap-17, 0x1.15e22cb77f562p-21, 0x1.5f02bf38a0d89p-26, 0x1.5aad6134c4c94p-31, 0x1.05070ff78b221p-36, 0x1.1cc1e2df80824p-42, 0x1.94fcfe65b1145p-49, 0x1.1cd3b01a822a6p-56},
-};
+#define MEXP_PADE_TABLE                                                               \
+    {{1.0, 0x1.0000000000000p-1, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.5555555555555p-4, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.999999999999ap-4, 0x1.1111111111111p-7, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.b6db6db6db6dbp-4, 0x1.8618618618618p-7, 0x1.3813813813814p-11, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.c71c71c71c71cp-4, 0x1.c71c71c71c71cp-7, 0x1.0410410410410p-10, 0x1.1566abc011567p-15, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.d1745d1745d17p-4, 0x1.f07c1f07c1f08p-7, 0x1.4afd6a052bf5bp-10, 0x1.08cabb37565e2p-14, 0x1.937e11175f095p-20, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.d89d89d89d89ep-4, 0x1.0690690690690p-6, 0x1.7de952f2466a4p-10, 0x1.6ea28d118b474p-14, 0x1.b287c3a303e2bp-19, 0x1.f09b28ba4d955p-25, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.ddddddddddddep-4, 0x1.1111111111111p-6, 0x1.a41a41a41a41ap-10, 0x1.c01c01c01c01cp-14, 0x1.45e5d2ba42ea0p-18, 0x1.29f6b20961c00p-23, 0x1.08db48ebe51c7p-29, 0.0, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.e1e1e1e1e1e1ep-4, 0x1.1919191919192p-6, 0x1.c1c1c1c1c1c1cp-10, 0x1.0101010101010p-13, 0x1.a5c001a5c001ap-18, 0x1.e20001e20001ep-23, 0x1.5e8ba44745d2dp-28, 0x1.f28db670be53bp-35, 0.0, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.e50d79435e50dp-4, 0x1.1f7047dc11f70p-6, 0x1.d96da388960f5p-10, 0x1.1c0e9551f3a2dp-13, 0x1.f8fd7b3c5bcc1p-18, 0x1.49ca1c3c50d8ep-22, 0x1.306bcb4b5e520p-27, 0x1.68cb9b9bb2285p-33, 0x1.a3d5a71b92cd3p-40, 0.0, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.e79e79e79e79ep-4, 0x1.2492492492492p-6, 0x1.ecc07b301ecc0p-10, 0x1.3299e6401329ap-13, 0x1.2090d8b4c6bdcp-17, 0x1.9c3ca34b650f1p-22, 0x1.b7b825a5c1212p-27, 0x1.4f06351093257p-32, 0x1.49deba27f3581p-38, 0x1.3fdfbc45c52eap-45, 0.0, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.e9bd37a6f4deap-4, 0x1.28cfc4a33f129p-6, 0x1.fcd1e360fe68fp-10, 0x1.45a50c670938fp-13, 0x1.3fee80f4f29acp-17, 0x1.e783d0b234bb0p-22, 0x1.1ec6024ab59b3p-26, 0x1.fdd1cb2f7bbe9p-32, 0x1.4648d3f56deaap-37, 0x1.0f328eed3d6fep-43, 0x1.bd0ac3296b624p-51, 0.0}, \
+     {1.0, 0x1.0000000000000p-1, 0x1.eb851eb851eb8p-4, 0x1.2c5f92c5f92c6p-6, 0x1.0531b747fa105p-9, 0x1.55ed4d05c9af0p-13, 0x1.5b5ab7e55f2bap-17, 0x1.15e22cb77f562p-21, 0x1.5f02bf38a0d89p-26, 0x1.5aad6134c4c94p-31, 0x1.05070ff78b221p-36, 0x1.1cc1e2df80824p-42, 0x1.94fcfe65b1145p-49, 0x1.1cd3b01a822a6p-56} \
+    }
+__device__ constexpr double c_pade[13][14] = MEXP_PADE_TABLE;
+constexpr double kPadeHost[13][14] = MEXP_PADE_TABLE;  // host copy (large-n schedule)
 // theta_m of entry e of a family's table: the reference's decimal literals
 // (theta_tables.cpp:45-51 TaylorNew, :53-59 TaylorPS)
 __host__ __device__ __forceinline__ double theta_entry(int family, int accuracy, int e) {

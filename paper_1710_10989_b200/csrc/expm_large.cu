@@ -20,8 +20,12 @@
 //   7. each matrix's last GEMM writes e^A straight into the caller's output
 //      (when n is a multiple of 128; otherwise an unpad copy at the end).
 //
+// Family::PadeDiagonal: the same GEMM chain forms U, V (pade.cpp:50-113) and,
+// in the last product's epilogue, M = V - U and R = V + U; lu_batched.cu then
+// overwrites R with M^-1 R before the squarings.
+//
 // GEMM: 128x128 CTA tile, 8 warps each 64x32 (8x4 DMMA m8n8k4 tiles, 64 fp64
-// accumulators per lane), k-tiles of 16 through a 4-stage cp.async ring in
+// accumulators per lane), k-tiles of 32 through a 3-stage cp.async ring in
 // shared memory (rows padded to 4 (mod 16) doubles: conflict-free fragment
 // loads). One DMMA occupies an SM sub-partition's FP64 pipe for 16 cycles, so
 // 32 independent DMMAs per k-step keep all four pipes saturated.
@@ -32,6 +36,7 @@
 
 #include "expm_common.cuh"
 #include "expm_large.cuh"
+#include "lu_batched.cuh"
 
 namespace mexp_b200 {
 
@@ -73,8 +78,9 @@ enum Epi : int {
     EPI_T4_1,     // c = A2; in = A         -> o0 = A2, o1 = (I/2 + A/6) + A2/24
     EPI_T4_2,     // c = inner*A2; in = A   -> o0 = (I + A) + c
     EPI_T2,       // c = A2; in = A         -> o0 = (I + A) + A2/2
-    EPI_PS_B,     // c = A^p; in = A, A2, A3 (or null) -> o0 = A^p,
-                  //   o_j = lc[j-1] . {I, A, A2, A3, A^p} for j = 1..nlc (Paterson-Stockmeyer)
+    EPI_PS_B,     // c = X*Y; in0..in2 (each may be null) -> o0 = c (unless !store_c),
+                  //   o_j = lc[j-1] . {I, in0, in1, in2, c} for j = 1..nlc
+                  //   (Paterson-Stockmeyer chunks, the Pade lincombs and M, R)
 };
 
 struct GemmArgs {
@@ -84,6 +90,7 @@ struct GemmArgs {
     double* out[5];
     double lc[4][5];      // EPI_PS_B coefficients (runtime: one kernel for every degree)
     int nlc;
+    int store_c;          // EPI_PS_B: write c to out[0]
     double* final_out;    // the caller's e^A buffer (list entries with bit 31 set)
     const int32_t* list;  // participating matrix indices (blockIdx.z); bit 31 set =
                           // this is the matrix's last product: out[0] -> final_out
@@ -162,9 +169,9 @@ __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, i
         const double2 a = ld(0);
         st(0, (id0 + a.x) + 0.5 * c0, (id1 + a.y) + 0.5 * c1);
     } else if constexpr (EPI == EPI_PS_B) {
-        const double2 a = ld(0), a2 = ld(1);
-        const double2 a3 = g.in[2] ? ld(2) : make_double2(0.0, 0.0);
-        st(0, c0, c1);
+        const double2 z = make_double2(0.0, 0.0);
+        const double2 a = g.in[0] ? ld(0) : z, a2 = g.in[1] ? ld(1) : z, a3 = g.in[2] ? ld(2) : z;
+        if (g.store_c) st(0, c0, c1);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (j >= g.nlc) break;
@@ -326,6 +333,32 @@ __global__ void unpad_kernel(const double* __restrict__ src, double* __restrict_
             out[m * int64_t(n) * n + int64_t(i) * n + j] = src[m * int64_t(np) * np + int64_t(i) * np + j];
 }
 
+// r_2 (no product): M = b0 I - b1 A, R = b0 I + b1 A (pade.cpp:99-109)
+__global__ void pade2_kernel(const double* __restrict__ a, double* __restrict__ m_out,
+                             double* __restrict__ r_out, int np, const int32_t* __restrict__ list,
+                             double b0, double b1) {
+    const int64_t m = list[blockIdx.y];
+    for (int i = blockIdx.x; i < np; i += gridDim.x)
+        for (int j = threadIdx.x; j < np; j += blockDim.x) {
+            const int64_t e = m * int64_t(np) * np + int64_t(i) * np + j;
+            const double id = i == j ? b0 : 0.0, u = b1 * a[e];
+            m_out[e] = id - u;
+            r_out[e] = id + u;
+        }
+}
+
+// NaN over e^A of the listed matrices whose Pade solve met a zero pivot
+__global__ void nan_singular_kernel(double* __restrict__ out, int n,
+                                    const int32_t* __restrict__ list,
+                                    const mexp_selection* __restrict__ sel) {
+    const int64_t m = list[blockIdx.y];
+    if (sel[m].status != MEXP_ERR_SINGULAR) return;
+    const int64_t total = int64_t(n) * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x)
+        out[m * total + e] = __longlong_as_double(0x7ff8000000000000ll);
+}
+
 // NaN for the listed matrices (per-matrix errors: non-finite input, norm overflow)
 __global__ void nan_kernel(double* __restrict__ out, int n, const int32_t* __restrict__ list) {
     const int64_t m = list[blockIdx.y];
@@ -358,6 +391,13 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
     for (int j = 0; j < nlc; ++j)
         for (int t = 0; t < 5; ++t) g.lc[j][t] = lc[j][t];
     g.nlc = nlc;
+    g.store_c = 1;
+    if (nlc < 0) {  // EPI_PS_B without the product itself
+        g.nlc = -nlc;
+        g.store_c = 0;
+        for (int j = 0; j < g.nlc; ++j)
+            for (int t = 0; t < 5; ++t) g.lc[j][t] = lc[j][t];
+    }
     g.list = d_list;
     g.np = np;
     g.mstride = int64_t(np) * np;
@@ -392,7 +432,9 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
                    int64_t batch, int acc_arg, cudaStream_t st, std::atomic<uint64_t>* launches) {
     const int np = (n + BM - 1) / BM * BM;
     const int64_t mat = int64_t(np) * np;
-    constexpr int kBuffers = 6;
+    const bool pade = (acc_arg >> 4) == MEXP_FAMILY_PADE;
+    constexpr int kMaxBuffers = 8;
+    const int kBuffers = pade ? 8 : 6;  // r26 keeps A, A2, A4, A6, two lincombs, V and u''
     // workspace: kBuffers padded matrices per batch entry + per-matrix scratch
     const size_t need = size_t(kBuffers) * batch * mat * sizeof(double);
     Workspace& ws = workspace();
@@ -401,7 +443,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         LCUDA(cudaMallocAsync(&ws.buf, need, st));
         ws.bytes = need;
     }
-    double* W[kBuffers];
+    double* W[kMaxBuffers] = {};
     for (int k = 0; k < kBuffers; ++k) W[k] = ws.buf + size_t(k) * batch * mat;
 
     unsigned long long* maxbits = nullptr;
@@ -422,7 +464,8 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     LCUDA(cudaMemcpyAsync(h_sel.data(), d_sel, sizeof(mexp_selection) * batch,
                           cudaMemcpyDeviceToHost, st));
     LCUDA(cudaStreamSynchronize(st));
-    std::vector<int32_t> by_deg[19];
+    constexpr int kMaxDeg = 26;
+    std::vector<int32_t> by_deg[kMaxDeg + 1];
     int max_s = 0;
     for (int64_t m = 0; m < batch; ++m) {
         if (h_sel[m].status != MEXP_OK) continue;
@@ -437,9 +480,9 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         return off;
     };
     std::vector<int32_t> all_ok;
-    for (int d = 1; d <= 18; ++d) all_ok.insert(all_ok.end(), by_deg[d].begin(), by_deg[d].end());
-    size_t off_deg[19] = {};
-    for (int d = 1; d <= 18; ++d) off_deg[d] = append(by_deg[d]);
+    for (int d = 1; d <= kMaxDeg; ++d) all_ok.insert(all_ok.end(), by_deg[d].begin(), by_deg[d].end());
+    size_t off_deg[kMaxDeg + 1] = {};
+    for (int d = 1; d <= kMaxDeg; ++d) off_deg[d] = append(by_deg[d]);
     // Schemes, then squarings. Each matrix's LAST product writes its e^A
     // straight into the caller's output when no padding is needed (np == n):
     // the matrices with s == 0 at the scheme's final GEMM, those with s == k
@@ -479,10 +522,18 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         const size_t oc = append(fc.second);
         return std::make_pair(Part{of, int(fc.first.size())}, Part{oc, int(fc.second.size())});
     };
-    std::vector<Part> deg_flag(19), sq_flag(max_s + 1);
-    std::vector<std::pair<Part, Part>> deg_parts(19);
-    deg_parts[1] = parts(by_deg[1], 0);
-    for (int d = 2; d <= 18; ++d) deg_flag[d] = flagged(by_deg[d], 0);
+    std::vector<Part> deg_flag(kMaxDeg + 1), sq_flag(max_s + 1);
+    std::vector<std::pair<Part, Part>> deg_parts(kMaxDeg + 1);
+    Part pade_s0{0, 0};  // Pade: s == 0 results are copied out of R after the solve
+    if (!pade) {
+        deg_parts[1] = parts(by_deg[1], 0);
+        for (int d = 2; d <= kMaxDeg; ++d) deg_flag[d] = flagged(by_deg[d], 0);
+    } else if (direct) {
+        std::vector<int32_t> v;
+        for (int32_t m : all_ok)
+            if (h_sel[m].s == 0) v.push_back(m);
+        pade_s0 = Part{append(v), int(v.size())};
+    }
     for (int k = 1; k <= max_s; ++k) {
         std::vector<int32_t> v;
         for (int32_t m : all_ok)
@@ -520,6 +571,98 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     using ET4_2 = std::integral_constant<int, EPI_T4_2>;
     using ET2 = std::integral_constant<int, EPI_T2>;
     (void)EStore{};
+    if (pade) {
+        // eval_pade (pade.cpp:50-113) per order; every order leaves M = V - U
+        // in W2 and R = V + U in W1. Epilogue rows are coefficients of
+        // {I, in0, in1, in2, c}.
+        for (int d = 2; d <= kMaxDeg; d += 2) {
+            const int c = int(by_deg[d].size());
+            if (!c) continue;
+            const int32_t* l = L(off_deg[d]);
+            const int m = d / 2;
+            const double* b = kPadeHost[m - 1];
+            const double mr[2][5] = {{0, 1, 0, 0, -1}, {0, 1, 0, 0, 1}};  // V -/+ c
+            if (d == 2) {
+                pade2_kernel<<<dim3(ew_rows, unsigned(c)), ew_block, 0, st>>>(W[0], W[2], W[1], np, l,
+                                                                              b[0], b[1]);
+                launches->fetch_add(1, std::memory_order_relaxed);
+                continue;
+            }
+            if (d == 4) {  // A2 -> M = b0 I - b1 A + b2 A2, R = b0 I + b1 A + b2 A2
+                const double k[2][5] = {{b[0], -b[1], 0, 0, b[2]}, {b[0], b[1], 0, 0, b[2]}};
+                if ((r = gemm<EPI_PS_B>(W[0], W[0], {W[0], nullptr, nullptr}, {nullptr, W[2], W[1]}, l,
+                                        c, np, st, launches, nullptr, k, -2)))
+                    return r;
+                continue;
+            }
+            if (d == 10) {  // eval_r10
+                if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;
+                // A4 = A2*A2 -> t = b5 A4 + b3 A2 + b1 I (W3), V = b4 A4 + b2 A2 + b0 I (W4)
+                const double k[2][5] = {{b[1], b[3], 0, 0, b[5]}, {b[0], b[2], 0, 0, b[4]}};
+                if ((r = gemm<EPI_PS_B>(W[1], W[1], {W[1], nullptr, nullptr}, {nullptr, W[3], W[4]}, l,
+                                        c, np, st, launches, nullptr, k, -2)))
+                    return r;
+                if ((r = gemm<EPI_PS_B>(W[0], W[3], {W[4], nullptr, nullptr}, {nullptr, W[2], W[1]}, l,
+                                        c, np, st, launches, nullptr, mr, -2)))
+                    return r;
+                continue;
+            }
+            if (d == 26) {  // eval_r26
+                if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;
+                if ((r = gemm<EPI_STORE>(W[1], W[1], {}, {W[2]}, l, c, np, st, launches))) return r;
+                // A6 = A2*A4 (W3), t1 = b13 A6 + b11 A4 + b9 A2 (W4), t2 = b12 A6 + b10 A4 + b8 A2 (W5)
+                const double k6[2][5] = {{0, b[9], b[11], 0, b[13]}, {0, b[8], b[10], 0, b[12]}};
+                if ((r = gemm<EPI_PS_B>(W[1], W[2], {W[1], W[2], nullptr}, {W[3], W[4], W[5]}, l, c,
+                                        np, st, launches, nullptr, k6, 2)))
+                    return r;
+                // V = A6*t2 + b6 A6 + b4 A4 + b2 A2 + b0 I (W6); u = A6*t1 + b7 A6 + ... + b1 I (W7)
+                const double kv[1][5] = {{b[0], b[2], b[4], b[6], 1.0}};
+                const double ku[1][5] = {{b[1], b[3], b[5], b[7], 1.0}};
+                if ((r = gemm<EPI_PS_B>(W[3], W[5], {W[1], W[2], W[3]}, {nullptr, W[6]}, l, c, np, st,
+                                        launches, nullptr, kv, -1)))
+                    return r;
+                if ((r = gemm<EPI_PS_B>(W[3], W[4], {W[1], W[2], W[3]}, {nullptr, W[7]}, l, c, np, st,
+                                        launches, nullptr, ku, -1)))
+                    return r;
+                if ((r = gemm<EPI_PS_B>(W[0], W[7], {W[6], nullptr, nullptr}, {nullptr, W[2], W[1]}, l,
+                                        c, np, st, launches, nullptr, mr, -2)))
+                    return r;
+                continue;
+            }
+            // the even-power chain (pade.cpp:82-110): A2 (W1), odd (W3) =
+            // b1 I + b3 A2 + b5 A4 + ..., V (W4) = b0 I + b2 A2 + ...
+            const int top = m - (m % 2);
+            const double k2[2][5] = {{b[1], 0, 0, 0, m >= 3 ? b[3] : 0.0}, {b[0], 0, 0, 0, b[2]}};
+            if ((r = gemm<EPI_PS_B>(W[0], W[0], {}, {W[1], W[3], W[4]}, l, c, np, st, launches,
+                                    nullptr, k2, 2)))
+                return r;
+            const double* P = W[1];
+            for (int e = 4; e <= top; e += 2) {  // A^e = A2 * A^(e-2)
+                double* Pn = (P == W[2]) ? W[5] : W[2];
+                const double ke[2][5] = {{0, 1, 0, 0, e + 1 <= m ? b[e + 1] : 0.0}, {0, 0, 1, 0, b[e]}};
+                if ((r = gemm<EPI_PS_B>(W[1], P, {W[3], W[4], nullptr}, {Pn, W[3], W[4]}, l, c, np, st,
+                                        launches, nullptr, ke, e < top ? 2 : -2)))
+                    return r;
+                P = Pn;
+            }
+            // U = A * odd -> M (W2), R (W1)
+            if ((r = gemm<EPI_PS_B>(W[0], W[3], {W[4], nullptr, nullptr}, {nullptr, W[2], W[1]}, l, c,
+                                    np, st, launches, nullptr, mr, -2)))
+                return r;
+        }
+        // R <- (V - U)^-1 (V + U) for every OK matrix (pade_solve, pade.cpp:26-28)
+        if (!all_ok.empty()) {
+            r = lu_solve_batched(W[2], W[1], np, batch, L(off_all2), int(all_ok.size()), d_sel, st,
+                                 launches);
+            if (r == MEXP_ERR_CUDA) g_err = lu_last_error();
+            if (r) return r;
+        }
+        if (pade_s0.count) {  // no squarings: e^A = R
+            unpad_kernel<<<dim3(ew_rows, unsigned(pade_s0.count)), ew_block, 0, st>>>(
+                W[1], d_out, n, np, L(pade_s0.off));
+            launches->fetch_add(1, std::memory_order_relaxed);
+        }
+    } else {
     if (int c = int(by_deg[18].size())) {  // T18 (taylor_schemes.cpp:127-141)
         const int32_t* l = L(off_deg[18]);
         if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
@@ -626,6 +769,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
             launches->fetch_add(1, std::memory_order_relaxed);
         }
     }
+    }  // Taylor families
     // squarings: step k maps R -> S (k odd) or S -> R (k even)
     for (int k = 1; k <= max_s; ++k) {
         const double* src = (k & 1) ? R : S;
@@ -656,6 +800,11 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     }
     if (!bad_list.empty()) {
         nan_kernel<<<dim3(64, unsigned(bad_list.size())), 256, 0, st>>>(d_out, n, L(off_bad));
+        launches->fetch_add(1, std::memory_order_relaxed);
+    }
+    if (pade && !all_ok.empty()) {  // "singular denominator" matrices -> NaN
+        nan_singular_kernel<<<dim3(64, unsigned(all_ok.size())), 256, 0, st>>>(d_out, n, L(off_all2),
+                                                                              d_sel);
         launches->fetch_add(1, std::memory_order_relaxed);
     }
     LCUDA(cudaGetLastError());

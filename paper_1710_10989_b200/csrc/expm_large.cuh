@@ -1,6 +1,7 @@
 // Large-n (n > 64) fp64 expm engine: FP64 tensor-core (DMMA) GEMMs with the
-// T18 linear combinations fused into their epilogues, batched over matrices
-// with per-matrix scaling exponents. Implementation: expm_large.cu.
+// schemes' linear combinations fused into their epilogues, batched over
+// matrices with per-matrix scaling exponents; all three families (the Pade
+// solve through lu_batched.cuh). Implementation: expm_large.cu.
 #pragma once
 
 #include <atomic>
@@ -11,8 +12,9 @@
 
 namespace mexp_b200 {
 
+// acc_arg = mexp_accuracy | mexp_family << 4
 int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel, int n,
-                   int64_t batch, int accuracy, cudaStream_t st, std::atomic<uint64_t>* launches);
+                   int64_t batch, int acc_arg, cudaStream_t st, std::atomic<uint64_t>* launches);
 
 // X <- X^(2^s), in place, for `batch` n x n fp64 matrices.
 int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaStream_t st,

@@ -1,0 +1,380 @@
+// Batched LU with partial pivoting and the Pade solve X = (V - U)^-1 (V + U)
+// for the large-n path (n > 64), on all listed matrices at once
+// (reference lu_solve: dense_matrix.cpp:112-118 -> kernels.cpp:55-112).
+//
+// Right-looking blocked LU, panel width NB = 64, per panel:
+//   lu_col_kernel, once per panel column c (+1 finishing step): every CTA
+//     owns 64 rows of the panel; it scales column c-1 by its pivot, applies
+//     that column's rank-1 update to the panel columns right of it, and finds
+//     its rows' largest |M[r][c]|; the matrix's last CTA to finish (atomic
+//     ticket) picks the pivot (largest value, ties to the lower row, NaN
+//     never wins -- the reference's strict '>' scan) and swaps the two rows
+//     across the panel;
+//   laswp_kernel: the panel's row swaps on the columns outside it and on R;
+//   trsm_kernel<lower, unit>: U12 = L11^-1 A12;
+//   gemm_sub_kernel: A22 -= L21 U12 on the FP64 tensor cores (DMMA).
+// Then the solves, blocked the same way: R_j = L_jj^-1 R_j, R_>j -= L_>j,j R_j
+// forward, R_j = U_jj^-1 R_j, R_<j -= U_<j,j R_j backward.
+// Pivot order and multipliers follow the reference; the trailing updates use
+// FMA/DMMA rounding (the large-n path is FAST-only).
+#include <algorithm>
+#include <string>
+
+#include "expm_common.cuh"
+#include "lu_batched.cuh"
+
+namespace mexp_b200 {
+
+namespace {
+
+constexpr int NB = 64;         // panel width
+constexpr int COL_ROWS = 64;   // rows per CTA in the column step
+constexpr int COL_THREADS = 256;
+constexpr int TRSM_THREADS = 128;
+constexpr int GB = 128;        // gemm_sub tile
+constexpr int GLDX = NB + 4;   // X tile row stride (doubles), 4 (mod 16)
+constexpr int GLDY = GB + 4;   // Y tile row stride
+constexpr size_t GEMM_SUB_SMEM = (size_t(GB) * GLDX + size_t(NB) * GLDY) * sizeof(double);
+
+thread_local std::string g_lu_err;
+
+#define LUCUDA(call)                                                             \
+    do {                                                                         \
+        cudaError_t e_ = (call);                                                 \
+        if (e_ != cudaSuccess) {                                                 \
+            g_lu_err = std::string(#call) + ": " + cudaGetErrorString(e_);       \
+            return MEXP_ERR_CUDA;                                                \
+        }                                                                        \
+    } while (0)
+
+__device__ __forceinline__ bool better(double v, int r, double bv, int br) {
+    return v > bv || (v == bv && r < br);  // NaN never wins; ties to the lower row
+}
+
+// Column step c of the panel [c0, c0 + NB). finish = (c == c0 + NB): only the
+// scaling of the panel's last column.
+__global__ void __launch_bounds__(COL_THREADS) lu_col_kernel(
+    double* __restrict__ Mb, int np, const int32_t* __restrict__ list, int c0, int c,
+    double* __restrict__ part_v, int* __restrict__ part_r, unsigned* __restrict__ counter,
+    int* __restrict__ piv, mexp_selection* __restrict__ sel) {
+    const int64_t m = list[blockIdx.y];
+    double* M = Mb + m * int64_t(np) * np;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool upd = c > c0, search = c < c0 + NB;
+    const int jm = c - 1 - c0;  // panel column being eliminated
+    double u0 = 0.0, u1 = 0.0, pv = 1.0;
+    if (upd) {
+        const double* urow = M + int64_t(c - 1) * np + c0;
+        u0 = urow[lane];
+        u1 = urow[32 + lane];
+        pv = M[int64_t(c - 1) * np + (c - 1)];
+    }
+    const int js = c - c0;  // panel column searched
+    double best = -1.0;
+    int brow = np;
+    const int rbeg = c + blockIdx.x * COL_ROWS;
+    for (int i = warp; i < COL_ROWS; i += COL_THREADS / 32) {
+        const int r = rbeg + i;
+        if (r >= np) break;
+        double* row = M + int64_t(r) * np + c0;
+        double v0 = row[lane], v1 = row[32 + lane];
+        if (upd) {
+            const double mine = jm < 32 ? v0 : v1;
+            const double l = __shfl_sync(0xffffffffu, mine, jm & 31) / pv;  // row[k] / piv
+            if (jm < 32) {
+                if (lane == jm) v0 = l;
+                if (lane > jm) v0 = fma(-l, u0, v0);
+                v1 = fma(-l, u1, v1);
+            } else {
+                if (lane == (jm & 31)) v1 = l;
+                if (lane > (jm & 31)) v1 = fma(-l, u1, v1);
+            }
+            row[lane] = v0;
+            row[32 + lane] = v1;
+        }
+        if (search) {
+            const double cv = fabs(__shfl_sync(0xffffffffu, js < 32 ? v0 : v1, js & 31));
+            if (better(cv, r, best, brow)) {
+                best = cv;
+                brow = r;
+            }
+        }
+    }
+    if (!search) return;
+    __shared__ double sb[COL_THREADS / 32];
+    __shared__ int sr[COL_THREADS / 32];
+    __shared__ bool last;
+    if (lane == 0) {
+        sb[warp] = best;
+        sr[warp] = brow;
+    }
+    __syncthreads();
+    const int G = gridDim.x, maxg = np / COL_ROWS;
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < COL_THREADS / 32; ++w)
+            if (better(sb[w], sr[w], best, brow)) {
+                best = sb[w];
+                brow = sr[w];
+            }
+        part_v[m * maxg + blockIdx.x] = best;
+        part_r[m * maxg + blockIdx.x] = brow;
+        __threadfence();
+        last = atomicAdd(counter + m, 1u) == unsigned(G - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __shared__ int sp;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        double bv = -1.0;
+        int br = np;
+        for (int b = 0; b < G; ++b) {
+            const double v = __ldcg(part_v + m * maxg + b);
+            const int r = __ldcg(part_r + m * maxg + b);
+            if (better(v, r, bv, br)) {
+                bv = v;
+                br = r;
+            }
+        }
+        const double dk = fabs(__ldcg(M + int64_t(c) * np + c));
+        int p = br;
+        if (dk != dk) p = c;  // a NaN diagonal: the reference's scan never moves
+        else if (bv == 0.0) {  // "singular denominator" (kernels.cpp:71-72)
+            p = c;
+            sel[m].status = MEXP_ERR_SINGULAR;
+        }
+        piv[m * int64_t(np) + c] = p;
+        counter[m] = 0u;
+        sp = p;
+    }
+    __syncthreads();
+    const int p = sp;
+    if (p != c && threadIdx.x < NB) {  // swap rows c and p across the panel
+        double* rc = M + int64_t(c) * np + c0 + threadIdx.x;
+        double* rp = M + int64_t(p) * np + c0 + threadIdx.x;
+        const double a = __ldcg(rc), b = __ldcg(rp);
+        *rc = b;
+        *rp = a;
+    }
+}
+
+// The panel's row swaps (in order) on M's columns outside [c0, c0 + NB)
+// (blockIdx.z = 0) and on every column of R (blockIdx.z = 1).
+__global__ void laswp_kernel(double* __restrict__ Mb, double* __restrict__ Rb, int np,
+                             const int32_t* __restrict__ list, int c0,
+                             const int* __restrict__ piv) {
+    const int64_t m = list[blockIdx.y];
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= np) return;
+    double* X = (blockIdx.z == 0 ? Mb : Rb) + m * int64_t(np) * np;
+    if (blockIdx.z == 0 && col >= c0 && col < c0 + NB) return;
+    const int* pv = piv + m * int64_t(np);
+    for (int c = c0; c < c0 + NB; ++c) {
+        const int p = pv[c];
+        if (p != c) {
+            const double a = X[int64_t(c) * np + col];
+            X[int64_t(c) * np + col] = X[int64_t(p) * np + col];
+            X[int64_t(p) * np + col] = a;
+        }
+    }
+}
+
+// X[r0 .. r0 + NB) x [cb, cb + ncols) <- T^-1 X with T the NB x NB diagonal
+// block of M at (r0, r0): unit lower (kLower) or upper. One column per thread.
+template <bool kLower>
+__global__ void __launch_bounds__(TRSM_THREADS) trsm_kernel(const double* __restrict__ Mb,
+                                                            double* __restrict__ Xb, int np,
+                                                            const int32_t* __restrict__ list,
+                                                            int r0, int cb, int ncols) {
+    const int64_t m = list[blockIdx.y];
+    const double* M = Mb + m * int64_t(np) * np;
+    double* X = Xb + m * int64_t(np) * np;
+    __shared__ double T[NB][NB + 1];
+    for (int e = threadIdx.x; e < NB * NB; e += TRSM_THREADS)
+        T[e / NB][e % NB] = M[int64_t(r0 + e / NB) * np + r0 + e % NB];
+    __syncthreads();
+    const int col = cb + blockIdx.x * TRSM_THREADS + threadIdx.x;
+    if (col >= cb + ncols) return;
+    double x[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) x[i] = X[int64_t(r0 + i) * np + col];
+    if constexpr (kLower) {
+#pragma unroll
+        for (int i = 1; i < NB; ++i)
+#pragma unroll
+            for (int q = 0; q < i; ++q) x[i] = fma(-T[i][q], x[q], x[i]);
+    } else {
+#pragma unroll
+        for (int i = NB - 1; i >= 0; --i) {
+#pragma unroll
+            for (int q = i + 1; q < NB; ++q) x[i] = fma(-T[i][q], x[q], x[i]);
+            x[i] = x[i] / T[i][i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) X[int64_t(r0 + i) * np + col] = x[i];
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// C[rc .. rc + rows) x [cc .. cc + cols) -= X[rc.., kc .. kc + NB) * Y[kc.., cc..]
+// (all of one matrix, row stride np); 128 x 128 tiles, 8 warps of 64 x 32.
+struct SubArgs {
+    double* C;
+    const double* X;
+    const double* Y;
+    int rc, cc, kc, rows, cols, np;
+    const int32_t* list;
+};
+
+__global__ void __launch_bounds__(256, 1) gemm_sub_kernel(SubArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    double* sx = sm;                 // GB x GLDX
+    double* sy = sm + GB * GLDX;     // NB x GLDY
+    const int64_t m = a.list[blockIdx.z];
+    const int64_t base = m * int64_t(a.np) * a.np;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 2, wn = warp & 3;
+    const int r = lane >> 2, q = lane & 3;
+    const int tr = blockIdx.y * GB, tc = blockIdx.x * GB;  // tile origin within the block
+    for (int e = tid; e < GB * NB / 2; e += 256) {
+        const int i = e / (NB / 2), k = (e % (NB / 2)) * 2;
+        double2 v = make_double2(0.0, 0.0);
+        if (tr + i < a.rows)
+            v = *reinterpret_cast<const double2*>(a.X + base + int64_t(a.rc + tr + i) * a.np + a.kc + k);
+        *reinterpret_cast<double2*>(sx + i * GLDX + k) = v;
+    }
+    for (int e = tid; e < NB * GB / 2; e += 256) {
+        const int k = e / (GB / 2), j = (e % (GB / 2)) * 2;
+        double2 v = make_double2(0.0, 0.0);
+        if (tc + j < a.cols)
+            v = *reinterpret_cast<const double2*>(a.Y + base + int64_t(a.kc + k) * a.np + a.cc + tc + j);
+        *reinterpret_cast<double2*>(sy + k * GLDY + j) = v;
+    }
+    __syncthreads();
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const double* px = sx + (wm * 64 + r) * GLDX + q;
+    const double* py = sy + q * GLDY + wn * 32 + r;
+#pragma unroll 2
+    for (int k = 0; k < NB; k += 4) {
+        double af[8], bf[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) af[i] = px[i * 8 * GLDX + k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = py[k * GLDY + j * 8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = tr + wm * 64 + i * 8 + r;
+        if (row >= a.rows) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = tc + wn * 32 + j * 8 + 2 * q;
+            if (col >= a.cols) continue;
+            double2* p = reinterpret_cast<double2*>(a.C + base + int64_t(a.rc + row) * a.np + a.cc + col);
+            double2 v = *p;
+            v.x -= acc[i][j][0];
+            v.y -= acc[i][j][1];
+            *p = v;
+        }
+    }
+}
+
+int sub(double* C, const double* X, const double* Y, int rc, int cc, int kc, int rows, int cols,
+        int np, const int32_t* list, int count, cudaStream_t st, std::atomic<uint64_t>* launches) {
+    if (rows <= 0 || cols <= 0 || count == 0) return MEXP_OK;
+    static bool attr = [] {
+        cudaFuncSetAttribute(gemm_sub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(GEMM_SUB_SMEM));
+        return true;
+    }();
+    (void)attr;
+    SubArgs a{C, X, Y, rc, cc, kc, rows, cols, np, list};
+    for (int z0 = 0; z0 < count; z0 += 65535) {
+        a.list = list + z0;
+        const dim3 grid((cols + GB - 1) / GB, (rows + GB - 1) / GB, std::min(count - z0, 65535));
+        gemm_sub_kernel<<<grid, 256, GEMM_SUB_SMEM, st>>>(a);
+        launches->fetch_add(1, std::memory_order_relaxed);
+    }
+    return MEXP_OK;
+}
+
+template <bool kLower>
+int trsm(const double* M, double* X, int np, const int32_t* list, int count, int r0, int cb,
+         int ncols, cudaStream_t st, std::atomic<uint64_t>* launches) {
+    if (ncols <= 0) return MEXP_OK;
+    for (int z0 = 0; z0 < count; z0 += 65535) {
+        const dim3 grid((ncols + TRSM_THREADS - 1) / TRSM_THREADS, std::min(count - z0, 65535));
+        trsm_kernel<kLower><<<grid, TRSM_THREADS, 0, st>>>(M, X, np, list + z0, r0, cb, ncols);
+        launches->fetch_add(1, std::memory_order_relaxed);
+    }
+    return MEXP_OK;
+}
+
+}  // namespace
+
+const char* lu_last_error() { return g_lu_err.c_str(); }
+
+int lu_solve_batched(double* M, double* R, int np, int64_t batch, const int32_t* d_list, int count,
+                     mexp_selection* d_sel, cudaStream_t st, std::atomic<uint64_t>* launches) {
+    if (count == 0) return MEXP_OK;
+    if (np % NB != 0 || count > 65535) return MEXP_ERR_UNSUPPORTED;
+    const int maxg = np / COL_ROWS;
+    // scratch: pivots (batch x np), per-CTA partial maxima, per-matrix tickets
+    const size_t piv_b = sizeof(int) * size_t(batch) * np;
+    const size_t pv_b = sizeof(double) * size_t(batch) * maxg;
+    const size_t pr_b = sizeof(int) * size_t(batch) * maxg;
+    const size_t ct_b = sizeof(unsigned) * size_t(batch);
+    char* scratch = nullptr;
+    LUCUDA(cudaMallocAsync(&scratch, piv_b + pv_b + pr_b + ct_b + 64, st));
+    double* part_v = reinterpret_cast<double*>(scratch);
+    int* piv = reinterpret_cast<int*>(scratch + pv_b);
+    int* part_r = reinterpret_cast<int*>(scratch + pv_b + piv_b);
+    unsigned* counter = reinterpret_cast<unsigned*>(scratch + pv_b + piv_b + pr_b);
+    LUCUDA(cudaMemsetAsync(counter, 0, ct_b, st));
+    int r;
+    for (int c0 = 0; c0 < np; c0 += NB) {
+        for (int c = c0; c <= c0 + NB; ++c) {
+            if (c >= np) break;
+            const dim3 grid((np - c + COL_ROWS - 1) / COL_ROWS, count);
+            lu_col_kernel<<<grid, COL_THREADS, 0, st>>>(M, np, d_list, c0, c, part_v, part_r,
+                                                         counter, piv, d_sel);
+            launches->fetch_add(1, std::memory_order_relaxed);
+        }
+        laswp_kernel<<<dim3((np + 255) / 256, count, 2), 256, 0, st>>>(M, R, np, d_list, c0, piv);
+        launches->fetch_add(1, std::memory_order_relaxed);
+        const int rest = np - c0 - NB;
+        if (rest > 0) {
+            if ((r = trsm<true>(M, M, np, d_list, count, c0, c0 + NB, rest, st, launches))) return r;
+            if ((r = sub(M, M, M, c0 + NB, c0 + NB, c0, rest, rest, np, d_list, count, st, launches)))
+                return r;
+        }
+    }
+    // forward: L Y = P R
+    for (int j = 0; j < np; j += NB) {
+        if ((r = trsm<true>(M, R, np, d_list, count, j, 0, np, st, launches))) return r;
+        if ((r = sub(R, M, R, j + NB, 0, j, np - j - NB, np, np, d_list, count, st, launches))) return r;
+    }
+    // backward: U X = Y
+    for (int j = np - NB; j >= 0; j -= NB) {
+        if ((r = trsm<false>(M, R, np, d_list, count, j, 0, np, st, launches))) return r;
+        if ((r = sub(R, M, R, 0, 0, j, j, np, np, d_list, count, st, launches))) return r;
+    }
+    LUCUDA(cudaGetLastError());
+    LUCUDA(cudaFreeAsync(scratch, st));
+    return MEXP_OK;
+}
+
+}  // namespace mexp_b200

@@ -125,8 +125,9 @@ static void device_cases() {
     CHECK(rpd.degree == 22 && rpd.s == 0 && rpd.cost_thirds == 22);
     CHECK(norm1(DenseMatrix::from_rows({{rpd.result.at(0, 0) + 1, rpd.result.at(0, 1)},
                                         {rpd.result.at(1, 0), rpd.result.at(1, 1) + 1}})) <= 1e-12);
-    // Pade beyond n = 64 is not built
-    CHECK(throws<std::invalid_argument>([] { expm(DenseMatrix(65), Accuracy::Double, Family::PadeDiagonal); }));
+    // Pade beyond n = 64: the DMMA GEMM chain + batched blocked LU
+    const auto pz = expm(DenseMatrix(65), Accuracy::Double, Family::PadeDiagonal);
+    CHECK(pz.result == DenseMatrix::identity(65) && pz.degree == 2 && pz.s == 0);
     // Paterson-Stockmeyer family: rotation by pi -> m = 16, s = 3, 6 + 3 products
     const auto rps = expm(DenseMatrix::from_rows({{0, pi}, {-pi, 0}}), Accuracy::Double,
                           Family::TaylorPS);

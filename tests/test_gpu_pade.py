@@ -80,10 +80,48 @@ def test_pade_drop_in_and_limits(cuda):
     assert (r.degree, r.s, r.cost_thirds) == (22, 0, 22)
     assert np.abs(r.result + np.eye(2)).max() < 1e-12
     a = np.zeros((2, 65, 65))
-    with pytest.raises(ValueError, match="unsupported"):
-        mx.expm_batched_host(a, family=PADE)
+    out, sel, st = mx.expm_batched_host(a, family=PADE)
+    assert st == mx.OK and np.array_equal(out, np.broadcast_to(np.eye(65), out.shape))
     b = np.zeros((3, 8, 8))
     b[1, 2, 2] = np.nan
     out, sel, st = mx.expm_batched_host(b, family=PADE, raise_on_error=False)
     assert st == mx.ERR_NONFINITE and list(sel["status"]) == [0, 1, 0]
     assert np.array_equal(out[0], np.eye(8))
+
+
+@pytest.mark.parametrize("n", [96, 128, 200])
+def test_pade_large_n_every_order(cuda, oracle, n):
+    """n > 64: U, V on the DMMA GEMM chain with fused lincombs, M = V - U and
+    R = V + U from the last epilogue, the batched blocked LU (lu_batched.cu),
+    then the squarings; within 50 n u of the reference."""
+    rng = np.random.default_rng(3000 + n)
+    theta = [3.65e-8, 5.32e-4, 1.50e-2, 8.54e-2, 2.54e-1, 5.41e-1, 9.50e-1, 1.47, 2.10, 2.81,
+             3.60, 4.46, 5.37]
+    norms = np.array([0.9 * t for t in theta] + [20.0, 300.0])
+    a = rng.uniform(-1, 1, (len(norms), n, n))
+    a *= (norms / workloads.one_norm_batched(a))[:, None, None]
+    ref = oracle.expm_batch(a, family=int(PADE))
+    assert set(ref.degree) == set(range(2, 27, 2))
+    out, sel, st = mx.expm_batched_host(a, family=PADE)
+    assert st == mx.OK
+    assert np.array_equal(sel["degree"], ref.degree) and np.array_equal(sel["s"], ref.s)
+    assert np.array_equal(sel["norm_in"], ref.norm_in)
+    err = rel_fro(out, ref.out)
+    assert err.max() <= 50 * n * U53, err
+
+
+def test_pade_large_n_pivoting(cuda, oracle):
+    """A matrix whose Pade denominator needs row exchanges at every step of
+    the blocked LU (a permutation-like dominant part) still matches."""
+    n = 150
+    rng = np.random.default_rng(77)
+    perm = rng.permutation(n)
+    a = np.zeros((2, n, n))
+    a[0][np.arange(n), perm] = 1.0
+    a[0] += 0.01 * rng.standard_normal((n, n))
+    a[0] *= 4.0 / workloads.one_norm_batched(a[:1])[0]
+    a[1] = rng.standard_normal((n, n)) * 0.02
+    ref = oracle.expm_batch(a, family=int(PADE))
+    out, sel, st = mx.expm_batched_host(a, family=PADE)
+    assert st == mx.OK and np.array_equal(sel["s"], ref.s)
+    assert rel_fro(out, ref.out).max() <= 50 * n * U53

@@ -362,8 +362,8 @@ def test_pade_coefficients(oracle, golden):
     for m in range(1, 14):
         assert np.array_equal(oracle.pade_coeffs(m).view(np.uint64), g[m - 1, :m + 1].view(np.uint64))
     src = open(os.path.join(ROOT, "paper_1710_10989_b200", "csrc", "expm_common.cuh")).read()
-    body = src[src.index("constexpr double c_pade[13][14]"):]
-    body = body[body.index("{") + 1:body.index("};")]
+    body = src[src.index("#define MEXP_PADE_TABLE"):]
+    body = body[body.index("{") + 1:body.index("c_pade[13][14]")]
     vals = [float.fromhex(t) if "0x" in t else float(t)
             for t in re.findall(r"0x[0-9a-fA-Fp.+-]+|\d+\.\d+", body)]
     dev = np.array(vals).reshape(13, 14)
