@@ -14,7 +14,7 @@ OBJDIR   := build/obj
 OBJS := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(CU_SRCS)) \
         $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.cpp.o,$(CXX_SRCS))
 
-all: $(LIB) oracle tests/cpp/dropin_kats bin/mexp
+all: $(LIB) oracle tests/cpp/dropin_kats tests/cpp/gallery_dump bin/mexp
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -22,7 +22,7 @@ $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 
 $(OBJDIR)/%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS)
 	@mkdir -p $(OBJDIR)
-	g++ -O2 -std=c++20 -fPIC -Iinclude -I/usr/local/cuda/include -c $< -o $@
+	g++ -O2 -std=c++20 -ffp-contract=off -fPIC -Iinclude -I/usr/local/cuda/include -c $< -o $@
 
 $(LIB): $(OBJS)
 	@mkdir -p $(PKG)/_lib
@@ -37,6 +37,9 @@ clean:
 .PHONY: all oracle clean
 
 tests/cpp/dropin_kats: tests/cpp/dropin_kats.cpp $(LIB) $(wildcard include/mexp/*.hpp)
+	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/_lib -lmexp_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/_lib'
+
+tests/cpp/gallery_dump: tests/cpp/gallery_dump.cpp $(LIB) $(wildcard include/mexp/*.hpp)
 	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/_lib -lmexp_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/_lib'
 
 bin/mexp: tools/cli/mexp_cli.cpp $(LIB) $(wildcard include/mexp/*.hpp)

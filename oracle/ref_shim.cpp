@@ -11,11 +11,16 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <random>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
+#include "mexp/bench.hpp"
 #include "mexp/dense_matrix.hpp"
+#include "mexp/gallery.hpp"
 #include "mexp/expm.hpp"
 #include "mexp/kernels.hpp"
 #include "mexp/pade.hpp"
@@ -197,6 +202,64 @@ int ref_eval_pade(const double* a, int n, int order, double* out) {
         return -1;
     } catch (const std::runtime_error&) {
         return -2;
+    }
+}
+
+// gallery (src/gallery.cpp): kind index into kAllGalleryKinds. Returns 0, or
+// 1 when the reference throws (zero matrix / bad arguments).
+int ref_gallery(int kind, int n, uint64_t seed, double target_norm, double* out) {
+    try {
+        mexp::GallerySpec spec{mexp::kAllGalleryKinds[kind], n, seed, target_norm};
+        const auto m = mexp::gallery(spec);
+        std::memcpy(out, m.data(), sizeof(double) * std::size_t(n) * n);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+// reference_expm (src/bench.cpp:10-20)
+void ref_reference_expm(const double* a, int n, double* out) {
+    const auto r = mexp::reference_expm(to_dense(a, n));
+    std::memcpy(out, r.data(), sizeof(double) * std::size_t(n) * n);
+}
+
+// cost_staircase + staircase_csv over log_grid (bench.cpp:32-57, 123-136):
+// writes the CSV text (NUL-terminated, truncated to cap) and returns its length
+int ref_staircase_csv(int family, int accuracy, double lo, double hi, int points, char* buf,
+                      int cap) {
+    const std::string csv = mexp::staircase_csv(
+        mexp::cost_staircase(fam_of(family), acc_of(accuracy), mexp::log_grid(lo, hi, points)));
+    std::snprintf(buf, std::size_t(cap), "%s", csv.c_str());
+    return int(csv.size());
+}
+
+// The `sweep` subcommand of the reference CLI (tools/mexp_cli.cpp:122-161),
+// whose own build needs the absent CLI11: the same spec derivation from the
+// base seed, then error_sweep + sweep_csv. kinds / families are index lists.
+int ref_sweep_csv(const int* kinds, int nk, const int* families, int nf, int n, int count,
+                  uint64_t seed, int accuracy, double lo, double hi, char* buf, int cap) {
+    std::vector<mexp::Family> fams;
+    for (int i = 0; i < nf; ++i) fams.push_back(fam_of(families[i]));
+    std::mt19937_64 rng(seed ^ 0xda3e39cb94b95bdbULL);
+    std::vector<mexp::GallerySpec> specs;
+    const double llo = std::log(lo), lhi = std::log(hi);
+    for (int i = 0; i < count; ++i) {
+        mexp::GallerySpec spec;
+        spec.kind = mexp::kAllGalleryKinds[kinds[i % nk]];
+        spec.n = n;
+        spec.seed = seed * 1000003ULL + std::uint64_t(i);
+        const double f = 0.5 * (mexp::uniform_pm1(rng) + 1.0);
+        spec.target_norm = std::exp(llo + f * (lhi - llo));
+        specs.push_back(spec);
+    }
+    try {
+        const std::string csv = mexp::sweep_csv(mexp::error_sweep(specs, fams, acc_of(accuracy)));
+        std::snprintf(buf, std::size_t(cap), "%s", csv.c_str());
+        return int(csv.size());
+    } catch (const std::exception& e) {
+        std::snprintf(buf, std::size_t(cap), "error: %s", e.what());
+        return -1;
     }
 }
 

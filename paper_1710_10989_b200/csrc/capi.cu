@@ -55,6 +55,10 @@ bool valid_args(int dtype, int n, int64_t batch, int accuracy, int family, int r
 
 // the kernels' `acc_arg`: accuracy in the low nibble, family above it
 int acc_arg(int accuracy, int family) { return accuracy | (family << 4); }
+// Pade evaluation: the public family, or reference_expm's internal one
+bool is_pade(int aarg) {
+    return (aarg >> 4) == MEXP_FAMILY_PADE || (aarg >> 4) == kFamilyPadeReference;
+}
 
 // Rounding threshold of the AUTO policy: matrices with s >= this run the
 // reference-exact arithmetic. Each squaring roughly doubles the relative
@@ -237,7 +241,7 @@ int launch_small_family(const double* a, double* out, mexp_selection* sel, int64
     if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)
         return launch_small_f64<N, GPC, MEXP_FAMILY_TAYLOR_PS>(a, out, sel, batch, accuracy,
                                                                rounding, smin, st);
-    if ((accuracy >> 4) == MEXP_FAMILY_PADE)
+    if (is_pade(accuracy))
         return launch_small_f64<N, GPC, MEXP_FAMILY_PADE>(a, out, sel, batch, accuracy, rounding,
                                                           smin, st);
     return launch_small_f64<N, GPC, MEXP_FAMILY_TAYLOR_NEW>(a, out, sel, batch, accuracy, rounding,
@@ -247,7 +251,7 @@ int launch_small_family(const double* a, double* out, mexp_selection* sel, int64
 int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
                   int accuracy, int rounding, int smin, cudaStream_t st) {
     if (batch == 0) return MEXP_OK;
-    if ((accuracy >> 4) == MEXP_FAMILY_PADE)  // the generic engine (its LU solve)
+    if (is_pade(accuracy))  // the generic engine (its LU solve)
         return launch_small_f64<8, 8, MEXP_FAMILY_PADE>(a, out, sel, batch, accuracy, rounding,
                                                        smin, st);
     if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)  // the default variant only
@@ -288,7 +292,7 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
         return r;
     }
     const int np = padded_n(n);
-    if (dtype == MEXP_F32 && (accuracy >> 4) == MEXP_FAMILY_PADE) {
+    if (dtype == MEXP_F32 && is_pade(accuracy)) {
         // fp32 storage, fp64 evaluation: the LU solve of a Pade denominator
         // amplifies fp32 rounding by cond(V - U), which reaches ~1e3 at the
         // Single table's thetas (up to 11.2), so the fp32 Pade path widens to
@@ -402,6 +406,9 @@ int ensure_pipe(HostPipe& p, size_t bytes, int64_t sels) {
     return MEXP_OK;
 }
 
+int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch, int aarg,
+                   int rounding, mexp_selection* h_sel, int64_t* first_error);
+
 }  // namespace
 
 extern "C" {
@@ -481,6 +488,17 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
                            int accuracy, int family, int rounding, mexp_selection* h_sel,
                            int64_t* first_error) {
     if (!valid_args(dtype, n, batch, accuracy, family, rounding)) return MEXP_ERR_INVALID_ARGUMENT;
+    return expm_host_impl(h_a, h_out, dtype, n, batch, acc_arg(accuracy, family), rounding, h_sel,
+                          first_error);
+}
+
+}  // extern "C"
+
+namespace {
+// The host pipeline behind mexp_expm_batched_host; `aarg` is the kernels'
+// acc_arg (accuracy | family << 4, family 3 = reference_expm's selection).
+int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch, int aarg,
+                   int rounding, mexp_selection* h_sel, int64_t* first_error) {
     if (first_error) *first_error = -1;
     if (batch == 0) return MEXP_OK;
     if (!h_a || !h_out) return MEXP_ERR_INVALID_ARGUMENT;
@@ -577,8 +595,7 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
         cudaStream_t st = p.st[k];
         if (!prefetch && (r = h2d(c)) != MEXP_OK) return r;
         if (prefetch && c + 1 < nchunks && (r = h2d(c + 1)) != MEXP_OK) return r;
-        r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, acc_arg(accuracy, family), rounding,
-                        p.d_sel[k], st);
+        r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, aarg, rounding, p.d_sel[k], st);
         if (r != MEXP_OK) return r;
         MEXP_CUDA(cudaMemcpyAsync(dst + b0 * mat_bytes, p.d_out[k], nb * mat_bytes,
                                   cudaMemcpyDeviceToHost, st));
@@ -605,6 +622,10 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
     return first_status;
 }
 
+}  // namespace
+
+extern "C" {
+
 int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
               mexp_report* report) {
     mexp_selection sel{};
@@ -620,6 +641,18 @@ int mexp_expm(const double* a, int n, int accuracy, int family, double* result,
         report->norm_in = sel.norm_in;
     }
     return MEXP_OK;
+}
+
+// library-internal helper for the C++ drop-in mexp::reference_expm (bench_api.cpp):
+// Pade r26 with s = the least s such that ||2^-s A||_1 <= theta_26 / 8
+// (bench.cpp:10-20), batched over host matrices
+int mexp_b200_reference_expm_host(const double* a, double* out, int n, int64_t batch,
+                                  int rounding, mexp_selection* sel) {
+    if (n < 1 || batch < 0 || rounding < 0 || rounding > 2) return MEXP_ERR_INVALID_ARGUMENT;
+    const int dv = device_ok();
+    if (dv != MEXP_OK) return dv;
+    return expm_host_impl(a, out, MEXP_F64, n, batch,
+                          acc_arg(MEXP_ACCURACY_DOUBLE, kFamilyPadeReference), rounding, sel, nullptr);
 }
 
 // library-internal helper for the C++ drop-in mexp::squarings (dropin.cpp)

@@ -210,11 +210,26 @@ __host__ __device__ __forceinline__ double theta_entry(int family, int accuracy,
     }
 }
 
+// Internal family id (never in the public ABI): Pade evaluation with the
+// selection of reference_expm (bench.cpp:10-20) -- degree 26 and the least s
+// with ldexp(norm, -s) <= theta_26(Double) / 8.
+constexpr int kFamilyPadeReference = 3;
+
 __host__ __device__ __forceinline__ Sel select_device(double norm, int accuracy,
                                                       int family = MEXP_FAMILY_TAYLOR_NEW) {
     Sel r{0, 0, MEXP_OK};
     if (!isfinite(norm) || norm < 0.0) {
         r.status = MEXP_ERR_NORM_NONFINITE;
+        return r;
+    }
+    if (family == kFamilyPadeReference) {
+        const double t = pade_theta(1, kPadeEntries - 1) / 8.0;  // exact: a power-of-two divide
+        r.degree = 26;
+        if (norm > t) {
+            const long long nb = dbits(norm), tb = dbits(t);
+            const long long k = (nb >> 52) - (tb >> 52);
+            r.s = int(k) + int(norm > dfrom(tb + (k << 52)));
+        }
         return r;
     }
     if (family == MEXP_FAMILY_PADE) {

@@ -432,7 +432,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
                    int64_t batch, int acc_arg, cudaStream_t st, std::atomic<uint64_t>* launches) {
     const int np = (n + BM - 1) / BM * BM;
     const int64_t mat = int64_t(np) * np;
-    const bool pade = (acc_arg >> 4) == MEXP_FAMILY_PADE;
+    const bool pade = (acc_arg >> 4) == MEXP_FAMILY_PADE || (acc_arg >> 4) == kFamilyPadeReference;
     constexpr int kMaxBuffers = 8;
     const int kBuffers = pade ? 8 : 6;  // r26 keeps A, A2, A4, A6, two lincombs, V and u''
     // workspace: kBuffers padded matrices per batch entry + per-matrix scratch

@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(32 * TileShape<N>::W * GPC, TileShape<N>::MIN_
         if (!allfin) {
             sl.status = MEXP_ERR_NONFINITE;
         } else {
-            sl = select_device(norm, accuracy, family);
+            sl = select_device(norm, accuracy, acc_arg >> 4);  // (family 3: reference_expm)
         }
         if (sel && g.tid == 0) {
             mexp_selection r;
