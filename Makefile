@@ -7,7 +7,7 @@ CU_SRCS  := $(wildcard $(PKG)/csrc/*.cu)
 CXX_SRCS := $(wildcard $(PKG)/csrc/*.cpp)
 HDRS     := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard include/*.h) $(wildcard include/mexp/*.hpp)
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v \
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v $(EXTRA_NVFLAGS) \
             --expt-relaxed-constexpr
 OBJDIR   := build/obj
 

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "expm_cluster.cuh"
 #include "expm_common.cuh"
 #include "expm_large.cuh"
 #include "expm_n8.cuh"
@@ -234,6 +235,34 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
     return MEXP_OK;
 }
 
+// Few matrices of np = 64 (cfg1: one): a 4-CTA cluster per matrix instead of
+// one CTA (expm_cluster.cuh). Used while the clusters fit in about two waves
+// of the SMs; MEXP_CLUSTER_MAX overrides the batch limit (0 disables).
+int64_t cluster_max_batch() {
+    static int64_t v = [] {
+        const char* e = std::getenv("MEXP_CLUSTER_MAX");
+        return e ? int64_t(std::atoll(e)) : int64_t(2 * num_sms() / kClusterCtas);
+    }();
+    return v;
+}
+
+int launch_cluster64(const double* a, double* out, mexp_selection* sel, int64_t batch, int accuracy,
+                     int rounding, int smin, cudaStream_t st) {
+    using G = ClusterGroup64;
+    const size_t smem = size_t(G::SMEM_DOUBLES) * sizeof(double);
+    static bool attr = [&] {
+        cudaFuncSetAttribute(expm64_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+        return true;
+    }();
+    (void)attr;
+    const int grid = int(batch) * kClusterCtas;
+    expm64_cluster_kernel<<<grid, G::THREADS, smem, st>>>(a, out, sel, batch, accuracy, rounding, smin);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    MEXP_CUDA(cudaGetLastError());
+    return MEXP_OK;
+}
+
 // `accuracy` here and below is the kernels' acc_arg (mexp_accuracy | family << 4)
 template <int N, int GPC>
 int launch_small_family(const double* a, double* out, mexp_selection* sel, int64_t batch,
@@ -273,7 +302,10 @@ int run_small_f64(const double* a, double* out, mexp_selection* sel, int np, int
         case 8: return launch_n8_f64(a, out, sel, batch, accuracy, rounding, smin, st);
         case 16: return launch_small_family<16, 4>(a, out, sel, batch, accuracy, rounding, smin, st);
         case 32: return launch_small_family<32, 2>(a, out, sel, batch, accuracy, rounding, smin, st);
-        case 64: return launch_small_family<64, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 64:
+            if (!is_pade(accuracy) && batch <= cluster_max_batch())
+                return launch_cluster64(a, out, sel, batch, accuracy, rounding, smin, st);
+            return launch_small_family<64, 1>(a, out, sel, batch, accuracy, rounding, smin, st);
     }
     return MEXP_ERR_UNSUPPORTED;
 }

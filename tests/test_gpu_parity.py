@@ -237,3 +237,40 @@ def test_fp32_non_finite(cuda):
     out, sel, st = mx.expm_batched_host(a, accuracy=mx.Accuracy.Single, raise_on_error=False)
     assert st == mx.ERR_NONFINITE and list(sel["status"]) == [0, 1, 0]
     assert np.array_equal(out[0], np.eye(32, dtype=np.float32))
+
+
+@pytest.mark.parametrize("mode", ["reference", "auto", "fast"])
+def test_cfg1_cluster_path(cuda, oracle, mode):
+    """cfg1 (one 64x64 matrix) runs on the 4-CTA cluster kernel
+    (expm_cluster.cuh): REFERENCE bit-identical, AUTO/FAST within 50 n u."""
+    a = workloads.generate("cfg1", 0, 1)
+    ref = oracle.expm_batch(a)
+    out, sel, st = mx.expm_batched_host(a, rounding=MODES[mode])
+    assert st == mx.OK and (sel["degree"][0], sel["s"][0]) == (ref.degree[0], ref.s[0])
+    if mode == "reference":
+        assert np.array_equal(bits(out), bits(ref.out))
+    else:
+        assert rel_fro(out, ref.out).max() <= 50 * 64 * U53
+
+
+@pytest.mark.parametrize("batch", [3, 74, 75, 150])
+def test_cluster_and_cta_paths_agree(cuda, oracle, batch):
+    """np = 64 batches up to 2 * SMs / 4 use the cluster kernel, larger ones
+    the one-CTA kernel; both match the reference bit for bit in REFERENCE
+    rounding, across every degree and s, with n = 50 padded to 64."""
+    rng = np.random.default_rng(batch)
+    norms = 10.0 ** rng.uniform(-17, 2.5, batch)
+    a = rng.standard_normal((batch, 50, 50))
+    a *= (norms / workloads.one_norm_batched(a))[:, None, None]
+    a[batch // 2, 3, 4] = np.inf
+    ref = oracle.expm_batch(a)
+    out, sel, st = mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE, raise_on_error=False)
+    assert st == mx.ERR_NONFINITE and sel["status"][batch // 2] == mx.ERR_NONFINITE
+    ok = sel["status"] == 0
+    assert np.array_equal(sel["degree"][ok], ref.degree[ok]) and np.array_equal(sel["s"][ok], ref.s[ok])
+    assert np.array_equal(bits(out[ok]), bits(ref.out[ok]))
+    assert np.isnan(out[batch // 2]).all()
+    out_ps, sel_ps, _ = mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE, family=mx.Family.TaylorPS,
+                                             raise_on_error=False)
+    ref_ps = oracle.expm_batch(a, family=1)
+    assert np.array_equal(bits(out_ps[ok]), bits(ref_ps.out[ok]))
