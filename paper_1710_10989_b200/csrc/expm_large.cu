@@ -34,6 +34,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "expm_common.cuh"
 #include "expm_large.cuh"
 #include "lu_batched.cuh"
@@ -56,13 +59,29 @@ thread_local std::string g_err;
 #ifndef MEXP_GEMM_BK
 #define MEXP_GEMM_BK 32
 #endif
+// 0: cp.async (LDGSTS) for both operands; 1: row-wise cp.async.bulk for both;
+// 2: X tiles by tensor-map TMA (cp.async.bulk.tensor, 128B swizzle), Y rows
+// by cp.async.bulk (measured: profiles/gemm_tma_r1.txt)
+#ifndef MEXP_GEMM_TMA
+#define MEXP_GEMM_TMA 2
+#endif
 constexpr int BM = 128, BN = 128, BK = MEXP_GEMM_BK, STAGES = BK == 16 ? 4 : 3;
 constexpr int LDA = BK + 4;   // 20 doubles: 4 (mod 16)
 constexpr int LDB = BN + 4;   // 132 doubles: 4 (mod 16)
 constexpr int WM = 64, WN = 32, TM = WM / 8, TN = WN / 8;
 constexpr int GEMM_THREADS = 256;
-constexpr size_t STAGE_DOUBLES = size_t(BM) * LDA + size_t(BK) * LDB;
-constexpr size_t GEMM_SMEM = STAGES * STAGE_DOUBLES * sizeof(double);
+#if MEXP_GEMM_TMA == 2
+// X stage: BK / 16 boxes of 128 rows x 16 doubles (128 B), TMA's 128B swizzle
+// (16-byte chunk c of row r at c ^ (r & 7)): conflict-free fragment loads
+constexpr int XBOX = 16;
+constexpr size_t A_DOUBLES = size_t(BM) * BK;
+static_assert(BK % XBOX == 0 && (BM * XBOX * 8) % 1024 == 0, "swizzled boxes stay 1024 B aligned");
+#else
+constexpr size_t A_DOUBLES = size_t(BM) * LDA;
+#endif
+constexpr size_t STAGE_DOUBLES = A_DOUBLES + size_t(BK) * LDB;
+// + the stages' mbarriers and slack to align the ring to 1024 B
+constexpr size_t GEMM_SMEM = STAGES * STAGE_DOUBLES * sizeof(double) + 64 + 1024;
 
 // Epilogues. c = the product's value at (i, j); id = (i == j); in/out are
 // the step's extra matrices at the same position.
@@ -106,6 +125,45 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 template <int EPI>
@@ -183,8 +241,11 @@ __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, i
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_dmma_kernel(GemmArgs g) {
-    extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_dmma_kernel(GemmArgs g, const __grid_constant__ CUtensorMap tmx) {
+    extern __shared__ __align__(16) double smem_raw[];
+    double* const smem = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 2, wn = warp & 3;
     const int r = lane >> 2, q = lane & 3;
@@ -198,7 +259,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_dmma_kernel(GemmArgs g) 
     const int ktiles = g.np / BK;
 
     auto stage_a = [&](int s) { return smem + s * STAGE_DOUBLES; };
-    auto stage_b = [&](int s) { return smem + s * STAGE_DOUBLES + BM * LDA; };
+    auto stage_b = [&](int s) { return smem + s * STAGE_DOUBLES + A_DOUBLES; };
     auto load = [&](int s, int kt) {
         double* sa = stage_a(s);
         double* sb = stage_b(s);
@@ -221,24 +282,79 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_dmma_kernel(GemmArgs g) 
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+#if MEXP_GEMM_TMA
+    // warp 0 streams each stage through the TMA engine (see MEXP_GEMM_TMA);
+    // the stage's mbarrier completes on the bytes
+    uint64_t* const full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_DOUBLES);
+    constexpr unsigned kStageBytes = (BM * BK + BK * BN) * sizeof(double);
+    (void)load;
+    (void)tmx;
+    if (tid == 0) {
+        for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int st, int kt) {
+        if (warp != 0) return;
+        if (lane == 0) mbar_expect_tx(&full[st], kStageBytes);
+        __syncwarp();
+        double* sa = stage_a(st);
+        double* sb = stage_b(st);
+        const int k0 = kt * BK;
+#if MEXP_GEMM_TMA == 2
+        if (lane == 0)
+#pragma unroll
+            for (int b = 0; b < BK / XBOX; ++b)
+                tma_load_3d(sa + b * BM * XBOX, &tmx, k0 + b * XBOX, m0, int(mat), &full[st]);
+#else
+        for (int row = lane; row < BM; row += 32)
+            bulk_g2s(sa + row * LDA, X + int64_t(m0 + row) * g.np + k0, BK * sizeof(double), &full[st]);
+#endif
+        for (int row = lane; row < BK; row += 32)
+            bulk_g2s(sb + row * LDB, Y + int64_t(k0 + row) * g.np + n0, BN * sizeof(double), &full[st]);
+    };
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st)
+        if (st < ktiles) issue(st, st);
+#else
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < ktiles) load(s, s);
         cp_commit();
     }
+#endif
     for (int kt = 0; kt < ktiles; ++kt) {
+#if MEXP_GEMM_TMA
+        __syncthreads();  // every warp is done with the stage about to be refilled
+        const int nk = kt + STAGES - 1;
+        if (nk < ktiles) issue(nk % STAGES, nk);
+        mbar_wait(&full[kt % STAGES], unsigned(kt / STAGES) & 1u);
+#else
         cp_wait<STAGES - 2>();
         __syncthreads();
         const int nk = kt + STAGES - 1;
         if (nk < ktiles) load(nk % STAGES, nk);
         cp_commit();
+#endif
+#if MEXP_GEMM_TMA == 2
+        // row = wm*64 + 8i + r, so row & 7 = r; k = kk + q lies in box kk / 16
+        const double* sa = stage_a(kt % STAGES) + (wm * WM + r) * XBOX + (q & 1);
+#else
         const double* sa = stage_a(kt % STAGES) + (wm * WM + r) * LDA + q;
+#endif
         const double* sb = stage_b(kt % STAGES) + q * LDB + wn * WN + r;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
             double af[TM], bf[TN];
+#if MEXP_GEMM_TMA == 2
+            const int chunk = (((kk % XBOX) >> 1) + (q >> 1)) ^ r;
+            const double* sak = sa + (kk / XBOX) * (BM * XBOX) + 2 * chunk;
+#pragma unroll
+            for (int i = 0; i < TM; ++i) af[i] = sak[i * 8 * XBOX];
+#else
 #pragma unroll
             for (int i = 0; i < TM; ++i) af[i] = sa[i * 8 * LDA + kk];
+#endif
 #pragma unroll
             for (int j = 0; j < TN; ++j) bf[j] = sb[kk * LDB + j * 8];
 #pragma unroll
@@ -247,7 +363,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_dmma_kernel(GemmArgs g) 
                 for (int j = 0; j < TN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
     }
+#if !MEXP_GEMM_TMA
     cp_wait<0>();
+#endif
 
 #pragma unroll
     for (int i = 0; i < TM; ++i)
@@ -368,6 +486,29 @@ __global__ void nan_kernel(double* __restrict__ out, int n, const int32_t* __res
         out[m * total + e] = __longlong_as_double(0x7ff8000000000000ll);
 }
 
+// 3D tensor map over a workspace buffer of `batch` np x np matrices: boxes of
+// 16 (k) x 128 (rows) x 1 (matrix), 128B swizzle (the X-operand TMA loads)
+bool make_x_map(CUtensorMap* map, const double* base, int np, int64_t batch) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return false;
+    const cuuint64_t dims[3] = {cuuint64_t(np), cuuint64_t(np), cuuint64_t(batch)};
+    const cuuint64_t strides[2] = {cuuint64_t(np) * sizeof(double), cuuint64_t(np) * np * sizeof(double)};
+    const cuuint32_t box[3] = {16, cuuint32_t(BM), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+thread_local int64_t g_map_batch = 0;  // matrices per workspace buffer of the current call
+
 template <int EPI>
 int gemm(const double* X, const double* Y, std::initializer_list<const double*> in,
          std::initializer_list<double*> out, const int32_t* d_list, int count, int np,
@@ -401,11 +542,18 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
     g.list = d_list;
     g.np = np;
     g.mstride = int64_t(np) * np;
+    CUtensorMap tmx{};
+#if MEXP_GEMM_TMA == 2
+    if (!make_x_map(&tmx, X, np, g_map_batch)) {
+        g_err = "cuTensorMapEncodeTiled failed";
+        return MEXP_ERR_CUDA;
+    }
+#endif
     for (int z0 = 0; z0 < count; z0 += 65535) {
         const int zc = std::min(count - z0, 65535);
         g.list = d_list + z0;
         dim3 grid(np / BN, np / BM, zc);
-        gemm_dmma_kernel<EPI><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(g);
+        gemm_dmma_kernel<EPI><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(g, tmx);
         launches->fetch_add(1, std::memory_order_relaxed);
     }
     LCUDA(cudaGetLastError());
@@ -445,6 +593,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     }
     double* W[kMaxBuffers] = {};
     for (int k = 0; k < kBuffers; ++k) W[k] = ws.buf + size_t(k) * batch * mat;
+    g_map_batch = batch;
 
     unsigned long long* maxbits = nullptr;
     int* bad = nullptr;
@@ -824,6 +973,7 @@ int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaSt
     int32_t* list = nullptr;
     mexp_selection* sel0 = nullptr;  // s = 0 records: prep copies without scaling
     LCUDA(cudaMallocAsync(&w, sizeof(double) * 2 * batch * mat, st));
+    g_map_batch = batch;
     LCUDA(cudaMallocAsync(&list, sizeof(int32_t) * batch, st));
     LCUDA(cudaMallocAsync(&sel0, sizeof(mexp_selection) * batch, st));
     LCUDA(cudaMemsetAsync(sel0, 0, sizeof(mexp_selection) * batch, st));
