@@ -54,7 +54,9 @@ typedef enum { MEXP_FAMILY_TAYLOR_NEW = 0, MEXP_FAMILY_TAYLOR_PS = 1, MEXP_FAMIL
 typedef enum { MEXP_ACCURACY_SINGLE = 0, MEXP_ACCURACY_DOUBLE = 1 } mexp_accuracy;
 
 /* Storage/arithmetic type of a batched call. F64 is the reference's type;
- * F32 evaluates in fp32 with FFMA (never TF32), norm and (m,s) in fp64. */
+ * F32 evaluates in fp32 with FFMA (never TF32) for n <= 64, norm and (m,s) in
+ * fp64; beyond n = 64 (and for the Pade family) fp32 storage runs the fp64
+ * engine on the widened values and rounds e^A once to float. */
 typedef enum { MEXP_F64 = 0, MEXP_F32 = 1 } mexp_dtype;
 
 /* Rounding policy of the fp64 small-N path (n <= 64):

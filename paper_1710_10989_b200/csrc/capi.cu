@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "async_buffer.hpp"
 #include "expm_cluster.cuh"
 #include "expm_common.cuh"
 #include "expm_large.cuh"
@@ -201,10 +202,12 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
         MEXP_CUDA(cudaGetLastError());
         return MEXP_OK;
     }
+    AsyncBuffer work_buf(st);
     int32_t* work = nullptr;
     const bool defer = kDefer && rounding == MEXP_ROUND_AUTO;
     if (defer) {
-        MEXP_CUDA(cudaMallocAsync(&work, sizeof(int32_t) * (batch + 1), st));
+        MEXP_CUDA(work_buf.alloc(sizeof(int32_t) * (batch + 1)));
+        work = work_buf.get<int32_t>();
         MEXP_CUDA(cudaMemsetAsync(work + batch, 0, sizeof(int32_t), st));
     }
     const int64_t want = (batch + 4 * kN8WarpsPerBlock - 1) / (4 * kN8WarpsPerBlock);
@@ -230,7 +233,6 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
                                                             work + batch);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         MEXP_CUDA(cudaGetLastError());
-        MEXP_CUDA(cudaFreeAsync(work, st));
     }
     return MEXP_OK;
 }
@@ -315,13 +317,33 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
                 int rounding, mexp_selection* d_sel, cudaStream_t st) {
     if (batch == 0) return MEXP_OK;
     if (n > 64) {
-        // the large-n engine is tensor-core DMMA only: no reference-rounded
-        // GEMM and no fp32 path beyond n = 64
-        if (dtype != MEXP_F64 || rounding == MEXP_ROUND_REFERENCE) return MEXP_ERR_UNSUPPORTED;
-        const int r = large_expm_f64(static_cast<const double*>(d_a), static_cast<double*>(d_out),
-                                     d_sel, n, batch, accuracy, st, &g_launches);
+        // the large-n engine is tensor-core DMMA only: no reference-rounded GEMM
+        if (rounding == MEXP_ROUND_REFERENCE) return MEXP_ERR_UNSUPPORTED;
+        if (dtype == MEXP_F64) {
+            const int r = large_expm_f64(static_cast<const double*>(d_a), static_cast<double*>(d_out),
+                                         d_sel, n, batch, accuracy, st, &g_launches);
+            if (r == MEXP_ERR_CUDA) g_last_cuda_error = large_last_error();
+            return r;
+        }
+        // fp32 storage beyond n = 64: the correctly rounded path is the fp64
+        // DMMA engine on the exactly widened values (the reference's own
+        // arithmetic), e^A rounded once to float -- never TF32
+        const size_t bytes = size_t(batch) * n * n * sizeof(double);
+        AsyncBuffer bin(st), bout(st);
+        MEXP_CUDA(bin.alloc(bytes));
+        MEXP_CUDA(bout.alloc(bytes));
+        double* win = bin.get<double>();
+        double* wout = bout.get<double>();
+        const int grid = 4 * num_sms();
+        pad_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(d_a), win, n, n, batch);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        const int r = large_expm_f64(win, wout, d_sel, n, batch, accuracy, st, &g_launches);
         if (r == MEXP_ERR_CUDA) g_last_cuda_error = large_last_error();
-        return r;
+        if (r != MEXP_OK) return r;
+        unpad_kernel<<<grid, 256, 0, st>>>(wout, static_cast<float*>(d_out), n, n, batch);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        MEXP_CUDA(cudaGetLastError());
+        return MEXP_OK;
     }
     const int np = padded_n(n);
     if (dtype == MEXP_F32 && is_pade(accuracy)) {
@@ -331,9 +353,11 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
         // the fp64 engine -- the reference's own arithmetic -- and rounds
         // e^A once to float
         const size_t bytes = size_t(batch) * np * np * sizeof(double);
-        double *win = nullptr, *wout = nullptr;
-        MEXP_CUDA(cudaMallocAsync(&win, bytes, st));
-        MEXP_CUDA(cudaMallocAsync(&wout, bytes, st));
+        AsyncBuffer bin(st), bout(st);
+        MEXP_CUDA(bin.alloc(bytes));
+        MEXP_CUDA(bout.alloc(bytes));
+        double* win = bin.get<double>();
+        double* wout = bout.get<double>();
         const int grid = 4 * num_sms();
         pad_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(d_a), win, n, np, batch);
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -341,20 +365,21 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
         if (r != MEXP_OK) return r;
         unpad_kernel<<<grid, 256, 0, st>>>(wout, static_cast<float*>(d_out), n, np, batch);
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        MEXP_CUDA(cudaFreeAsync(win, st));
-        MEXP_CUDA(cudaFreeAsync(wout, st));
         MEXP_CUDA(cudaGetLastError());
         return MEXP_OK;
     }
     const size_t esz = dtype == MEXP_F64 ? sizeof(double) : sizeof(float);
     const void* src = d_a;
     void* dst = d_out;
+    AsyncBuffer bin(st), bout(st);
     void* pin = nullptr;
     void* pout = nullptr;
     if (np != n) {
         const size_t bytes = size_t(batch) * np * np * esz;
-        MEXP_CUDA(cudaMallocAsync(&pin, bytes, st));
-        MEXP_CUDA(cudaMallocAsync(&pout, bytes, st));
+        MEXP_CUDA(bin.alloc(bytes));
+        MEXP_CUDA(bout.alloc(bytes));
+        pin = bin.get<void>();
+        pout = bout.get<void>();
         const int grid = 4 * num_sms();
         if (dtype == MEXP_F64)
             pad_kernel<<<grid, 256, 0, st>>>(static_cast<const double*>(d_a), static_cast<double*>(pin),
@@ -384,8 +409,6 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
             unpad_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(pout),
                                                static_cast<float*>(d_out), n, np, batch);
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        MEXP_CUDA(cudaFreeAsync(pin, st));
-        MEXP_CUDA(cudaFreeAsync(pout, st));
     }
     MEXP_CUDA(cudaGetLastError());
     return MEXP_OK;

@@ -37,6 +37,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include "async_buffer.hpp"
 #include "expm_common.cuh"
 #include "expm_large.cuh"
 #include "lu_batched.cuh"
@@ -595,14 +596,18 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     for (int k = 0; k < kBuffers; ++k) W[k] = ws.buf + size_t(k) * batch * mat;
     g_map_batch = batch;
 
-    unsigned long long* maxbits = nullptr;
-    int* bad = nullptr;
-    mexp_selection* d_sel = d_sel_user;
-    int32_t* d_lists = nullptr;
-    LCUDA(cudaMallocAsync(&maxbits, sizeof(unsigned long long) * batch + sizeof(int) * batch, st));
-    bad = reinterpret_cast<int*>(maxbits + batch);
+    // per-call scratch, released on every exit path
+    AsyncBuffer maxbits_buf(st), sel_buf(st), lists_buf(st), extra_buf(st);
+    LCUDA(maxbits_buf.alloc(sizeof(unsigned long long) * batch + sizeof(int) * batch));
+    unsigned long long* maxbits = maxbits_buf.get<unsigned long long>();
+    int* bad = reinterpret_cast<int*>(maxbits + batch);
     LCUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long) * batch + sizeof(int) * batch, st));
-    if (!d_sel) LCUDA(cudaMallocAsync(&d_sel, sizeof(mexp_selection) * batch, st));
+    mexp_selection* d_sel = d_sel_user;
+    if (!d_sel) {
+        LCUDA(sel_buf.alloc(sizeof(mexp_selection) * batch));
+        d_sel = sel_buf.get<mexp_selection>();
+    }
+    int32_t* d_lists = nullptr;
 
     norm_cols_kernel<<<dim3((n + 255) / 256, unsigned(batch)), 256, 0, st>>>(d_a, n, batch, maxbits, bad);
     select_kernel<<<unsigned((batch + 255) / 256), 256, 0, st>>>(maxbits, bad, batch, acc_arg, d_sel);
@@ -695,7 +700,8 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     const size_t off_bad = append(bad_list);
     const size_t off_all2 = append(all_ok);
     if (!host_lists.empty()) {
-        LCUDA(cudaMallocAsync(&d_lists, sizeof(int32_t) * host_lists.size(), st));
+        LCUDA(lists_buf.alloc(sizeof(int32_t) * host_lists.size()));
+        d_lists = lists_buf.get<int32_t>();
         LCUDA(cudaMemcpyAsync(d_lists, host_lists.data(), sizeof(int32_t) * host_lists.size(),
                               cudaMemcpyHostToDevice, st));
     }
@@ -932,10 +938,10 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         std::vector<int32_t> ev, od;
         for (int32_t m : all_ok) ((h_sel[m].s & 1) ? od : ev).push_back(m);
         // these lists were not uploaded: append now needs a second upload
-        int32_t* d_extra = nullptr;
         std::vector<int32_t> both(ev);
         both.insert(both.end(), od.begin(), od.end());
-        LCUDA(cudaMallocAsync(&d_extra, sizeof(int32_t) * both.size(), st));
+        LCUDA(extra_buf.alloc(sizeof(int32_t) * both.size()));
+        int32_t* d_extra = extra_buf.get<int32_t>();
         LCUDA(cudaMemcpyAsync(d_extra, both.data(), sizeof(int32_t) * both.size(),
                               cudaMemcpyHostToDevice, st));
         if (!ev.empty())
@@ -945,7 +951,6 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
                 S, d_out, n, np, d_extra + ev.size());
         launches->fetch_add(2, std::memory_order_relaxed);
         LCUDA(cudaStreamSynchronize(st));  // `both` must outlive the async copy
-        LCUDA(cudaFreeAsync(d_extra, st));
     }
     if (!bad_list.empty()) {
         nan_kernel<<<dim3(64, unsigned(bad_list.size())), 256, 0, st>>>(d_out, n, L(off_bad));
@@ -958,9 +963,6 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     }
     LCUDA(cudaGetLastError());
     LCUDA(cudaStreamSynchronize(st));  // host lists must outlive their async upload
-    if (d_lists) LCUDA(cudaFreeAsync(d_lists, st));
-    LCUDA(cudaFreeAsync(maxbits, st));
-    if (!d_sel_user) LCUDA(cudaFreeAsync(d_sel, st));
     return MEXP_OK;
 }
 
@@ -969,13 +971,14 @@ int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaSt
     if (rounding == MEXP_ROUND_REFERENCE) return MEXP_ERR_UNSUPPORTED;
     const int np = (n + BM - 1) / BM * BM;
     const int64_t mat = int64_t(np) * np;
-    double* w = nullptr;
-    int32_t* list = nullptr;
-    mexp_selection* sel0 = nullptr;  // s = 0 records: prep copies without scaling
-    LCUDA(cudaMallocAsync(&w, sizeof(double) * 2 * batch * mat, st));
+    AsyncBuffer w_buf(st), list_buf(st), sel0_buf(st);
+    LCUDA(w_buf.alloc(sizeof(double) * 2 * batch * mat));
+    LCUDA(list_buf.alloc(sizeof(int32_t) * batch));
+    LCUDA(sel0_buf.alloc(sizeof(mexp_selection) * batch));  // s = 0: prep copies unscaled
+    double* w = w_buf.get<double>();
+    int32_t* list = list_buf.get<int32_t>();
+    mexp_selection* sel0 = sel0_buf.get<mexp_selection>();
     g_map_batch = batch;
-    LCUDA(cudaMallocAsync(&list, sizeof(int32_t) * batch, st));
-    LCUDA(cudaMallocAsync(&sel0, sizeof(mexp_selection) * batch, st));
     LCUDA(cudaMemsetAsync(sel0, 0, sizeof(mexp_selection) * batch, st));
     std::vector<int32_t> idx(batch);
     for (int64_t m = 0; m < batch; ++m) idx[m] = int32_t(m);
@@ -993,9 +996,6 @@ int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaSt
     launches->fetch_add(1, std::memory_order_relaxed);
     LCUDA(cudaGetLastError());
     LCUDA(cudaStreamSynchronize(st));  // idx must outlive the async copy
-    LCUDA(cudaFreeAsync(w, st));
-    LCUDA(cudaFreeAsync(list, st));
-    LCUDA(cudaFreeAsync(sel0, st));
     return MEXP_OK;
 }
 

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <string>
 
+#include "async_buffer.hpp"
 #include "expm_common.cuh"
 #include "lu_batched.cuh"
 
@@ -337,8 +338,9 @@ int lu_solve_batched(double* M, double* R, int np, int64_t batch, const int32_t*
     const size_t pv_b = sizeof(double) * size_t(batch) * maxg;
     const size_t pr_b = sizeof(int) * size_t(batch) * maxg;
     const size_t ct_b = sizeof(unsigned) * size_t(batch);
-    char* scratch = nullptr;
-    LUCUDA(cudaMallocAsync(&scratch, piv_b + pv_b + pr_b + ct_b + 64, st));
+    AsyncBuffer scratch_buf(st);
+    LUCUDA(scratch_buf.alloc(piv_b + pv_b + pr_b + ct_b + 64));
+    char* scratch = scratch_buf.get<char>();
     double* part_v = reinterpret_cast<double*>(scratch);
     int* piv = reinterpret_cast<int*>(scratch + pv_b);
     int* part_r = reinterpret_cast<int*>(scratch + pv_b + piv_b);
@@ -373,7 +375,6 @@ int lu_solve_batched(double* M, double* R, int np, int64_t batch, const int32_t*
         if ((r = sub(R, M, R, 0, 0, j, j, np, np, d_list, count, st, launches))) return r;
     }
     LUCUDA(cudaGetLastError());
-    LUCUDA(cudaFreeAsync(scratch, st));
     return MEXP_OK;
 }
 

@@ -87,3 +87,19 @@ def test_cfg5_leading_block_and_structure(cuda, oracle):
     assert bool((torch.tril(out[0], -1) == 0).all())
     diag = torch.diagonal(out[0]).cpu().numpy()
     assert np.max(np.abs(diag - np.exp(np.diag(a[0]))) / np.exp(np.diag(a[0]))) <= 1e-12
+
+
+def test_large_n_fp32_storage(cuda, oracle):
+    """fp32 storage beyond n = 64: the fp64 DMMA engine on the widened values
+    (never TF32), e^A rounded once; (m, s) from the fp64 norm of the floats."""
+    rng = np.random.default_rng(64)
+    n = 100
+    norms = np.array([1e-6, 0.3, 2.5, 40.0])
+    a = rng.standard_normal((len(norms), n, n))
+    a *= (norms / workloads.one_norm_batched(a))[:, None, None]
+    a = a.astype(np.float32)
+    ref = oracle.expm_batch(a, accuracy=0)
+    out, sel, st = mx.expm_batched_host(a, accuracy=mx.Accuracy.Single)
+    assert st == mx.OK and out.dtype == np.float32
+    assert np.array_equal(sel["degree"], ref.degree) and np.array_equal(sel["s"], ref.s)
+    assert rel_fro(out.astype(np.float64), ref.out).max() <= 50 * n * 2.0 ** -24

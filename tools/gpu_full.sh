@@ -1,0 +1,6 @@
+#!/bin/bash
+# full GPU test suite + default bench line
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1
