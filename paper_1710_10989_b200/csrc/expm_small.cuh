@@ -466,24 +466,32 @@ __device__ bool lu_solve_group(const G& g, T* M, T* R, int* flag) {
     constexpr int N = G::NDIM, LD = G::LD, TH = G::THREADS;
     static_assert(TH % N == 0, "threads cover whole columns");
     constexpr int RS = TH / N;  // row phases of the trailing update
+    // small n: every loop fully unrolled (the index arithmetic and branches of
+    // the rolled loops cost more than the arithmetic at n = 8)
+    constexpr int kU = N <= 16 ? N : 1;
+    constexpr int kShfl = N >= 32 ? 16 : N / 2;  // lanes holding candidates: [0, N)
     const int j = g.tid % N, r0 = g.tid / N;
-#pragma unroll 1
+#pragma unroll kU
     for (int k = 0; k < N; ++k) {
+        int p = N;
         if (g.warp == 0) {
             // pivot: the first row holding the largest |M[i][k]|, i >= k, with
             // the reference's strict '>' scan from |M[k][k]| (NaN never wins;
             // a NaN diagonal keeps p = k)
             T best = T(-1);
-            int p = N;
-            for (int i = k + g.lane; i < N; i += 32) {
-                const T v = fabs(M[i * LD + k]);
-                if (v > best) {
-                    best = v;
-                    p = i;
+#pragma unroll
+            for (int i0 = 0; i0 < N; i0 += 32) {
+                const int i = i0 + g.lane;
+                if (i >= k && i < N) {
+                    const T v = fabs(M[i * LD + k]);
+                    if (v > best) {
+                        best = v;
+                        p = i;
+                    }
                 }
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
+            for (int o = kShfl; o > 0; o >>= 1) {
                 const T ob = __shfl_xor_sync(0xffffffffu, best, o);
                 const int op = __shfl_xor_sync(0xffffffffu, p, o);
                 if (ob > best || (ob == best && op < p)) {
@@ -493,10 +501,17 @@ __device__ bool lu_solve_group(const G& g, T* M, T* R, int* flag) {
             }
             const T vk = fabs(M[k * LD + k]);
             if (vk != vk) p = k;
-            if (g.lane == 0) *flag = (vk == vk && best == T(0)) ? -1 : p;
+            if (vk == vk && best == T(0)) p = -1;
+            if constexpr (G::W > 1) {
+                if (g.lane == 0) *flag = p;
+            } else {
+                p = __shfl_sync(0xffffffffu, p, 0);
+            }
         }
-        g.sync();
-        const int p = *flag;
+        if constexpr (G::W > 1) {
+            g.sync();
+            p = *flag;
+        }
         if (p < 0) return false;
         if (p != k && g.tid < N) {  // swap rows k and p of M and R
             const T m0 = M[k * LD + j], r0v = R[k * LD + j];
@@ -507,23 +522,40 @@ __device__ bool lu_solve_group(const G& g, T* M, T* R, int* flag) {
         }
         g.sync();
         const T piv = M[k * LD + k];
-        for (int i = k + 1 + g.tid; i < N; i += TH) M[i * LD + k] = lu_div(M[i * LD + k], piv);
+        if constexpr (N <= 16) {  // k is a constant here: predicated, unrolled
+#pragma unroll
+            for (int i0 = 0; i0 < N; i0 += TH) {
+                const int i = k + 1 + i0 + g.tid;
+                if (i < N) M[i * LD + k] = lu_div(M[i * LD + k], piv);
+            }
+        } else {  // rolled: only the rows below k
+            for (int i = k + 1 + g.tid; i < N; i += TH) M[i * LD + k] = lu_div(M[i * LD + k], piv);
+        }
         g.sync();
         if (j > k) {
             const T pk = M[k * LD + j];
-            for (int i = k + 1 + r0; i < N; i += RS) M[i * LD + j] = lu_fms(M[i * LD + j], M[i * LD + k], pk);
+            if constexpr (N <= 16) {
+#pragma unroll
+                for (int i0 = 0; i0 < N; i0 += RS) {
+                    const int i = k + 1 + i0 + r0;
+                    if (i < N) M[i * LD + j] = lu_fms(M[i * LD + j], M[i * LD + k], pk);
+                }
+            } else {
+                for (int i = k + 1 + r0; i < N; i += RS)
+                    M[i * LD + j] = lu_fms(M[i * LD + j], M[i * LD + k], pk);
+            }
         }
         g.sync();
     }
     if (g.tid < N) {  // one right-hand-side column per thread (lu_apply)
         const int c = g.tid;
-#pragma unroll 1
+#pragma unroll kU
         for (int i = 1; i < N; ++i) {
             T s = R[i * LD + c];
             for (int q = 0; q < i; ++q) s = lu_fms(s, M[i * LD + q], R[q * LD + c]);
             R[i * LD + c] = s;
         }
-#pragma unroll 1
+#pragma unroll kU
         for (int i = N - 1; i >= 0; --i) {
             T s = R[i * LD + c];
             for (int q = i + 1; q < N; ++q) s = lu_fms(s, M[i * LD + q], R[q * LD + c]);
