@@ -132,9 +132,11 @@ int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t 
     return MEXP_OK;
 }
 
-// Ring of device counters for kernels that hand out work dynamically; a slot
-// is reused only after 4096 further launches on the device.
-int next_ticket(unsigned long long** out) {
+// Ring of device counters for kernels that hand out work dynamically. Slots
+// start zeroed; the kernel using slot i zeroes slot i + kSlots/2, which its
+// next user reaches 2048 launches later -- no memset per launch (at most
+// 2048 launches of a device in flight at once).
+int next_ticket(unsigned long long** out, unsigned long long** clear) {
     constexpr int kSlots = 4096;
     static unsigned long long* ring[16] = {};
     static std::atomic<uint32_t> next[16];
@@ -144,9 +146,16 @@ int next_ticket(unsigned long long** out) {
     if (!ring[dev]) {
         static std::mutex mu;
         std::lock_guard<std::mutex> lock(mu);
-        if (!ring[dev]) MEXP_CUDA(cudaMalloc(&ring[dev], sizeof(unsigned long long) * kSlots));
+        if (!ring[dev]) {
+            unsigned long long* r = nullptr;
+            MEXP_CUDA(cudaMalloc(&r, sizeof(unsigned long long) * kSlots));
+            MEXP_CUDA(cudaMemset(r, 0, sizeof(unsigned long long) * kSlots));
+            ring[dev] = r;
+        }
     }
-    *out = ring[dev] + (next[dev].fetch_add(1) % kSlots);
+    const uint32_t i = next[dev].fetch_add(1) % kSlots;
+    *out = ring[dev] + i;
+    *clear = ring[dev] + (i + kSlots / 2) % kSlots;
     return MEXP_OK;
 }
 
@@ -214,17 +223,17 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
     const int grid = int(want < cap ? want : cap);
     // work ticket for the dynamically distributed rounds: a slot of a
     // persistent per-device ring, reset in stream order
-    unsigned long long* ticket = nullptr;
+    unsigned long long *ticket = nullptr, *ticket_clear = nullptr;
     {
-        int r = next_ticket(&ticket);
+        int r = next_ticket(&ticket, &ticket_clear);
         if (r != MEXP_OK) return r;
     }
-    MEXP_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st));
     // AUTO: the last fast_tail() squarings of the reference-rounded matrices
     // run with FMA/DMMA rounding (expm_small.cuh run_expm)
     const int rounding_arg = rounding == MEXP_ROUND_AUTO ? (rounding | (fast_tail() << 8)) : rounding;
     kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding_arg, smin,
-                                                 work, defer ? work + batch : nullptr, ticket);
+                                                 work, defer ? work + batch : nullptr, ticket,
+                                                 ticket_clear);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());
     if (defer) {
@@ -416,7 +425,7 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
 
 // ---- host pipeline state: per-device streams and chunk buffers ------------
 struct HostPipe {
-    static constexpr int kStreams = 4;
+    static constexpr int kStreams = 8;  // capacity; host_streams() are used
     int device = -1;
     cudaStream_t st[kStreams] = {};
     void* d_in[kStreams] = {};
@@ -426,9 +435,21 @@ struct HostPipe {
     int64_t cap_sel = 0;
     mexp_selection* h_sel_scratch = nullptr;  // pinned, used when the caller passes none
     std::vector<cudaEvent_t> ev;  // one per chunk of a call: its records have landed
+    std::vector<cudaEvent_t> ev_in, ev_k;  // staged pipeline: chunk's H2D / kernel done
     int64_t h_sel_cap = 0;
     std::mutex mu;
 };
+
+// streams (and chunk buffer slots) of the host pipeline (MEXP_HOST_STREAMS,
+// default 4, 3 to 8)
+int host_streams() {
+    static int v = [] {
+        const char* e = std::getenv("MEXP_HOST_STREAMS");
+        const int x = e ? std::atoi(e) : 4;
+        return x < 3 ? 3 : (x > HostPipe::kStreams ? HostPipe::kStreams : x);
+    }();
+    return v;
+}
 
 HostPipe& pipe_for_current_device() {
     static HostPipe pipes[16];
@@ -441,12 +462,12 @@ int ensure_pipe(HostPipe& p, size_t bytes, int64_t sels) {
     int dev = 0;
     MEXP_CUDA(cudaGetDevice(&dev));
     if (p.device != dev) {
-        for (int i = 0; i < HostPipe::kStreams; ++i)
+        for (int i = 0; i < host_streams(); ++i)
             MEXP_CUDA(cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking));
         p.device = dev;
     }
     if (bytes > p.cap_bytes || sels > p.cap_sel) {
-        for (int i = 0; i < HostPipe::kStreams; ++i) {
+        for (int i = 0; i < host_streams(); ++i) {
             MEXP_CUDA(cudaStreamSynchronize(p.st[i]));
             cudaFree(p.d_in[i]);
             cudaFree(p.d_out[i]);
@@ -628,13 +649,14 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
         }
     }
     const int64_t nchunks = int64_t(plan.size());
-    while (int64_t(p.ev.size()) < nchunks) {
-        cudaEvent_t e;
-        MEXP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        p.ev.push_back(e);
-    }
+    for (auto* v : {&p.ev, &p.ev_in, &p.ev_k})
+        while (int64_t(v->size()) < nchunks) {
+            cudaEvent_t e;
+            MEXP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            v->push_back(e);
+        }
     auto h2d = [&](int64_t c) -> int {
-        const int k = int(c % HostPipe::kStreams);
+        const int k = int(c % host_streams());
         const int64_t b0 = plan[c].first, nb = plan[c].second;
         MEXP_CUDA(cudaMemcpyAsync(p.d_in[k], src + b0 * mat_bytes, nb * mat_bytes,
                                   cudaMemcpyHostToDevice, p.st[k]));
@@ -643,20 +665,78 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
     // the large-n engine synchronises its stream once per call (it schedules
     // from the selections), so the next chunk's H2D is issued before it runs
     const bool prefetch = n > 64;
+    // MEXP_HOST_TRACE=1: timed events around every stage, timeline on stderr
+    static const bool trace = std::getenv("MEXP_HOST_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tev.push_back(e);
+    };
+    // Small n: a staged pipeline -- every H2D in order on one stream, every
+    // kernel on a second, every D2H on a third, chained by events, chunk
+    // buffers rotating over host_streams() slots. Each copy direction then
+    // streams chunk after chunk at full rate instead of round-robining
+    // between concurrent copies of several streams (MEXP_HOST_PIPE=streams
+    // restores the per-stream pipeline).
+    static const bool staged = [] {
+        const char* e = std::getenv("MEXP_HOST_PIPE");
+        return !(e && std::strcmp(e, "streams") == 0);
+    }();
+    if (!prefetch && staged) {
+        cudaStream_t s_in = p.st[0], s_k = p.st[1], s_out = p.st[2];
+        const int nslots = host_streams();
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int k = int(c % nslots);
+            const int64_t b0 = plan[c].first, nb = plan[c].second;
+            if (c >= nslots) MEXP_CUDA(cudaStreamWaitEvent(s_in, p.ev_k[c - nslots], 0));
+            MEXP_CUDA(cudaMemcpyAsync(p.d_in[k], src + b0 * mat_bytes, nb * mat_bytes,
+                                      cudaMemcpyHostToDevice, s_in));
+            MEXP_CUDA(cudaEventRecord(p.ev_in[c], s_in));
+            MEXP_CUDA(cudaStreamWaitEvent(s_k, p.ev_in[c], 0));
+            if (c >= nslots) MEXP_CUDA(cudaStreamWaitEvent(s_k, p.ev[c - nslots], 0));
+            r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, aarg, rounding, p.d_sel[k], s_k);
+            if (r != MEXP_OK) return r;
+            MEXP_CUDA(cudaEventRecord(p.ev_k[c], s_k));
+            MEXP_CUDA(cudaStreamWaitEvent(s_out, p.ev_k[c], 0));
+            MEXP_CUDA(cudaMemcpyAsync(dst + b0 * mat_bytes, p.d_out[k], nb * mat_bytes,
+                                      cudaMemcpyDeviceToHost, s_out));
+            MEXP_CUDA(cudaMemcpyAsync(hs + b0, p.d_sel[k], nb * sizeof(mexp_selection),
+                                      cudaMemcpyDeviceToHost, s_out));
+            MEXP_CUDA(cudaEventRecord(p.ev[c], s_out));
+        }
+    }
     if (prefetch && (r = h2d(0)) != MEXP_OK) return r;
-    for (int64_t c = 0; c < nchunks; ++c) {
-        const int k = int(c % HostPipe::kStreams);
+    for (int64_t c = 0; c < nchunks && !(!prefetch && staged); ++c) {
+        const int k = int(c % host_streams());
         const int64_t b0 = plan[c].first, nb = plan[c].second;
         cudaStream_t st = p.st[k];
+        mark(st);
         if (!prefetch && (r = h2d(c)) != MEXP_OK) return r;
         if (prefetch && c + 1 < nchunks && (r = h2d(c + 1)) != MEXP_OK) return r;
+        mark(st);
         r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, aarg, rounding, p.d_sel[k], st);
         if (r != MEXP_OK) return r;
+        mark(st);
         MEXP_CUDA(cudaMemcpyAsync(dst + b0 * mat_bytes, p.d_out[k], nb * mat_bytes,
                                   cudaMemcpyDeviceToHost, st));
         MEXP_CUDA(cudaMemcpyAsync(hs + b0, p.d_sel[k], nb * sizeof(mexp_selection),
                                   cudaMemcpyDeviceToHost, st));
+        mark(st);
         MEXP_CUDA(cudaEventRecord(p.ev[c], st));
+    }
+    if (trace) {
+        cudaDeviceSynchronize();
+        for (int64_t c = 0; c < nchunks; ++c) {
+            float t[4];
+            for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], tev[0], tev[4 * c + i]);
+            std::fprintf(stderr, "chunk %2lld n=%7lld  h2d %8.1f-%8.1f  kernel -%8.1f  d2h -%8.1f us\n",
+                         (long long)c, (long long)plan[c].second, 1e3 * t[0], 1e3 * t[1], 1e3 * t[2],
+                         1e3 * t[3]);
+        }
+        for (auto e : tev) cudaEventDestroy(e);
     }
     // Host-side work on the records (status scan, copy to a pageable h_sel)
     // overlaps the pipeline: chunk c is handled as soon as its records land.
@@ -673,7 +753,7 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
                     break;
                 }
     }
-    for (int i = 0; i < HostPipe::kStreams; ++i) MEXP_CUDA(cudaStreamSynchronize(p.st[i]));
+    for (int i = 0; i < host_streams(); ++i) MEXP_CUDA(cudaStreamSynchronize(p.st[i]));
     return first_status;
 }
 

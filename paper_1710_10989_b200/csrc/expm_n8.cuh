@@ -189,10 +189,12 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     expm8_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
                      mexp_selection* __restrict__ sel, int64_t batch, int acc_arg, int rounding_arg,
                      int exact_s_min, int32_t* __restrict__ worklist, int32_t* __restrict__ wcount,
-                     unsigned long long* __restrict__ ticket) {
+                     unsigned long long* __restrict__ ticket,
+                     unsigned long long* __restrict__ ticket_clear) {
     using Group8 = Group8T<kSplit>;
     using F = typename Group8::Frag;
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ticket_clear = 0ull;  // see capi.cu next_ticket
     // rounding policy in the low byte; AUTO's fast squaring tail above it
     const int rounding = rounding_arg & 0xff, fast_tail = rounding_arg >> 8;
     // accuracy in the low 4 bits (mexp_accuracy); the family is kFamily
