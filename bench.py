@@ -217,6 +217,9 @@ def parse():
                    help="Family (theta_tables.hpp:8); the headline is taylor-new")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--strong", action="store_true",
+                   help="split the config's batch across the ranks (strong scaling) instead of "
+                        "one full batch per rank (weak, the default)")
     return p.parse_args()
 
 
@@ -281,8 +284,11 @@ def run_ours(args):
     cfg = workloads.CONFIGS[args.config]
     n = cfg.n
     B = cfg.batch
-    # weak scaling: each rank owns a full config-sized batch of its own matrices
-    shard = shard_range(rank, world, B, weak=True)
+    # weak scaling (default): each rank owns a full config-sized batch of its
+    # own matrices; --strong: the config's batch split by matrix across ranks
+    shard = shard_range(rank, world, B, weak=not args.strong)
+    Bl = shard.count
+    total = B if args.strong else world * B
     a_host = workloads.generate(args.config, shard.b0, shard.count)
     torch_dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
     rounding = {"auto": mx.ROUND_AUTO, "reference": mx.ROUND_REFERENCE,
@@ -291,10 +297,10 @@ def run_ours(args):
     esz = 8 if cfg.dtype == "f64" else 4
     mat_bytes = n * n * esz
     # two input/output buffer pairs alternate so the working set exceeds L2
-    pairs = 2 if 2 * B * mat_bytes < 4 * L2_BYTES else 1
+    pairs = 2 if 2 * Bl * mat_bytes < 4 * L2_BYTES else 1
     ins = [torch.from_numpy(a_host).to(dev) for _ in range(pairs)]
     outs = [torch.empty_like(ins[0]) for _ in range(pairs)]
-    sel = torch.empty(B * 16, dtype=torch.uint8, device=dev)
+    sel = torch.empty(Bl * 16, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step(i):
@@ -325,7 +331,7 @@ def run_ours(args):
         ms = max_over_ranks(ms, dev)
         dist.barrier()
     ms_step = ms / args.steps
-    value = world * B / (ms_step * 1e-3)
+    value = total / (ms_step * 1e-3)
 
     # ---- e2e through the host C-ABI call (pinned buffers) ----
     h_in = torch.from_numpy(a_host).pin_memory()
@@ -342,7 +348,7 @@ def run_ours(args):
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
         e2e_s = max_over_ranks(e2e_s, dev)
-    e2e_value = world * B / e2e_s
+    e2e_value = total / e2e_s
 
     # ---- gather of the results to rank 0 (NCCL), timed separately ----
     gather = None
@@ -350,15 +356,17 @@ def run_ours(args):
         torch.cuda.synchronize()
         dist.barrier()
         g0 = time.perf_counter()
-        gathered = gather_to_root(outs[0], [B] * world)
+        counts = [shard_range(r, world, B, weak=not args.strong).count for r in range(world)]
+        gathered = gather_to_root(outs[0], counts)
         torch.cuda.synchronize()
         del gathered
         gather = {"ms": 1e3 * (time.perf_counter() - g0),
-                  "bytes_to_root": (world - 1) * B * mat_bytes, "how": "torch.distributed.gather (NCCL)"}
+                  "bytes_to_root": (sum(counts) - counts[0]) * mat_bytes,
+                  "how": "torch.distributed.gather (NCCL)"}
 
     if rank == 0:
         peaks = load_peaks()
-        alg_bytes = 2.0 * B * mat_bytes  # one read of A, one write of e^A per matrix
+        alg_bytes = 2.0 * Bl * mat_bytes  # one read of A, one write of e^A per matrix (this rank)
         hbm_gbs = alg_bytes / (ms_step * 1e-3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -380,13 +388,14 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+            "vs_baseline": None,
             "dtype": cfg.dtype, "data": "synthetic (seeded, counter-based; see workloads.py)",
             "config": {"workload": args.config, "description": cfg.description, "n": n,
-                       "batch_per_rank": B, "global_batch": world * B, "rounding": args.rounding,
+                       "batch_per_rank": Bl, "global_batch": total, "rounding": args.rounding,
                        "family": args.family,
                        "parallelism": f"matrix-sharded x{world}",
-                       "l2": f"inputs larger than L2 ({pairs} x {2 * B * mat_bytes / 2**20:.0f} MiB "
+                       "l2": f"inputs larger than L2 ({pairs} x {2 * Bl * mat_bytes / 2**20:.0f} MiB "
                              f"in+out, alternating buffers)"},
             "effective_tflops": tflops,
             "compute_peak": {"tflops": peakc, "source": peakc_src, "frac": tflops / peakc},
@@ -394,8 +403,8 @@ def run_ours(args):
                     "frac": hbm_gbs / peaks["hbm_gbs"]},
             "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": B * mat_bytes,
-                    "d2h_bytes_per_step": B * mat_bytes + 16 * B,
+                    "h2d_bytes_per_step": Bl * mat_bytes,
+                    "d2h_bytes_per_step": Bl * mat_bytes + 16 * Bl,
                     "how": "mexp_expm_batched_host, pinned host buffers, wall clock"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
