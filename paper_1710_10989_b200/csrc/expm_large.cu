@@ -806,9 +806,10 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
                 return r;
         }
         // R <- (V - U)^-1 (V + U) for every OK matrix (pade_solve, pade.cpp:26-28)
-        if (!all_ok.empty()) {
-            r = lu_solve_batched(W[2], W[1], np, batch, L(off_all2), int(all_ok.size()), d_sel, st,
-                                 launches);
+        // (grid.y-sized slices of the matrix list)
+        for (size_t i0 = 0; i0 < all_ok.size(); i0 += 65535) {
+            const int cnt = int(std::min<size_t>(65535, all_ok.size() - i0));
+            r = lu_solve_batched(W[2], W[1], np, batch, L(off_all2) + i0, cnt, d_sel, st, launches);
             if (r == MEXP_ERR_CUDA) g_err = lu_last_error();
             if (r) return r;
         }
