@@ -379,8 +379,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // ---- prologue / epilogue kernels -------------------------------------------
 __global__ void norm_cols_kernel(const double* __restrict__ a, int n, int64_t batch,
                                  unsigned long long* __restrict__ maxbits,
-                                 int* __restrict__ bad) {
-    const int64_t m = blockIdx.y;
+                                 int* __restrict__ bad, int64_t m0) {
+    const int64_t m = m0 + blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= batch || j >= n) return;
     const double* p = a + m * int64_t(n) * n + j;
@@ -485,6 +485,13 @@ __global__ void nan_kernel(double* __restrict__ out, int n, const int32_t* __res
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
          e += int64_t(gridDim.x) * blockDim.x)
         out[m * total + e] = __longlong_as_double(0x7ff8000000000000ll);
+}
+
+// Per-matrix kernels index matrices by blockIdx.y (a list entry): launch
+// them in slices of at most 65535 (the grid's y limit), fn(y0, ny)
+template <class Fn>
+void sliced(int64_t count, Fn fn) {
+    for (int64_t y0 = 0; y0 < count; y0 += 65535) fn(y0, unsigned(std::min<int64_t>(65535, count - y0)));
 }
 
 // 3D tensor map over a workspace buffer of `batch` np x np matrices: boxes of
@@ -609,7 +616,9 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     }
     int32_t* d_lists = nullptr;
 
-    norm_cols_kernel<<<dim3((n + 255) / 256, unsigned(batch)), 256, 0, st>>>(d_a, n, batch, maxbits, bad);
+    sliced(batch, [&](int64_t y0, unsigned ny) {
+        norm_cols_kernel<<<dim3((n + 255) / 256, ny), 256, 0, st>>>(d_a, n, batch, maxbits, bad, y0);
+    });
     select_kernel<<<unsigned((batch + 255) / 256), 256, 0, st>>>(maxbits, bad, batch, acc_arg, d_sel);
     launches->fetch_add(2, std::memory_order_relaxed);
 
@@ -709,8 +718,9 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     const dim3 ew_block(256);
     const unsigned ew_rows = unsigned(std::min(np, 64));
     if (!all_ok.empty()) {
-        prep_kernel<<<dim3(ew_rows, unsigned(all_ok.size())), ew_block, 0, st>>>(
-            d_a, W[0], n, np, L(off_all2), d_sel);
+        sliced(int64_t(all_ok.size()), [&](int64_t y0, unsigned ny) {
+            prep_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(d_a, W[0], n, np, L(off_all2) + y0, d_sel);
+        });
         launches->fetch_add(1, std::memory_order_relaxed);
     }
     // the scheme's final GEMM of degree d: finishing matrices -> out, rest -> R
@@ -738,8 +748,10 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
             const double* b = kPadeHost[m - 1];
             const double mr[2][5] = {{0, 1, 0, 0, -1}, {0, 1, 0, 0, 1}};  // V -/+ c
             if (d == 2) {
-                pade2_kernel<<<dim3(ew_rows, unsigned(c)), ew_block, 0, st>>>(W[0], W[2], W[1], np, l,
-                                                                              b[0], b[1]);
+                sliced(c, [&](int64_t y0, unsigned ny) {
+                    pade2_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(W[0], W[2], W[1], np, l + y0,
+                                                                         b[0], b[1]);
+                });
                 launches->fetch_add(1, std::memory_order_relaxed);
                 continue;
             }
@@ -814,8 +826,10 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
             if (r) return r;
         }
         if (pade_s0.count) {  // no squarings: e^A = R
-            unpad_kernel<<<dim3(ew_rows, unsigned(pade_s0.count)), ew_block, 0, st>>>(
-                W[1], d_out, n, np, L(pade_s0.off));
+            sliced(pade_s0.count, [&](int64_t y0, unsigned ny) {
+                unpad_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(W[1], d_out, n, np,
+                                                                     L(pade_s0.off) + y0);
+            });
             launches->fetch_add(1, std::memory_order_relaxed);
         }
     } else {
@@ -915,13 +929,17 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     {  // degree 1: I + A
         const auto& pp = deg_parts[1];
         if (pp.first.count) {
-            t1_kernel<<<dim3(ew_rows, unsigned(pp.first.count)), ew_block, 0, st>>>(
-                W[0], d_out, n, np, n, L(pp.first.off));
+            sliced(pp.first.count, [&](int64_t y0, unsigned ny) {
+                t1_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(W[0], d_out, n, np, n,
+                                                                  L(pp.first.off) + y0);
+            });
             launches->fetch_add(1, std::memory_order_relaxed);
         }
         if (pp.second.count) {
-            t1_kernel<<<dim3(ew_rows, unsigned(pp.second.count)), ew_block, 0, st>>>(
-                W[0], R, np, np, np, L(pp.second.off));
+            sliced(pp.second.count, [&](int64_t y0, unsigned ny) {
+                t1_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(W[0], R, np, np, np,
+                                                                  L(pp.second.off) + y0);
+            });
             launches->fetch_add(1, std::memory_order_relaxed);
         }
     }
@@ -945,21 +963,25 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         int32_t* d_extra = extra_buf.get<int32_t>();
         LCUDA(cudaMemcpyAsync(d_extra, both.data(), sizeof(int32_t) * both.size(),
                               cudaMemcpyHostToDevice, st));
-        if (!ev.empty())
-            unpad_kernel<<<dim3(ew_rows, unsigned(ev.size())), ew_block, 0, st>>>(R, d_out, n, np, d_extra);
-        if (!od.empty())
-            unpad_kernel<<<dim3(ew_rows, unsigned(od.size())), ew_block, 0, st>>>(
-                S, d_out, n, np, d_extra + ev.size());
+        sliced(int64_t(ev.size()), [&](int64_t y0, unsigned ny) {
+            unpad_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(R, d_out, n, np, d_extra + y0);
+        });
+        sliced(int64_t(od.size()), [&](int64_t y0, unsigned ny) {
+            unpad_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(S, d_out, n, np, d_extra + ev.size() + y0);
+        });
         launches->fetch_add(2, std::memory_order_relaxed);
         LCUDA(cudaStreamSynchronize(st));  // `both` must outlive the async copy
     }
     if (!bad_list.empty()) {
-        nan_kernel<<<dim3(64, unsigned(bad_list.size())), 256, 0, st>>>(d_out, n, L(off_bad));
+        sliced(int64_t(bad_list.size()), [&](int64_t y0, unsigned ny) {
+            nan_kernel<<<dim3(64, ny), 256, 0, st>>>(d_out, n, L(off_bad) + y0);
+        });
         launches->fetch_add(1, std::memory_order_relaxed);
     }
     if (pade && !all_ok.empty()) {  // "singular denominator" matrices -> NaN
-        nan_singular_kernel<<<dim3(64, unsigned(all_ok.size())), 256, 0, st>>>(d_out, n, L(off_all2),
-                                                                              d_sel);
+        sliced(int64_t(all_ok.size()), [&](int64_t y0, unsigned ny) {
+            nan_singular_kernel<<<dim3(64, ny), 256, 0, st>>>(d_out, n, L(off_all2) + y0, d_sel);
+        });
         launches->fetch_add(1, std::memory_order_relaxed);
     }
     LCUDA(cudaGetLastError());
@@ -985,7 +1007,9 @@ int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaSt
     for (int64_t m = 0; m < batch; ++m) idx[m] = int32_t(m);
     LCUDA(cudaMemcpyAsync(list, idx.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice, st));
     const unsigned rows = unsigned(std::min(np, 64));
-    prep_kernel<<<dim3(rows, unsigned(batch)), 256, 0, st>>>(d_x, w, n, np, list, sel0);
+    sliced(batch, [&](int64_t y0, unsigned ny) {
+        prep_kernel<<<dim3(rows, ny), 256, 0, st>>>(d_x, w, n, np, list + y0, sel0);
+    });
     launches->fetch_add(1, std::memory_order_relaxed);
     double* bufs[2] = {w, w + batch * mat};
     int r;
@@ -993,7 +1017,9 @@ int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaSt
         if ((r = gemm<EPI_STORE>(bufs[k & 1], bufs[k & 1], {}, {bufs[(k + 1) & 1]}, list, int(batch),
                                  np, st, launches)))
             return r;
-    unpad_kernel<<<dim3(rows, unsigned(batch)), 256, 0, st>>>(bufs[s & 1], d_x, n, np, list);
+    sliced(batch, [&](int64_t y0, unsigned ny) {
+        unpad_kernel<<<dim3(rows, ny), 256, 0, st>>>(bufs[s & 1], d_x, n, np, list + y0);
+    });
     launches->fetch_add(1, std::memory_order_relaxed);
     LCUDA(cudaGetLastError());
     LCUDA(cudaStreamSynchronize(st));  // idx must outlive the async copy

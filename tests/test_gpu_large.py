@@ -103,3 +103,24 @@ def test_large_n_fp32_storage(cuda, oracle):
     assert st == mx.OK and out.dtype == np.float32
     assert np.array_equal(sel["degree"], ref.degree) and np.array_equal(sel["s"], ref.s)
     assert rel_fro(out.astype(np.float64), ref.out).max() <= 50 * n * 2.0 ** -24
+
+
+def test_large_n_batch_beyond_grid_y(cuda, oracle):
+    """More than 65,535 matrices of n > 64: every per-matrix launch of the
+    large-n path is sliced along the grid's y limit."""
+    n, batch = 65, 66000
+    a = np.zeros((batch, n, n))
+    rng = np.random.default_rng(65)
+    idx = np.array([0, 1, 65534, 65535, 65536, batch - 1])
+    for k, i in enumerate(idx):
+        m = rng.uniform(-1, 1, (n, n))
+        a[i] = m * (10.0 ** (k - 3) / np.abs(m).sum(axis=0).max())
+    a[123, 4, 4] = np.nan
+    out, sel, st = mx.expm_batched_host(a, raise_on_error=False)
+    assert st == mx.ERR_NONFINITE and sel["status"][123] == mx.ERR_NONFINITE
+    assert np.isnan(out[123]).all()
+    ref = oracle.expm_batch(a[idx])
+    assert np.array_equal(sel["degree"][idx], ref.degree) and np.array_equal(sel["s"][idx], ref.s)
+    assert rel_fro(out[idx], ref.out).max() <= 50 * n * U53
+    zero = np.setdiff1d(np.arange(batch), np.append(idx, 123))[::997]
+    assert all(np.array_equal(out[i], np.eye(n)) for i in zero)
