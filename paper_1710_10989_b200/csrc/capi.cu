@@ -18,6 +18,7 @@
 #include "expm_common.cuh"
 #include "expm_large.cuh"
 #include "expm_n8.cuh"
+#include "expm_pade8.cuh"
 #include "expm_small.cuh"
 #include "expm_small_f32.cuh"
 
@@ -288,12 +289,36 @@ int launch_small_family(const double* a, double* out, mexp_selection* sel, int64
                                                             smin, st);
 }
 
+int launch_pade8(const double* a, double* out, mexp_selection* sel, int64_t batch, int accuracy,
+                 int rounding, int smin, cudaStream_t st) {
+    static int blocks_per_sm = [] {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, expm8_pade_kernel<8>, 32 * kN8WarpsPerBlock, 0);
+        return b > 0 ? b : 1;
+    }();
+    const int64_t cap = int64_t(blocks_per_sm) * num_sms();
+    const int64_t want = (batch + 4 * kN8WarpsPerBlock - 1) / (4 * kN8WarpsPerBlock);
+    const int grid = int(want < cap ? want : cap);
+    unsigned long long *ticket = nullptr, *ticket_clear = nullptr;
+    const int r = next_ticket(&ticket, &ticket_clear);
+    if (r != MEXP_OK) return r;
+    expm8_pade_kernel<8><<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding,
+                                                                 smin, ticket, ticket_clear);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    MEXP_CUDA(cudaGetLastError());
+    return MEXP_OK;
+}
+
 int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
                   int accuracy, int rounding, int smin, cudaStream_t st) {
     if (batch == 0) return MEXP_OK;
-    if (is_pade(accuracy))  // the generic engine (its LU solve)
-        return launch_small_f64<8, 8, MEXP_FAMILY_PADE>(a, out, sel, batch, accuracy, rounding,
-                                                       smin, st);
+    if (is_pade(accuracy)) {  // four matrices per warp, the LU on all 32 lanes
+        static const bool generic = std::getenv("MEXP_PADE8_GENERIC") != nullptr;
+        if (generic)
+            return launch_small_f64<8, 8, MEXP_FAMILY_PADE>(a, out, sel, batch, accuracy, rounding,
+                                                           smin, st);
+        return launch_pade8(a, out, sel, batch, accuracy, rounding, smin, st);
+    }
     if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)  // the default variant only
         return launch_n8_variant<false, 0, 8, MEXP_FAMILY_TAYLOR_PS>(a, out, sel, batch, accuracy,
                                                                      rounding, smin, st);
