@@ -31,6 +31,7 @@
 // 32 independent DMMAs per k-step keep all four pipes saturated.
 #include <algorithm>
 #include <cstdio>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -572,6 +573,7 @@ struct Workspace {
     double* buf = nullptr;
     size_t bytes = 0;
     int device = -1;
+    std::mutex mu;  // one large-n call per device at a time owns the buffers
 };
 Workspace& workspace() {
     static Workspace ws[16];
@@ -594,6 +596,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     // workspace: kBuffers padded matrices per batch entry + per-matrix scratch
     const size_t need = size_t(kBuffers) * batch * mat * sizeof(double);
     Workspace& ws = workspace();
+    std::lock_guard<std::mutex> ws_lock(ws.mu);  // the call synchronises its stream before returning
     if (ws.bytes < need) {
         if (ws.buf) LCUDA(cudaFreeAsync(ws.buf, st));
         LCUDA(cudaMallocAsync(&ws.buf, need, st));
