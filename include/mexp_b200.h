@@ -67,7 +67,10 @@ typedef enum { MEXP_F64 = 0, MEXP_F32 = 1 } mexp_dtype;
  *   FAST:      FP64 tensor-core DMMA products, FMA combinations;
  *   AUTO:      FAST, except matrices with s >= 6 squarings, whose rounding
  *              differences the squarings amplify, run REFERENCE.
- * The large-n path (n > 64) is always tensor-core DMMA. F32 ignores it. */
+ * For n > 64, REFERENCE runs the products as k-ordered DMUL+DADD chains on
+ * the CUDA cores and the lincombs literally (bit-identical for TaylorNew and
+ * TaylorPS; the Pade LU is DMMA-only and refuses it), AUTO and FAST the
+ * tensor-core DMMA GEMMs. F32 with n <= 64 ignores it. */
 typedef enum { MEXP_ROUND_AUTO = 0, MEXP_ROUND_REFERENCE = 1, MEXP_ROUND_FAST = 2 } mexp_rounding;
 
 /* Per-matrix selection record written by the batched calls (16 bytes).

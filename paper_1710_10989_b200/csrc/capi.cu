@@ -351,11 +351,11 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
                 int rounding, mexp_selection* d_sel, cudaStream_t st) {
     if (batch == 0) return MEXP_OK;
     if (n > 64) {
-        // the large-n engine is tensor-core DMMA only: no reference-rounded GEMM
-        if (rounding == MEXP_ROUND_REFERENCE) return MEXP_ERR_UNSUPPORTED;
+        // DMMA products, or for REFERENCE rounding the k-ordered exact ones
+        // (taylor-new / taylor-ps; the Pade LU is DMMA only)
         if (dtype == MEXP_F64) {
             const int r = large_expm_f64(static_cast<const double*>(d_a), static_cast<double*>(d_out),
-                                         d_sel, n, batch, accuracy, st, &g_launches);
+                                         d_sel, n, batch, accuracy, rounding, st, &g_launches);
             if (r == MEXP_ERR_CUDA) g_last_cuda_error = large_last_error();
             return r;
         }
@@ -371,7 +371,7 @@ int expm_device(const void* d_a, void* d_out, int dtype, int n, int64_t batch, i
         const int grid = 4 * num_sms();
         pad_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(d_a), win, n, n, batch);
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        const int r = large_expm_f64(win, wout, d_sel, n, batch, accuracy, st, &g_launches);
+        const int r = large_expm_f64(win, wout, d_sel, n, batch, accuracy, rounding, st, &g_launches);
         if (r == MEXP_ERR_CUDA) g_last_cuda_error = large_last_error();
         if (r != MEXP_OK) return r;
         unpad_kernel<<<grid, 256, 0, st>>>(wout, static_cast<float*>(d_out), n, n, batch);
@@ -824,7 +824,8 @@ int mexp_b200_squarings_host(double* x, int n, int s) {
     MEXP_CUDA(cudaMalloc(&d, bytes));
     int r = MEXP_OK;
     if (cudaMemcpy(d, x, bytes, cudaMemcpyHostToDevice) != cudaSuccess) r = MEXP_ERR_CUDA;
-    if (r == MEXP_OK) r = squarings_f64(d, n, 1, s, MEXP_ROUND_AUTO, nullptr, &g_launches);
+    // the reference's squarings (expm.cpp:31-35), bit for bit
+    if (r == MEXP_OK) r = squarings_f64(d, n, 1, s, MEXP_ROUND_REFERENCE, nullptr, &g_launches);
     if (r == MEXP_OK && cudaMemcpy(x, d, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
         r = MEXP_ERR_CUDA;
     cudaFree(d);

@@ -117,7 +117,20 @@ struct GemmArgs {
                           // this is the matrix's last product: out[0] -> final_out
     int np;
     int64_t mstride;      // np * np
+    int n;                // the true dimension: the exact product sums k < n only
 };
+
+// Left-to-right linear combination c0*m0 + c1*m1 + ... in the arithmetic of
+// Ops: ExactOps is the reference's lincomb (kernels.cpp:29-37: every multiply
+// and add rounded separately, in order); FastOps fuses into FMAs.
+template <class O>
+__device__ __forceinline__ double lcx(double c0, double m0) {
+    return O::mul(c0, m0);
+}
+template <class O, class... R>
+__device__ __forceinline__ double lcx(double c0, double m0, double c1, double m1, R... rest) {
+    return lcx<O>(1.0, O::mac(O::mul(c0, m0), c1, m1), rest...);
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -168,7 +181,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         : "memory");
 }
 
-template <int EPI>
+// The epilogues in the arithmetic of O. For ExactOps every formula is the
+// reference's lincomb/add term for term (identity terms included, absent
+// operands skipped), so REFERENCE rounding reproduces its bits.
+template <int EPI, class O>
 __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, int64_t base,
                                               int row, int col, double c0, double c1) {
     const int64_t off = base + int64_t(row) * g.np + col;
@@ -179,56 +195,59 @@ __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, i
     };
     if constexpr (EPI == EPI_STORE) {
         st(0, c0, c1);
-    } else if constexpr (EPI == EPI_ADD) {
+    } else if constexpr (EPI == EPI_ADD) {  // add(b, P)
         const double2 b = ld(0);
-        st(0, c0 + b.x, c1 + b.y);
-    } else if constexpr (EPI == EPI_AL) {
+        st(0, O::add(b.x, c0), O::add(b.y, c1));
+    } else if constexpr (EPI == EPI_AL) {  // A9 = add(P, B4); L = add(B3, A9)
         const double2 b = ld(0), l = ld(1);
-        const double x0 = c0 + b.x, x1 = c1 + b.y;
+        const double x0 = O::add(c0, b.x), x1 = O::add(c1, b.y);
         st(0, x0, x1);
-        st(1, l.x + x0, l.y + x1);
-    } else if constexpr (EPI == EPI_T18_B) {
+        st(1, O::add(l.x, x0), O::add(l.y, x1));
+    } else if constexpr (EPI == EPI_T18_B) {  // lincomb(kT18A, {I,A,A2,A3}), lincomb(kT18B[j], {.., A6})
         const double2 a = ld(0), a2 = ld(1), a3 = ld(2);
-        st(0, c_t18a[1] * a.x + c_t18a[2] * a2.x + c_t18a[3] * a3.x,
-           c_t18a[1] * a.y + c_t18a[2] * a2.y + c_t18a[3] * a3.y);
+        st(0, lcx<O>(c_t18a[0], id0, c_t18a[1], a.x, c_t18a[2], a2.x, c_t18a[3], a3.x),
+           lcx<O>(c_t18a[0], id1, c_t18a[1], a.y, c_t18a[2], a2.y, c_t18a[3], a3.y));
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             st(1 + j,
-               c_t18b[j][0] * id0 + c_t18b[j][1] * a.x + c_t18b[j][2] * a2.x + c_t18b[j][3] * a3.x +
-                   c_t18b[j][4] * c0,
-               c_t18b[j][0] * id1 + c_t18b[j][1] * a.y + c_t18b[j][2] * a2.y + c_t18b[j][3] * a3.y +
-                   c_t18b[j][4] * c1);
+               lcx<O>(c_t18b[j][0], id0, c_t18b[j][1], a.x, c_t18b[j][2], a2.x, c_t18b[j][3], a3.x,
+                      c_t18b[j][4], c0),
+               lcx<O>(c_t18b[j][0], id1, c_t18b[j][1], a.y, c_t18b[j][2], a2.y, c_t18b[j][3], a3.y,
+                      c_t18b[j][4], c1));
     } else if constexpr (EPI == EPI_T12_B) {
         const double2 a = ld(0), a2 = ld(1);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            st(j, c_t12[0][j] * id0 + c_t12[1][j] * a.x + c_t12[2][j] * a2.x + c_t12[3][j] * c0,
-               c_t12[0][j] * id1 + c_t12[1][j] * a.y + c_t12[2][j] * a2.y + c_t12[3][j] * c1);
+            st(j, lcx<O>(c_t12[0][j], id0, c_t12[1][j], a.x, c_t12[2][j], a2.x, c_t12[3][j], c0),
+               lcx<O>(c_t12[0][j], id1, c_t12[1][j], a.y, c_t12[2][j], a2.y, c_t12[3][j], c1));
     } else if constexpr (EPI == EPI_T8_1) {
         const double2 a = ld(0);
         st(0, c0, c1);
-        st(1, T8C::x1 * a.x + T8C::x2 * c0, T8C::x1 * a.y + T8C::x2 * c1);
+        st(1, lcx<O>(T8C::x1, a.x, T8C::x2, c0), lcx<O>(T8C::x1, a.y, T8C::x2, c1));
     } else if constexpr (EPI == EPI_T8_2) {
         const double2 a = ld(0), a2 = ld(1);
-        st(0, T8C::x3 * a2.x + c0, T8C::x3 * a2.y + c1);
-        st(1, T8C::x4 * id0 + T8C::x5 * a.x + T8C::x6 * a2.x + T8C::x7 * c0,
-           T8C::x4 * id1 + T8C::x5 * a.y + T8C::x6 * a2.y + T8C::x7 * c1);
+        st(0, lcx<O>(T8C::x3, a2.x, 1.0, c0), lcx<O>(T8C::x3, a2.y, 1.0, c1));
+        st(1, lcx<O>(T8C::x4, id0, T8C::x5, a.x, T8C::x6, a2.x, T8C::x7, c0),
+           lcx<O>(T8C::x4, id1, T8C::x5, a.y, T8C::x6, a2.y, T8C::x7, c1));
     } else if constexpr (EPI == EPI_T8_3) {
         const double2 a = ld(0), a2 = ld(1);
-        st(0, T8C::y0 * id0 + T8C::y1 * a.x + T8C::y2 * a2.x + c0,
-           T8C::y0 * id1 + T8C::y1 * a.y + T8C::y2 * a2.y + c1);
-    } else if constexpr (EPI == EPI_T4_1) {
+        st(0, lcx<O>(T8C::y0, id0, T8C::y1, a.x, T8C::y2, a2.x, 1.0, c0),
+           lcx<O>(T8C::y0, id1, T8C::y1, a.y, T8C::y2, a2.y, 1.0, c1));
+    } else if constexpr (EPI == EPI_T4_1) {  // inner = lincomb({1, 1/4!}, {lincomb({1/2!, 1/3!}, {I, A}), A2})
         const double2 a = ld(0);
         st(0, c0, c1);
-        st(1, (kInvFact2 * id0 + kInvFact3 * a.x) + kInvFact4 * c0,
-           (kInvFact2 * id1 + kInvFact3 * a.y) + kInvFact4 * c1);
-    } else if constexpr (EPI == EPI_T4_2) {
+        st(1, lcx<O>(1.0, lcx<O>(kInvFact2, id0, kInvFact3, a.x), kInvFact4, c0),
+           lcx<O>(1.0, lcx<O>(kInvFact2, id1, kInvFact3, a.y), kInvFact4, c1));
+    } else if constexpr (EPI == EPI_T4_2) {  // add(f0, P), f0 = lincomb({1, 1}, {I, A})
         const double2 a = ld(0);
-        st(0, (id0 + a.x) + c0, (id1 + a.y) + c1);
-    } else if constexpr (EPI == EPI_T2) {
+        st(0, O::add(lcx<O>(1.0, id0, 1.0, a.x), c0), O::add(lcx<O>(1.0, id1, 1.0, a.y), c1));
+    } else if constexpr (EPI == EPI_T2) {  // lincomb({1, 1, 0.5}, {I, A, A2})
         const double2 a = ld(0);
-        st(0, (id0 + a.x) + 0.5 * c0, (id1 + a.y) + 0.5 * c1);
+        st(0, lcx<O>(1.0, id0, 1.0, a.x, 0.5, c0), lcx<O>(1.0, id1, 1.0, a.y, 0.5, c1));
     } else if constexpr (EPI == EPI_PS_B) {
+        // rows of coefficients over {I, in0, in1, in2, c}; absent operands and a
+        // zero coefficient of c contribute no term (the reference's lincombs
+        // have no such term)
         const double2 z = make_double2(0.0, 0.0);
         const double2 a = g.in[0] ? ld(0) : z, a2 = g.in[1] ? ld(1) : z, a3 = g.in[2] ? ld(2) : z;
         if (g.store_c) st(0, c0, c1);
@@ -236,10 +255,77 @@ __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, i
         for (int j = 0; j < 4; ++j) {
             if (j >= g.nlc) break;
             const double* k = g.lc[j];
-            st(1 + j, k[0] * id0 + k[1] * a.x + k[2] * a2.x + k[3] * a3.x + k[4] * c0,
-               k[0] * id1 + k[1] * a.y + k[2] * a2.y + k[3] * a3.y + k[4] * c1);
+            double r0 = O::mul(k[0], id0), r1 = O::mul(k[0], id1);
+            if (g.in[0]) r0 = O::mac(r0, k[1], a.x), r1 = O::mac(r1, k[1], a.y);
+            if (g.in[1]) r0 = O::mac(r0, k[2], a2.x), r1 = O::mac(r1, k[2], a2.y);
+            if (g.in[2]) r0 = O::mac(r0, k[3], a3.x), r1 = O::mac(r1, k[3], a3.y);
+            if (k[4] != 0.0) r0 = O::mac(r0, k[4], c0), r1 = O::mac(r1, k[4], c1);
+            st(1 + j, r0, r1);
         }
     }
+}
+
+// Reference-rounded batched product (REFERENCE policy, n > 64): every output
+// is 0.0 + x_i0*y_0j + x_i1*y_1j + ... over k < n in order, each multiply and
+// add rounded (kernels.cpp:16-27), i.e. the reference's i-k-j loop bit for
+// bit. 64 x 64 CTA tiles, 256 threads of 4 x 4 outputs (16 independent
+// chains each), k-tiles of 16 double-buffered in shared memory.
+constexpr int XB = 64, XK = 16, XLDA = XK + 1, XLDB = XB + 2;
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
+    __shared__ double sa[2][XB][XLDA];
+    __shared__ __align__(16) double sb[2][XK][XLDB];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int32_t entry = g.list[blockIdx.z];
+    const int64_t mat = entry & 0x7fffffff;
+    double* out0 = entry < 0 ? g.final_out : g.out[0];
+    const int64_t base = mat * g.mstride;
+    const double* X = g.X + base;
+    const double* Y = g.Y + base;
+    const int m0 = blockIdx.y * XB, n0 = blockIdx.x * XB;
+    const int ktiles = (g.n + XK - 1) / XK;
+    auto load = [&](int s, int kt) {
+        const int k0 = kt * XK;
+        for (int e = tid; e < XB * XK; e += 256) {
+            const int r = e / XK, k = e % XK;
+            sa[s][r][k] = (k0 + k < g.n) ? X[int64_t(m0 + r) * g.np + k0 + k] : 0.0;
+        }
+        for (int e = tid; e < XK * XB; e += 256) {
+            const int k = e / XB, c = e % XB;
+            sb[s][k][c] = (k0 + k < g.n) ? Y[int64_t(k0 + k) * g.np + n0 + c] : 0.0;
+        }
+    };
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    load(0, 0);
+    __syncthreads();
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt & 1;
+        if (kt + 1 < ktiles) load(s ^ 1, kt + 1);
+        const int kend = min(XK, g.n - kt * XK);  // never a padded term
+        for (int k = 0; k < kend; ++k) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = sa[s][4 * ty + i][k];
+            const double2 b01 = *reinterpret_cast<const double2*>(&sb[s][k][4 * tx]);
+            const double2 b23 = *reinterpret_cast<const double2*>(&sb[s][k][4 * tx + 2]);
+            b[0] = b01.x, b[1] = b01.y, b[2] = b23.x, b[3] = b23.y;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; j += 2)
+            epilogue_pair<EPI, ExactOps>(g, out0, base, m0 + 4 * ty + i, n0 + 4 * tx + j, acc[i][j],
+                                         acc[i][j + 1]);
 }
 
 template <int EPI>
@@ -373,8 +459,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j)
-            epilogue_pair<EPI>(g, out0, base, m0 + wm * WM + i * 8 + r, n0 + wn * WN + j * 8 + 2 * q,
-                               acc[i][j][0], acc[i][j][1]);
+            epilogue_pair<EPI, FastOps>(g, out0, base, m0 + wm * WM + i * 8 + r,
+                                        n0 + wn * WN + j * 8 + 2 * q, acc[i][j][0], acc[i][j][1]);
 }
 
 // ---- prologue / epilogue kernels -------------------------------------------
@@ -517,6 +603,7 @@ bool make_x_map(CUtensorMap* map, const double* base, int np, int64_t batch) {
 }
 
 thread_local int64_t g_map_batch = 0;  // matrices per workspace buffer of the current call
+thread_local int g_exact_n = 0;         // > 0: products in reference rounding over k < g_exact_n
 
 template <int EPI>
 int gemm(const double* X, const double* Y, std::initializer_list<const double*> in,
@@ -551,6 +638,17 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
     g.list = d_list;
     g.np = np;
     g.mstride = int64_t(np) * np;
+    g.n = g_exact_n > 0 ? g_exact_n : np;
+    if (g_exact_n > 0) {  // REFERENCE rounding: the k-ordered DMUL+DADD product
+        for (int z0 = 0; z0 < count; z0 += 65535) {
+            const int zc = std::min(count - z0, 65535);
+            g.list = d_list + z0;
+            gemm_exact_kernel<EPI><<<dim3(np / XB, np / XB, zc), 256, 0, st>>>(g);
+            launches->fetch_add(1, std::memory_order_relaxed);
+        }
+        LCUDA(cudaGetLastError());
+        return MEXP_OK;
+    }
     CUtensorMap tmx{};
 #if MEXP_GEMM_TMA == 2
     if (!make_x_map(&tmx, X, np, g_map_batch)) {
@@ -587,10 +685,18 @@ Workspace& workspace() {
 const char* large_last_error() { return g_err.c_str(); }
 
 int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user, int n,
-                   int64_t batch, int acc_arg, cudaStream_t st, std::atomic<uint64_t>* launches) {
+                   int64_t batch, int acc_arg, int rounding, cudaStream_t st,
+                   std::atomic<uint64_t>* launches) {
     const int np = (n + BM - 1) / BM * BM;
     const int64_t mat = int64_t(np) * np;
     const bool pade = (acc_arg >> 4) == MEXP_FAMILY_PADE || (acc_arg >> 4) == kFamilyPadeReference;
+    // REFERENCE rounding: every product k-ordered and every lincomb literal
+    // (the Pade LU has no reference-rounded variant)
+    if (rounding == MEXP_ROUND_REFERENCE && pade) return MEXP_ERR_UNSUPPORTED;
+    struct ExactScope {
+        explicit ExactScope(int v) { g_exact_n = v; }
+        ~ExactScope() { g_exact_n = 0; }
+    } exact_scope(rounding == MEXP_ROUND_REFERENCE ? n : 0);
     constexpr int kMaxBuffers = 8;
     const int kBuffers = pade ? 8 : 6;  // r26 keeps A, A2, A4, A6, two lincombs, V and u''
     // workspace: kBuffers padded matrices per batch entry + per-matrix scratch
@@ -994,7 +1100,10 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
 
 int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaStream_t st,
                   std::atomic<uint64_t>* launches) {
-    if (rounding == MEXP_ROUND_REFERENCE) return MEXP_ERR_UNSUPPORTED;
+    struct ExactScope {
+        explicit ExactScope(int v) { g_exact_n = v; }
+        ~ExactScope() { g_exact_n = 0; }
+    } exact_scope(rounding == MEXP_ROUND_REFERENCE ? n : 0);
     const int np = (n + BM - 1) / BM * BM;
     const int64_t mat = int64_t(np) * np;
     AsyncBuffer w_buf(st), list_buf(st), sel0_buf(st);

@@ -12,9 +12,12 @@
 
 namespace mexp_b200 {
 
-// acc_arg = mexp_accuracy | mexp_family << 4
+// acc_arg = mexp_accuracy | mexp_family << 4; rounding: MEXP_ROUND_REFERENCE
+// runs every product and lincomb in the reference's arithmetic (bit-identical
+// e^A; not for the Pade family), anything else the DMMA path
 int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel, int n,
-                   int64_t batch, int acc_arg, cudaStream_t st, std::atomic<uint64_t>* launches);
+                   int64_t batch, int acc_arg, int rounding, cudaStream_t st,
+                   std::atomic<uint64_t>* launches);
 
 // X <- X^(2^s), in place, for `batch` n x n fp64 matrices.
 int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaStream_t st,

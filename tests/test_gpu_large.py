@@ -42,8 +42,8 @@ def test_large_n_errors_and_reference_rounding(cuda):
     assert list(sel["status"]) == [0, 1, 2]
     assert np.array_equal(out[0], np.eye(100))
     assert np.isnan(out[1]).all() and np.isnan(out[2]).all()
-    with pytest.raises(ValueError, match="unsupported"):
-        mx.expm_batched_host(a[:1], rounding=mx.ROUND_REFERENCE)
+    out_r, sel_r, _ = mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE, raise_on_error=False)
+    assert list(sel_r["status"]) == [0, 1, 2] and np.array_equal(out_r[0], np.eye(100))
 
 
 def test_cfg4_subset(cuda, oracle):
@@ -124,3 +124,34 @@ def test_large_n_batch_beyond_grid_y(cuda, oracle):
     assert rel_fro(out[idx], ref.out).max() <= 50 * n * U53
     zero = np.setdiff1d(np.arange(batch), np.append(idx, 123))[::997]
     assert all(np.array_equal(out[i], np.eye(n)) for i in zero)
+
+
+@pytest.mark.parametrize("n", [65, 96, 130, 200])
+def test_large_n_reference_rounding_bitwise(cuda, oracle, n):
+    """REFERENCE rounding beyond n = 64: k-ordered DMUL+DADD products over the
+    true n (never a padded term) and literal lincombs -> e^A bit-identical to
+    the reference for every degree and s, both Taylor families."""
+    rng = np.random.default_rng(5000 + n)
+    norms = np.array([1e-17, 1e-9, 1e-4, 5e-3, 0.03, 0.2, 0.9, 2.0, 7.0, 30.0, 100.0])
+    a = rng.uniform(-1, 1, (len(norms), n, n))
+    a *= (norms / workloads.one_norm_batched(a))[:, None, None]
+    for family in (0, 1):
+        ref = oracle.expm_batch(a, family=family)
+        out, sel, st = mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE, family=mx.Family(family))
+        assert st == mx.OK
+        assert np.array_equal(sel["degree"], ref.degree) and np.array_equal(sel["s"], ref.s)
+        assert np.array_equal(out.view(np.uint64), ref.out.view(np.uint64)), (n, family)
+
+
+def test_large_n_reference_rounding_cfg4_slice(cuda, oracle):
+    a = workloads.generate("cfg4", 0, 3)
+    ref = oracle.expm_batch(a)
+    out, sel, st = mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE)
+    assert st == mx.OK and np.array_equal(sel["s"], ref.s)
+    assert np.array_equal(out.view(np.uint64), ref.out.view(np.uint64))
+
+
+def test_large_n_reference_rounding_refuses_pade(cuda):
+    a = np.zeros((1, 70, 70))
+    with pytest.raises(ValueError, match="unsupported"):
+        mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE, family=mx.Family.PadeDiagonal)
