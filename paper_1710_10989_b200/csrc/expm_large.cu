@@ -270,10 +270,18 @@ __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, i
 // add rounded (kernels.cpp:16-27), i.e. the reference's i-k-j loop bit for
 // bit. 64 x 64 CTA tiles, 256 threads of 4 x 4 outputs (16 independent
 // chains each), k-tiles of 16 double-buffered in shared memory.
-constexpr int XB = 64, XK = 16, XLDA = XK + 1, XLDB = XB + 2;
+constexpr int XB = 64, XK = 16, XLDA = XK + 2, XLDB = XB + 2;  // rows 16-byte aligned
+
+// 16-byte async copy of the first `bytes` (0, 8 or 16) of src, zero-filling the rest
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, int bytes) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(bytes)
+                 : "memory");
+}
+
 template <int EPI>
 __global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
-    __shared__ double sa[2][XB][XLDA];
+    __shared__ __align__(16) double sa[2][XB][XLDA];
     __shared__ __align__(16) double sb[2][XK][XLDB];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int32_t entry = g.list[blockIdx.z];
@@ -284,16 +292,20 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
     const double* Y = g.Y + base;
     const int m0 = blockIdx.y * XB, n0 = blockIdx.x * XB;
     const int ktiles = (g.n + XK - 1) / XK;
+    // k >= n is zero-filled (and never summed: the k loop stops at n)
     auto load = [&](int s, int kt) {
         const int k0 = kt * XK;
-        for (int e = tid; e < XB * XK; e += 256) {
-            const int r = e / XK, k = e % XK;
-            sa[s][r][k] = (k0 + k < g.n) ? X[int64_t(m0 + r) * g.np + k0 + k] : 0.0;
+        for (int e = tid; e < XB * XK / 2; e += 256) {
+            const int r = e / (XK / 2), k = (e % (XK / 2)) * 2;
+            const int valid = min(max(g.n - (k0 + k), 0), 2);
+            cp_async16_zfill(&sa[s][r][k], X + int64_t(m0 + r) * g.np + min(k0 + k, g.np - 2), 8 * valid);
         }
-        for (int e = tid; e < XK * XB; e += 256) {
-            const int k = e / XB, c = e % XB;
-            sb[s][k][c] = (k0 + k < g.n) ? Y[int64_t(k0 + k) * g.np + n0 + c] : 0.0;
+        for (int e = tid; e < XK * XB / 2; e += 256) {
+            const int k = e / (XB / 2), c = (e % (XB / 2)) * 2;
+            const bool ok = k0 + k < g.n;
+            cp_async16_zfill(&sb[s][k][c], Y + int64_t(ok ? k0 + k : 0) * g.np + n0 + c, ok ? 16 : 0);
         }
+        cp_commit();
     };
     double acc[4][4];
 #pragma unroll
@@ -301,10 +313,15 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
     load(0, 0);
-    __syncthreads();
     for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt & 1;
-        if (kt + 1 < ktiles) load(s ^ 1, kt + 1);
+        if (kt + 1 < ktiles) {
+            load(s ^ 1, kt + 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
         const int kend = min(XK, g.n - kt * XK);  // never a padded term
         for (int k = 0; k < kend; ++k) {
             double a[4], b[4];
