@@ -65,8 +65,10 @@ typedef enum { MEXP_F64 = 0, MEXP_F32 = 1 } mexp_dtype;
  *              (kernels.cpp:16-37, -ffp-contract=off) -> e^A bit-identical
  *              to the reference;
  *   FAST:      FP64 tensor-core DMMA products, FMA combinations;
- *   AUTO:      FAST, except matrices with s >= 6 squarings, whose rounding
- *              differences the squarings amplify, run REFERENCE.
+ *   AUTO:      FAST, except matrices with s >= 3 + floor(log2 n) squarings
+ *              (n >= 8; every matrix for n < 8), whose rounding differences
+ *              the squarings amplify: those run REFERENCE, all but their
+ *              last 2 squarings (the 8x8 kernel).
  * For n > 64, REFERENCE runs the products as k-ordered DMUL+DADD chains on
  * the CUDA cores and the lincombs literally (bit-identical for TaylorNew and
  * TaylorPS; the Pade LU is DMMA-only and refuses it), AUTO and FAST the
