@@ -258,21 +258,32 @@ int64_t cluster_max_batch() {
     return v;
 }
 
-int launch_cluster64(const double* a, double* out, mexp_selection* sel, int64_t batch, int accuracy,
-                     int rounding, int smin, cudaStream_t st) {
+template <int kFamily>
+int launch_cluster64_family(const double* a, double* out, mexp_selection* sel, int64_t batch,
+                            int accuracy, int rounding, int smin, cudaStream_t st) {
     using G = ClusterGroup64;
     const size_t smem = size_t(G::SMEM_DOUBLES) * sizeof(double);
     static bool attr = [&] {
-        cudaFuncSetAttribute(expm64_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(expm64_cluster_kernel<kFamily>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(smem));
         return true;
     }();
     (void)attr;
     const int grid = int(batch) * kClusterCtas;
-    expm64_cluster_kernel<<<grid, G::THREADS, smem, st>>>(a, out, sel, batch, accuracy, rounding, smin);
+    expm64_cluster_kernel<kFamily><<<grid, G::THREADS, smem, st>>>(a, out, sel, batch, accuracy,
+                                                                   rounding, smin);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());
     return MEXP_OK;
+}
+
+int launch_cluster64(const double* a, double* out, mexp_selection* sel, int64_t batch, int accuracy,
+                     int rounding, int smin, cudaStream_t st) {
+    if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)
+        return launch_cluster64_family<MEXP_FAMILY_TAYLOR_PS>(a, out, sel, batch, accuracy, rounding,
+                                                              smin, st);
+    return launch_cluster64_family<MEXP_FAMILY_TAYLOR_NEW>(a, out, sel, batch, accuracy, rounding,
+                                                           smin, st);
 }
 
 // `accuracy` here and below is the kernels' acc_arg (mexp_accuracy | family << 4)

@@ -260,6 +260,9 @@ struct ClusterGroup64 {
 };
 
 // One cluster of kClusterCtas CTAs per matrix; clusters stride over the batch.
+// one instantiation per family: a smaller kernel image (its first launch after
+// an L2 flush fetches every instruction line from HBM)
+template <int kFamily>
 __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(ClusterGroup64::THREADS, 1)
     expm64_cluster_kernel(const double* __restrict__ a, double* __restrict__ out,
                           mexp_selection* __restrict__ sel, int64_t batch, int acc_arg,
@@ -270,7 +273,8 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(ClusterGr
     constexpr int N = G::N, LD = G::LD;
     extern __shared__ __align__(16) double smem[];
     cg::cluster_group cluster = cg::this_cluster();
-    const int accuracy = acc_arg & 15, family = acc_arg >> 4;
+    const int accuracy = acc_arg & 15;
+    constexpr int family = kFamily;
     G g;
     g.rank = int(cluster.block_rank());
     g.bi = g.rank >> 1;
@@ -368,13 +372,8 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(ClusterGr
         } else {
             const bool exact = rounding == MEXP_ROUND_REFERENCE ||
                                (rounding == MEXP_ROUND_AUTO && sl.s >= exact_s_min);
-            if (family == MEXP_FAMILY_TAYLOR_PS) {
-                X = exact ? run_expm<ExactOps, MEXP_FAMILY_TAYLOR_PS>(g, A, sl.degree, sl.s)
-                          : run_expm<FastOps, MEXP_FAMILY_TAYLOR_PS>(g, A, sl.degree, sl.s);
-            } else {
-                X = exact ? run_expm<ExactOps>(g, A, sl.degree, sl.s)
-                          : run_expm<FastOps>(g, A, sl.degree, sl.s);
-            }
+            X = exact ? run_expm<ExactOps, family>(g, A, sl.degree, sl.s)
+                      : run_expm<FastOps, family>(g, A, sl.degree, sl.s);
         }
         CTRACE("expm_done");
         g.store_global(out + m * int64_t(N) * N, X);
