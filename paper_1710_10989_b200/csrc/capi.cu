@@ -133,11 +133,11 @@ int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t 
     return MEXP_OK;
 }
 
-// Ring of device counters for kernels that hand out work dynamically. Slots
-// start zeroed; the kernel using slot i zeroes slot i + kSlots/2, which its
-// next user reaches 2048 launches later -- no memset per launch (at most
-// 2048 launches of a device in flight at once).
-int next_ticket(unsigned long long** out, unsigned long long** clear) {
+// Ring of {work counter, finished-CTA counter} slots for kernels that hand out
+// work dynamically: concurrent launches (other streams) get distinct slots;
+// each kernel leaves its slot zeroed (release_ticket), so no memset per launch
+// and CUDA-graph replays of a captured launch find their slot ready.
+int next_ticket(unsigned long long** out) {
     constexpr int kSlots = 4096;
     static unsigned long long* ring[16] = {};
     static std::atomic<uint32_t> next[16];
@@ -149,14 +149,13 @@ int next_ticket(unsigned long long** out, unsigned long long** clear) {
         std::lock_guard<std::mutex> lock(mu);
         if (!ring[dev]) {
             unsigned long long* r = nullptr;
-            MEXP_CUDA(cudaMalloc(&r, sizeof(unsigned long long) * kSlots));
-            MEXP_CUDA(cudaMemset(r, 0, sizeof(unsigned long long) * kSlots));
+            MEXP_CUDA(cudaMalloc(&r, 2 * sizeof(unsigned long long) * kSlots));
+            MEXP_CUDA(cudaMemset(r, 0, 2 * sizeof(unsigned long long) * kSlots));
             ring[dev] = r;
         }
     }
     const uint32_t i = next[dev].fetch_add(1) % kSlots;
-    *out = ring[dev] + i;
-    *clear = ring[dev] + (i + kSlots / 2) % kSlots;
+    *out = ring[dev] + 2 * i;
     return MEXP_OK;
 }
 
@@ -224,17 +223,16 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
     const int grid = int(want < cap ? want : cap);
     // work ticket for the dynamically distributed rounds: a slot of a
     // persistent per-device ring, reset in stream order
-    unsigned long long *ticket = nullptr, *ticket_clear = nullptr;
+    unsigned long long* ticket = nullptr;
     {
-        int r = next_ticket(&ticket, &ticket_clear);
+        int r = next_ticket(&ticket);
         if (r != MEXP_OK) return r;
     }
     // AUTO: the last fast_tail() squarings of the reference-rounded matrices
     // run with FMA/DMMA rounding (expm_small.cuh run_expm)
     const int rounding_arg = rounding == MEXP_ROUND_AUTO ? (rounding | (fast_tail() << 8)) : rounding;
     kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding_arg, smin,
-                                                 work, defer ? work + batch : nullptr, ticket,
-                                                 ticket_clear);
+                                                 work, defer ? work + batch : nullptr, ticket);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());
     if (defer) {
@@ -310,11 +308,11 @@ int launch_pade8(const double* a, double* out, mexp_selection* sel, int64_t batc
     const int64_t cap = int64_t(blocks_per_sm) * num_sms();
     const int64_t want = (batch + 4 * kN8WarpsPerBlock - 1) / (4 * kN8WarpsPerBlock);
     const int grid = int(want < cap ? want : cap);
-    unsigned long long *ticket = nullptr, *ticket_clear = nullptr;
-    const int r = next_ticket(&ticket, &ticket_clear);
+    unsigned long long* ticket = nullptr;
+    const int r = next_ticket(&ticket);
     if (r != MEXP_OK) return r;
     expm8_pade_kernel<8><<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding,
-                                                                 smin, ticket, ticket_clear);
+                                                                 smin, ticket);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());
     return MEXP_OK;

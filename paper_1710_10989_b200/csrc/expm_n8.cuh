@@ -172,6 +172,21 @@ struct Group8T {
     }
 };
 
+// The work ticket {round counter, finished CTAs}: the last CTA to finish
+// zeroes both, so the slot is ready for the next launch -- including the
+// replay of a CUDA graph that captured this one.
+__device__ __forceinline__ void release_ticket(unsigned long long* ticket) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ticket + 1, 1ull) == gridDim.x - 1ull) {
+            ticket[0] = 0ull;
+            ticket[1] = 0ull;
+            __threadfence();
+        }
+    }
+}
+
 constexpr int kN8WarpsPerBlock = 4;  // 128-thread blocks
 constexpr int kN8Mpw = 4;            // matrices per warp per round
 
@@ -189,12 +204,10 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     expm8_f64_kernel(const double* __restrict__ a, double* __restrict__ out,
                      mexp_selection* __restrict__ sel, int64_t batch, int acc_arg, int rounding_arg,
                      int exact_s_min, int32_t* __restrict__ worklist, int32_t* __restrict__ wcount,
-                     unsigned long long* __restrict__ ticket,
-                     unsigned long long* __restrict__ ticket_clear) {
+                     unsigned long long* __restrict__ ticket) {
     using Group8 = Group8T<kSplit>;
     using F = typename Group8::Frag;
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
-    if (blockIdx.x == 0 && threadIdx.x == 0) *ticket_clear = 0ull;  // see capi.cu next_ticket
     // rounding policy in the low byte; AUTO's fast squaring tail above it
     const int rounding = rounding_arg & 0xff, fast_tail = rounding_arg >> 8;
     // accuracy in the low 4 bits (mexp_accuracy); the family is kFamily
@@ -310,6 +323,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
         if (lane == 0) t = atomicAdd(ticket, 1ull);
         rd = rstride + int64_t(__shfl_sync(0xffffffffu, t, 0));
     }
+    release_ticket(ticket);
 }
 
 // Reference-rounded 8x8 expm for the matrices listed in worklist[0, *wcount)

@@ -20,12 +20,10 @@ template <int kMinBlocks = 8>
 __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     expm8_pade_kernel(const double* __restrict__ a, double* __restrict__ out,
                       mexp_selection* __restrict__ sel, int64_t batch, int acc_arg, int rounding,
-                      int exact_s_min, unsigned long long* __restrict__ ticket,
-                      unsigned long long* __restrict__ ticket_clear) {
+                      int exact_s_min, unsigned long long* __restrict__ ticket) {
     using Group8 = Group8T<false>;
     using F = Group8::Frag;
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
-    if (blockIdx.x == 0 && threadIdx.x == 0) *ticket_clear = 0ull;  // see capi.cu next_ticket
     const int accuracy = acc_arg & 15, family = acc_arg >> 4;  // Pade, or reference_expm's rule
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -217,6 +215,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
         if (lane == 0) t = atomicAdd(ticket, 1ull);
         rd = rstride + int64_t(__shfl_sync(0xffffffffu, t, 0));
     }
+    release_ticket(ticket);
 }
 
 }  // namespace mexp_b200

@@ -274,3 +274,26 @@ def test_cluster_and_cta_paths_agree(cuda, oracle, batch):
                                              raise_on_error=False)
     ref_ps = oracle.expm_batch(a, family=1)
     assert np.array_equal(bits(out_ps[ok]), bits(ref_ps.out[ok]))
+
+
+@pytest.mark.parametrize("family", [mx.Family.TaylorNew, mx.Family.PadeDiagonal])
+def test_graph_capture_and_replay(cuda, oracle, family):
+    """A captured mexp_expm_batched launch (the 8x8 kernels hand out work
+    through a device ticket) gives the same bits on every replay of the graph."""
+    import torch
+    a_np = workloads.generate("cfg2", 500, 20000)
+    a = torch.from_numpy(a_np).cuda()
+    out = torch.empty_like(a)
+    sel = torch.empty(a.shape[0] * 16, dtype=torch.uint8, device="cuda")
+    mx.expm_batched(a, out, sel, rounding=mx.ROUND_REFERENCE, family=family)  # warm
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        mx.expm_batched(a, out, sel, rounding=mx.ROUND_REFERENCE, family=family,
+                        stream=torch.cuda.current_stream())
+    ref = oracle.expm_batch(a_np, family=int(family))
+    for _ in range(3):
+        out.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(out.cpu().numpy()), bits(ref.out))
