@@ -176,6 +176,7 @@ struct Group8T {
 // zeroes both, so the slot is ready for the next launch -- including the
 // replay of a CUDA graph that captured this one.
 __device__ __forceinline__ void release_ticket(unsigned long long* ticket) {
+    __syncwarp();
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
