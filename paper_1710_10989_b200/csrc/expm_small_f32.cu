@@ -128,12 +128,53 @@ struct GroupF32 {
             }
         }
     }
+    // Operand buffers. TC == 8 shapes (n = 32, 64): both operands row-major,
+    // unpadded, with the 16-byte chunk c of row i stored at chunk
+    // c ^ swz(i) (swz below); a lane's 8 columns are chunks tj and tj + GC.
+    // Per product the lane reads X[its 4 rows][4 k] as four float4 and Y[k][its
+    // 8 columns] as two float4 per k: the same vector loads as a transposed X,
+    // but no transposing scalar stores, and a squaring (X == Y) stores once.
+    // The swizzle makes all three access patterns bank-conflict-free: the X
+    // chunk loads (rows 4ti + r over the warp's ti), the Y row loads and the
+    // fragment stores (8 lanes per phase over 8 distinct bank quads).
+#ifndef MEXP_F32_SWZ
+#define MEXP_F32_SWZ 1
+#endif
+#ifndef MEXP_F32_UNROLL
+#define MEXP_F32_UNROLL 4
+#endif
+    static constexpr int kUnrollQ = MEXP_F32_UNROLL;
+    static constexpr bool kSwz = MEXP_F32_SWZ && (TC == 8 && TR == 4);
+    __device__ __forceinline__ static int swz(int i) {
+        const int t = (i >> 2) & 7;  // 8 row quads -> chunk xor {0,4,1,5,2,6,3,7}
+        return ((t & 1) << 2) | (t >> 1);
+    }
+    __device__ __forceinline__ static int at(int i, int j) {  // element (i, j) of a buffer
+        if constexpr (kSwz)
+            return i * N + 4 * ((j >> 2) ^ swz(i)) + (j & 3);
+        else
+            return i * LD + j;
+    }
+
     __device__ __forceinline__ void store_rows(float* s, const Frag& f) const {
+        if constexpr (kSwz) {
 #pragma unroll
-        for (int r = 0; r < TR; ++r)
+            for (int r = 0; r < TR; ++r) {
+                const int i = row_of(r);
 #pragma unroll
-            for (int cp = 0; cp < TP; ++cp)
-                *reinterpret_cast<float2*>(s + row_of(r) * LD + col_of(2 * cp)) = f.v[r * TP + cp];
+                for (int h = 0; h < 2; ++h) {
+                    const float2 a = f.v[r * TP + 2 * h], b = f.v[r * TP + 2 * h + 1];
+                    *reinterpret_cast<float4*>(s + i * N + 4 * ((tj + h * GC) ^ swz(i))) =
+                        make_float4(a.x, a.y, b.x, b.y);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < TR; ++r)
+#pragma unroll
+                for (int cp = 0; cp < TP; ++cp)
+                    *reinterpret_cast<float2*>(s + row_of(r) * LD + col_of(2 * cp)) = f.v[r * TP + cp];
+        }
     }
     __device__ __forceinline__ void store_cols(float* s, const Frag& f) const {
 #pragma unroll
@@ -159,41 +200,116 @@ struct GroupF32 {
     }
 
     template <class Ops>
-    __device__ __forceinline__ Frag mm(const Frag& X, const Frag& Y, bool) const {
-        return mm_impl(X, Y, nullptr);
+    __device__ __forceinline__ Frag mm(const Frag& X, const Frag& Y, bool same) const {
+        return mm_impl(X, Y, nullptr, same);
     }
     template <class Ops>
-    __device__ __forceinline__ Frag mm_add(const Frag& X, const Frag& Y, bool,
+    __device__ __forceinline__ Frag mm_add(const Frag& X, const Frag& Y, bool same,
                                            const Frag& B) const {
-        return mm_impl(X, Y, &B);
+        return mm_impl(X, Y, &B, same);
     }
     template <class Ops>
     __device__ __forceinline__ Frag sq_first(const Frag& A) const {
-        return mm_impl(A, A, nullptr);
+        return mm_impl(A, A, nullptr, true);
     }
-    __device__ __forceinline__ Frag mm_impl(const Frag& X, const Frag& Y, const Frag* init) const {
-        sync();
-        store_cols(sxt, X);
-        store_rows(sy, Y);
-        sync();
+#ifndef MEXP_F32_NOINLINE
+#define MEXP_F32_NOINLINE 1
+#endif
+#if MEXP_F32_NOINLINE
+#define MEXP_F32_KLOOP_ATTR __noinline__
+#else
+#define MEXP_F32_KLOOP_ATTR __forceinline__
+#endif
+    // C += X * Y over the swizzled buffers: pxl = the lane's first X row,
+    // sxl = its chunk xor. One out-of-line copy serves every product of the
+    // schemes and squarings (inlined copies overflow the instruction cache).
+    __device__ MEXP_F32_KLOOP_ATTR static Frag kloop(const float* pxl, const float* sy, int sxl, int tj,
+                                                     Frag C) {
+            // software-pipelined k loop: the next k-chunk of X and the next row
+            // of Y are loaded while the current ones feed the FFMA2s. All
+            // swizzles are per chunk q (Y) or per lane (X): addresses are a
+            // base pointer plus immediates.
+            constexpr int C1 = 4 * GC;           // offset of the lane's 2nd column chunk
+            float4 xc[TR], yc[2];
+#pragma unroll
+            for (int r = 0; r < TR; ++r) xc[r] = *reinterpret_cast<const float4*>(pxl + r * N + 4 * sxl);
+            int c0 = 4 * tj;  // chunk 0's swizzle is 0
+            yc[0] = *reinterpret_cast<const float4*>(sy + c0);
+            yc[1] = *reinterpret_cast<const float4*>(sy + (c0 ^ C1));
+#pragma unroll kUnrollQ
+            for (int q = 0; q < N / 4; ++q) {
+                const int qn = (q + 1) & (N / 4 - 1);
+                const float* xq = pxl + 4 * (qn ^ sxl);
+                float4 xn[TR];
+#pragma unroll
+                for (int r = 0; r < TR; ++r) xn[r] = *reinterpret_cast<const float4*>(xq + r * N);
+                const float* yq = sy + 4 * q * N + c0;
+                const int c0n = 4 * (tj ^ swz(4 * qn));
+                const float* yqn = sy + 4 * qn * N;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    float4 yn[2];
+                    if (kk < 3) {
+                        yn[0] = *reinterpret_cast<const float4*>(yq + (kk + 1) * N);
+                        yn[1] = *reinterpret_cast<const float4*>(yq + (kk + 1) * N + ((c0 ^ C1) - c0));
+                    } else {
+                        yn[0] = *reinterpret_cast<const float4*>(yqn + c0n);
+                        yn[1] = *reinterpret_cast<const float4*>(yqn + (c0n ^ C1));
+                    }
+#pragma unroll
+                    for (int r = 0; r < TR; ++r) {
+                        const float a = kk == 0 ? xc[r].x : kk == 1 ? xc[r].y : kk == 2 ? xc[r].z : xc[r].w;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            C.v[r * TP + 2 * h] = __ffma2_rn(make_float2(a, a), make_float2(yc[h].x, yc[h].y),
+                                                             C.v[r * TP + 2 * h]);
+                            C.v[r * TP + 2 * h + 1] = __ffma2_rn(make_float2(a, a), make_float2(yc[h].z, yc[h].w),
+                                                                 C.v[r * TP + 2 * h + 1]);
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) yc[h] = yn[h];
+                }
+#pragma unroll
+                for (int r = 0; r < TR; ++r) xc[r] = xn[r];
+                c0 = c0n;
+            }
+        return C;
+    }
+
+    __device__ __forceinline__ Frag mm_impl(const Frag& X, const Frag& Y, const Frag* init,
+                                            bool same) const {
         Frag C;
 #pragma unroll
         for (int e = 0; e < K; ++e) C.v[e] = init ? init->v[e] : make_float2(0.f, 0.f);
+        if constexpr (kSwz) {
+            sync();
+            store_rows(sy, Y);
+            if (!same) store_rows(sxt, X);
+            sync();
+            const float* px = same ? sy : sxt;
+            C = kloop(px + 4 * ti * N, sy, swz(4 * ti), tj, C);
+        } else {
+            sync();
+            store_cols(sxt, X);
+            store_rows(sy, Y);
+            sync();
 #pragma unroll 2
-        for (int k = 0; k < N; ++k) {
-            float a[TR];
-            float2 b[TP];
-            const float* xa = sxt + k * LD + ti * TR;
+            for (int k = 0; k < N; ++k) {
+                float a[TR];
+                float2 b[TP];
+                const float* xa = sxt + k * LD + ti * TR;
 #pragma unroll
-            for (int r = 0; r < TR; ++r) a[r] = xa[r];
-            const float* yb = sy + k * LD;
+                for (int r = 0; r < TR; ++r) a[r] = xa[r];
+                const float* yb = sy + k * LD;
 #pragma unroll
-            for (int cp = 0; cp < TP; ++cp) b[cp] = *reinterpret_cast<const float2*>(yb + col_of(2 * cp));
+                for (int cp = 0; cp < TP; ++cp) b[cp] = *reinterpret_cast<const float2*>(yb + col_of(2 * cp));
 #pragma unroll
-            for (int r = 0; r < TR; ++r)
+                for (int r = 0; r < TR; ++r)
 #pragma unroll
-                for (int cp = 0; cp < TP; ++cp)
-                    C.v[r * TP + cp] = __ffma2_rn(make_float2(a[r], a[r]), b[cp], C.v[r * TP + cp]);
+                    for (int cp = 0; cp < TP; ++cp)
+                        C.v[r * TP + cp] = __ffma2_rn(make_float2(a[r], a[r]), b[cp], C.v[r * TP + cp]);
+            }
         }
         return C;
     }
@@ -236,7 +352,7 @@ __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
         double colsum = 0.0;
         for (int j = g.tid; j < N; j += G::THREADS) {
             double s = 0.0;
-            for (int i = 0; i < N; ++i) s = __dadd_rn(s, fabs(double(g.sy[i * G::LD + j])));
+            for (int i = 0; i < N; ++i) s = __dadd_rn(s, fabs(double(g.sy[G::at(i, j)])));
             colsum = fmax(colsum, s);
         }
         const bool wfin = __all_sync(0xffffffffu, fin);
