@@ -1,10 +1,16 @@
 #!/bin/bash
+# Variant sweep: each variants/*.so in place of the library, then
+#   bench.py --config $1 --steps $2 --warmup 3 $3
+# (device time only), twice in alternating order to expose box noise.
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -s -k "cfg2 or golden or edge or padded or device" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-for v in 0 1 2 3; do
-  for m in auto fast; do
-    MEXP_N8_VARIANT=$v timeout 300 python bench.py --steps 200 --warmup 10 --rounding $m --no-cpu-baseline > gpurun_out/bench_v${v}_$m.log 2>&1
-  done
-done
-echo done
+cfg=${1:-cfg2}; steps=${2:-50}; extra=${3:-}
+cp paper_1710_10989_b200/_lib/libmexp_b200.so /tmp/lib_keep.so
+for pass in 1 2; do
+for v in variants/*.so; do
+  n=$(basename $v .so)
+  cp $v paper_1710_10989_b200/_lib/libmexp_b200.so
+  timeout 900 python bench.py --config $cfg --steps $steps --warmup 3 --no-cpu-baseline --e2e-steps 1 $extra > gpurun_out/var_${cfg}_${n}_$pass.log 2>&1
+  echo "$cfg $n pass$pass $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/var_${cfg}_${n}_$pass.log)" >> gpurun_out/variants.txt
+done; done
+cp /tmp/lib_keep.so paper_1710_10989_b200/_lib/libmexp_b200.so
