@@ -146,12 +146,38 @@ __device__ __forceinline__ void cp_wait() {
 // The epilogues in the arithmetic of O. For ExactOps every formula is the
 // reference's lincomb/add term for term (identity terms included, absent
 // operands skipped), so REFERENCE rounding reproduces its bits.
+// How many of g.in[] the epilogue reads (its loads are issued ahead of the
+// stores, see epi_load).
+template <int EPI>
+constexpr int epi_inputs() {
+    return EPI == EPI_STORE ? 0
+         : (EPI == EPI_AL || EPI == EPI_T12_B || EPI == EPI_T8_2 || EPI == EPI_T8_3) ? 2
+         : (EPI == EPI_T18_B || EPI == EPI_PS_B) ? 3
+         : 1;
+}
+struct EpiIn {
+    double2 v[3];
+};
+template <int EPI>
+__device__ __forceinline__ EpiIn epi_load(const GemmArgs& g, int64_t base, int row, int col) {
+    const int64_t off = base + int64_t(row) * g.np + col;
+    EpiIn e;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        e.v[k] = make_double2(0.0, 0.0);
+        if (k < epi_inputs<EPI>() && (EPI != EPI_PS_B || g.in[k]))
+            e.v[k] = __ldcg(reinterpret_cast<const double2*>(g.in[k] + off));
+    }
+    return e;
+}
+
 template <int EPI, class O>
 __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, int64_t base,
-                                              int row, int col, double c0, double c1) {
+                                              int row, int col, double c0, double c1,
+                                              const EpiIn& pre) {
     const int64_t off = base + int64_t(row) * g.np + col;
     const double id0 = (row == col) ? 1.0 : 0.0, id1 = (row == col + 1) ? 1.0 : 0.0;
-    auto ld = [&](int k) { return *reinterpret_cast<const double2*>(g.in[k] + off); };
+    auto ld = [&](int k) { return pre.v[k]; };
     auto st = [&](int k, double a, double b) {
         *reinterpret_cast<double2*>((k == 0 ? out0 : g.out[k]) + off) = make_double2(a, b);
     };
@@ -304,7 +330,8 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
 #pragma unroll
         for (int j = 0; j < 4; j += 2)
             epilogue_pair<EPI, ExactOps>(g, out0, base, m0 + 4 * ty + i, n0 + 4 * tx + j, acc[i][j],
-                                         acc[i][j + 1]);
+                                         acc[i][j + 1],
+                                         epi_load<EPI>(g, base, m0 + 4 * ty + i, n0 + 4 * tx + j));
 }
 
 template <int EPI>
@@ -434,12 +461,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     cp_wait<0>();
 #endif
 
+    // Epilogue by 8-row slabs: the slab's inputs are all loaded before any of
+    // its stores (the compiler cannot hoist loads over stores that may alias),
+    // so a warp waits for one round trip per slab, not per pair.
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < TM; ++i) {
+        EpiIn pre[TN];
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+            pre[j] = epi_load<EPI>(g, base, m0 + wm * WM + i * 8 + r, n0 + wn * WN + j * 8 + 2 * q);
 #pragma unroll
         for (int j = 0; j < TN; ++j)
             epilogue_pair<EPI, FastOps>(g, out0, base, m0 + wm * WM + i * 8 + r,
-                                        n0 + wn * WN + j * 8 + 2 * q, acc[i][j][0], acc[i][j][1]);
+                                        n0 + wn * WN + j * 8 + 2 * q, acc[i][j][0], acc[i][j][1], pre[j]);
+    }
 }
 
 // ---- prologue / epilogue kernels -------------------------------------------
