@@ -471,6 +471,8 @@ struct HostPipe {
     std::vector<cudaEvent_t> ev;  // one per chunk of a call: its records have landed
     std::vector<cudaEvent_t> ev_in, ev_k;  // staged pipeline: chunk's H2D / kernel done
     int64_t h_sel_cap = 0;
+    void* h_stage = nullptr;  // small calls: pinned staging for pageable A / e^A / records
+    size_t h_stage_cap = 0;
     std::mutex mu;
 };
 
@@ -605,6 +607,60 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
 }  // extern "C"
 
 namespace {
+// device-accessible address of mapped pinned host memory, or nullptr if p is
+// pageable
+void* mapped_device_ptr(const void* p) {
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return attr.type == cudaMemoryTypeHost ? attr.devicePointer : nullptr;
+}
+
+int small_call_impl(HostPipe& p, const void* h_a, void* h_out, int dtype, int n, int64_t batch,
+                    int aarg, int rounding, mexp_selection* h_sel, int64_t* first_error) {
+    int r = ensure_pipe(p, 0, 0);
+    if (r != MEXP_OK) return r;
+    const size_t bytes = size_t(batch) * n * n * (dtype == MEXP_F64 ? sizeof(double) : sizeof(float));
+    const size_t sel_bytes = size_t(batch) * sizeof(mexp_selection);
+    void* d_a = mapped_device_ptr(h_a);
+    void* d_out = mapped_device_ptr(h_out);
+    mexp_selection* d_sel = h_sel ? static_cast<mexp_selection*>(mapped_device_ptr(h_sel)) : nullptr;
+    const size_t need = 2 * bytes + sel_bytes + 64;
+    if ((!d_a || !d_out || !d_sel) && p.h_stage_cap < need) {
+        if (p.h_stage) cudaFreeHost(p.h_stage);
+        p.h_stage = nullptr;
+        p.h_stage_cap = 0;
+        MEXP_CUDA(cudaMallocHost(&p.h_stage, need));
+        p.h_stage_cap = need;
+    }
+    char* stage = static_cast<char*>(p.h_stage);
+    char* s_in = stage;
+    char* s_out = stage + ((bytes + 15) & ~size_t(15));
+    mexp_selection* s_sel = reinterpret_cast<mexp_selection*>(s_out + ((bytes + 15) & ~size_t(15)));
+    if (!d_a) {
+        std::memcpy(s_in, h_a, bytes);
+        d_a = mapped_device_ptr(s_in);
+    }
+    const bool out_staged = !d_out, sel_staged = !d_sel;
+    if (out_staged) d_out = mapped_device_ptr(s_out);
+    if (sel_staged) d_sel = static_cast<mexp_selection*>(mapped_device_ptr(s_sel));
+    if (!d_a || !d_out || !d_sel) return MEXP_ERR_CUDA;
+    r = expm_device(d_a, d_out, dtype, n, batch, aarg, rounding, d_sel, p.st[0]);
+    if (r != MEXP_OK) return r;
+    MEXP_CUDA(cudaStreamSynchronize(p.st[0]));
+    if (out_staged) std::memcpy(h_out, s_out, bytes);
+    const mexp_selection* hs = sel_staged ? s_sel : h_sel;
+    if (h_sel && sel_staged) std::memcpy(h_sel, s_sel, sel_bytes);
+    for (int64_t b = 0; b < batch; ++b)
+        if (hs[b].status != MEXP_OK) {
+            if (first_error) *first_error = b;
+            return hs[b].status;
+        }
+    return MEXP_OK;
+}
+
 // The host pipeline behind mexp_expm_batched_host; `aarg` is the kernels'
 // acc_arg (accuracy | family << 4, family 3 = reference_expm's selection).
 int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch, int aarg,
@@ -631,6 +687,18 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
         const char* e = std::getenv("MEXP_HOST_CHUNK_MB_LARGE");
         return size_t(e ? std::atoi(e) : 512) << 20;
     }();
+    // Small calls (n <= 64, up to MEXP_SMALL_CALL_KB each way, default 1 MiB):
+    // one stream and one synchronisation instead of the three-stream copy
+    // pipeline. The n <= 64 kernels read A once and write e^A once, so they
+    // run on host memory directly (mapped pinned memory, zero-copy over
+    // PCIe): the caller's buffers when they are pinned, else the pipe's
+    // pinned staging (one memcpy each way).
+    static const size_t small_call = [] {
+        const char* e = std::getenv("MEXP_SMALL_CALL_KB");
+        return size_t(e ? std::atoi(e) : 1024) << 10;
+    }();
+    if (n <= 64 && size_t(batch) * mat_bytes <= small_call)
+        return small_call_impl(p, h_a, h_out, dtype, n, batch, aarg, rounding, h_sel, first_error);
     int64_t chunk = int64_t((n > 64 ? chunk_large : chunk_small) / mat_bytes);
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;

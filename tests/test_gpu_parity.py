@@ -297,3 +297,37 @@ def test_graph_capture_and_replay(cuda, oracle, family):
         graph.replay()
         torch.cuda.synchronize()
         assert np.array_equal(bits(out.cpu().numpy()), bits(ref.out))
+
+
+@pytest.mark.parametrize("n", [8, 13, 50, 64])
+@pytest.mark.parametrize("kind", ["pinned", "pageable"])
+def test_small_call_path(cuda, oracle, n, kind):
+    """Host calls up to MEXP_SMALL_CALL_KB run on one stream with the kernels
+    reading/writing host memory (pinned caller buffers in place, pageable ones
+    through pinned staging): same bits as the device API and the reference,
+    and the first non-finite matrix reported."""
+    import torch
+    rng = np.random.default_rng(7 + n)
+    norms = np.array([1e-9, 0.02, 0.7, 1.5, 9.0])
+    a = rng.standard_normal((len(norms), n, n))
+    a *= (norms / workloads.one_norm_batched(a))[:, None, None]
+    ref = oracle.expm_batch(a)
+    if kind == "pinned":
+        ha = torch.from_numpy(a).pin_memory()
+        ho = torch.empty_like(ha).pin_memory()
+        sel_out = torch.empty(16 * len(a), dtype=torch.uint8).pin_memory()
+        out, sel, st = mx.expm_batched_host(ha, ho, rounding=mx.ROUND_REFERENCE, sel_out=sel_out)
+        out = out.numpy()
+    else:
+        out, sel, st = mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE)
+    assert st == mx.OK
+    assert np.array_equal(sel["degree"], ref.degree) and np.array_equal(sel["s"], ref.s)
+    assert np.array_equal(bits(out), bits(ref.out))
+    d = torch.from_numpy(a).cuda()
+    od = torch.empty_like(d)
+    mx.expm_batched(d, od, rounding=mx.ROUND_REFERENCE)
+    assert np.array_equal(bits(out), bits(od.cpu().numpy()))
+    bad = a.copy()
+    bad[3, 0, n - 1] = np.nan
+    _, sel, st = mx.expm_batched_host(bad, raise_on_error=False)
+    assert st == mx.ERR_NONFINITE and list(sel["status"]) == [0, 0, 0, 1, 0]
