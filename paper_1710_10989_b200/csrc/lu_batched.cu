@@ -74,11 +74,27 @@ __global__ void __launch_bounds__(COL_THREADS) lu_col_kernel(
     double best = -1.0;
     int brow = np;
     const int rbeg = c + blockIdx.x * COL_ROWS;
-    for (int i = warp; i < COL_ROWS; i += COL_THREADS / 32) {
+    // the warp's rows are all loaded before the first store (one memory
+    // round trip per CTA rather than one per row)
+    constexpr int RPW = COL_ROWS / (COL_THREADS / 32);
+    double w0[RPW], w1[RPW];
+#pragma unroll
+    for (int t = 0; t < RPW; ++t) {
+        const int r = rbeg + warp + t * (COL_THREADS / 32);
+        w0[t] = w1[t] = 0.0;
+        if (r < np) {
+            const double* row = M + int64_t(r) * np + c0;
+            w0[t] = row[lane];
+            w1[t] = row[32 + lane];
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < RPW; ++t) {
+        const int i = warp + t * (COL_THREADS / 32);
         const int r = rbeg + i;
         if (r >= np) break;
         double* row = M + int64_t(r) * np + c0;
-        double v0 = row[lane], v1 = row[32 + lane];
+        double v0 = w0[t], v1 = w1[t];
         if (upd) {
             const double mine = jm < 32 ? v0 : v1;
             const double l = __shfl_sync(0xffffffffu, mine, jm & 31) / pv;  // row[k] / piv
@@ -223,6 +239,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 // C[rc .. rc + rows) x [cc .. cc + cols) -= X[rc.., kc .. kc + NB) * Y[kc.., cc..]
+// (C may alias X's or Y's matrix, never the same elements)
 // (all of one matrix, row stride np); 128 x 128 tiles, 8 warps of 64 x 32.
 struct SubArgs {
     double* C;
@@ -242,12 +259,29 @@ __global__ void __launch_bounds__(256, 1) gemm_sub_kernel(SubArgs a) {
     const int wm = warp >> 2, wn = warp & 3;
     const int r = lane >> 2, q = lane & 3;
     const int tr = blockIdx.y * GB, tc = blockIdx.x * GB;  // tile origin within the block
+    // The accumulators start as C (D = (-X) Y + C on DMMA): C's loads are
+    // issued with the operand loads, before any store, so the tile costs one
+    // memory round trip instead of one per read-modify-write of the epilogue.
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = tr + wm * 64 + i * 8 + r;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = tc + wn * 32 + j * 8 + 2 * q;
+            double2 v = make_double2(0.0, 0.0);
+            if (row < a.rows && col < a.cols)
+                v = *reinterpret_cast<const double2*>(a.C + base + int64_t(a.rc + row) * a.np + a.cc + col);
+            acc[i][j][0] = v.x;
+            acc[i][j][1] = v.y;
+        }
+    }
     for (int e = tid; e < GB * NB / 2; e += 256) {
         const int i = e / (NB / 2), k = (e % (NB / 2)) * 2;
         double2 v = make_double2(0.0, 0.0);
         if (tr + i < a.rows)
             v = *reinterpret_cast<const double2*>(a.X + base + int64_t(a.rc + tr + i) * a.np + a.kc + k);
-        *reinterpret_cast<double2*>(sx + i * GLDX + k) = v;
+        *reinterpret_cast<double2*>(sx + i * GLDX + k) = make_double2(-v.x, -v.y);
     }
     for (int e = tid; e < NB * GB / 2; e += 256) {
         const int k = e / (GB / 2), j = (e % (GB / 2)) * 2;
@@ -257,11 +291,6 @@ __global__ void __launch_bounds__(256, 1) gemm_sub_kernel(SubArgs a) {
         *reinterpret_cast<double2*>(sy + k * GLDY + j) = v;
     }
     __syncthreads();
-    double acc[8][4][2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const double* px = sx + (wm * 64 + r) * GLDX + q;
     const double* py = sy + q * GLDY + wn * 32 + r;
 #pragma unroll 2
@@ -284,11 +313,8 @@ __global__ void __launch_bounds__(256, 1) gemm_sub_kernel(SubArgs a) {
         for (int j = 0; j < 4; ++j) {
             const int col = tc + wn * 32 + j * 8 + 2 * q;
             if (col >= a.cols) continue;
-            double2* p = reinterpret_cast<double2*>(a.C + base + int64_t(a.rc + row) * a.np + a.cc + col);
-            double2 v = *p;
-            v.x -= acc[i][j][0];
-            v.y -= acc[i][j][1];
-            *p = v;
+            *reinterpret_cast<double2*>(a.C + base + int64_t(a.rc + row) * a.np + a.cc + col) =
+                make_double2(acc[i][j][0], acc[i][j][1]);
         }
     }
 }
