@@ -32,10 +32,10 @@ constexpr int NB = 64;         // panel width
 constexpr int COL_ROWS = 64;   // rows per CTA in the column step
 constexpr int COL_THREADS = 256;
 constexpr int TRSM_THREADS = 128;
-constexpr int GB = 128;        // gemm_sub tile
+constexpr int GBM = 128, GBN = 64;  // gemm_sub tile: 8 warps of 32 x 32, two CTAs per SM
 constexpr int GLDX = NB + 4;   // X tile row stride (doubles), 4 (mod 16)
-constexpr int GLDY = GB + 4;   // Y tile row stride
-constexpr size_t GEMM_SUB_SMEM = (size_t(GB) * GLDX + size_t(NB) * GLDY) * sizeof(double);
+constexpr int GLDY = GBN + 4;  // Y tile row stride
+constexpr size_t GEMM_SUB_SMEM = (size_t(GBM) * GLDX + size_t(NB) * GLDY) * sizeof(double);
 
 thread_local std::string g_lu_err;
 
@@ -240,7 +240,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 // C[rc .. rc + rows) x [cc .. cc + cols) -= X[rc.., kc .. kc + NB) * Y[kc.., cc..]
 // (C may alias X's or Y's matrix, never the same elements)
-// (all of one matrix, row stride np); 128 x 128 tiles, 8 warps of 64 x 32.
+// (all of one matrix, row stride np); 128 x 64 tiles, 8 warps of 32 x 32.
 struct SubArgs {
     double* C;
     const double* X;
@@ -249,23 +249,23 @@ struct SubArgs {
     const int32_t* list;
 };
 
-__global__ void __launch_bounds__(256, 1) gemm_sub_kernel(SubArgs a) {
+__global__ void __launch_bounds__(256, 2) gemm_sub_kernel(SubArgs a) {
     extern __shared__ __align__(16) double sm[];
-    double* sx = sm;                 // GB x GLDX
-    double* sy = sm + GB * GLDX;     // NB x GLDY
+    double* sx = sm;                 // GBM x GLDX
+    double* sy = sm + GBM * GLDX;    // NB x GLDY
     const int64_t m = a.list[blockIdx.z];
     const int64_t base = m * int64_t(a.np) * a.np;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 2, wn = warp & 3;
+    const int wm = warp >> 1, wn = warp & 1;
     const int r = lane >> 2, q = lane & 3;
-    const int tr = blockIdx.y * GB, tc = blockIdx.x * GB;  // tile origin within the block
+    const int tr = blockIdx.y * GBM, tc = blockIdx.x * GBN;  // tile origin within the block
     // The accumulators start as C (D = (-X) Y + C on DMMA): C's loads are
     // issued with the operand loads, before any store, so the tile costs one
     // memory round trip instead of one per read-modify-write of the epilogue.
-    double acc[8][4][2];
+    double acc[4][4][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int row = tr + wm * 64 + i * 8 + r;
+    for (int i = 0; i < 4; ++i) {
+        const int row = tr + wm * 32 + i * 8 + r;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int col = tc + wn * 32 + j * 8 + 2 * q;
@@ -276,38 +276,38 @@ __global__ void __launch_bounds__(256, 1) gemm_sub_kernel(SubArgs a) {
             acc[i][j][1] = v.y;
         }
     }
-    for (int e = tid; e < GB * NB / 2; e += 256) {
+    for (int e = tid; e < GBM * NB / 2; e += 256) {
         const int i = e / (NB / 2), k = (e % (NB / 2)) * 2;
         double2 v = make_double2(0.0, 0.0);
         if (tr + i < a.rows)
             v = *reinterpret_cast<const double2*>(a.X + base + int64_t(a.rc + tr + i) * a.np + a.kc + k);
         *reinterpret_cast<double2*>(sx + i * GLDX + k) = make_double2(-v.x, -v.y);
     }
-    for (int e = tid; e < NB * GB / 2; e += 256) {
-        const int k = e / (GB / 2), j = (e % (GB / 2)) * 2;
+    for (int e = tid; e < NB * GBN / 2; e += 256) {
+        const int k = e / (GBN / 2), j = (e % (GBN / 2)) * 2;
         double2 v = make_double2(0.0, 0.0);
         if (tc + j < a.cols)
             v = *reinterpret_cast<const double2*>(a.Y + base + int64_t(a.kc + k) * a.np + a.cc + tc + j);
         *reinterpret_cast<double2*>(sy + k * GLDY + j) = v;
     }
     __syncthreads();
-    const double* px = sx + (wm * 64 + r) * GLDX + q;
+    const double* px = sx + (wm * 32 + r) * GLDX + q;
     const double* py = sy + q * GLDY + wn * 32 + r;
-#pragma unroll 2
+#pragma unroll 4
     for (int k = 0; k < NB; k += 4) {
-        double af[8], bf[4];
+        double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) af[i] = px[i * 8 * GLDX + k];
+        for (int i = 0; i < 4; ++i) af[i] = px[i * 8 * GLDX + k];
 #pragma unroll
         for (int j = 0; j < 4; ++j) bf[j] = py[k * GLDY + j * 8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int row = tr + wm * 64 + i * 8 + r;
+    for (int i = 0; i < 4; ++i) {
+        const int row = tr + wm * 32 + i * 8 + r;
         if (row >= a.rows) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -331,7 +331,7 @@ int sub(double* C, const double* X, const double* Y, int rc, int cc, int kc, int
     SubArgs a{C, X, Y, rc, cc, kc, rows, cols, np, list};
     for (int z0 = 0; z0 < count; z0 += 65535) {
         a.list = list + z0;
-        const dim3 grid((cols + GB - 1) / GB, (rows + GB - 1) / GB, std::min(count - z0, 65535));
+        const dim3 grid((cols + GBN - 1) / GBN, (rows + GBM - 1) / GBM, std::min(count - z0, 65535));
         gemm_sub_kernel<<<grid, 256, GEMM_SUB_SMEM, st>>>(a);
         launches->fetch_add(1, std::memory_order_relaxed);
     }
