@@ -59,8 +59,14 @@ thread_local std::string g_err;
         }                                                                        \
     } while (0)
 
+// CTA shape. 0: 128 x 128 tiles, 8 warps of 64 x 32, one CTA per SM;
+// 1: 128 x 64 tiles, 8 warps of 32 x 32, k-tiles of 16, two CTAs per SM (one
+// CTA's epilogue overlaps the other's mainloop)
+#ifndef MEXP_GEMM_SHAPE
+#define MEXP_GEMM_SHAPE 1
+#endif
 #ifndef MEXP_GEMM_BK
-#define MEXP_GEMM_BK 32
+#define MEXP_GEMM_BK (MEXP_GEMM_SHAPE == 1 ? 16 : 32)
 #endif
 // 0: cp.async (LDGSTS) for both operands; 1: row-wise cp.async.bulk for both;
 // 2: X tiles by tensor-map TMA (cp.async.bulk.tensor, 128B swizzle), Y rows
@@ -68,11 +74,15 @@ thread_local std::string g_err;
 #ifndef MEXP_GEMM_TMA
 #define MEXP_GEMM_TMA 2
 #endif
-constexpr int BM = 128, BN = 128, BK = MEXP_GEMM_BK, STAGES = BK == 16 ? 4 : 3;
-constexpr int LDA = BK + 4;   // 20 doubles: 4 (mod 16)
-constexpr int LDB = BN + 4;   // 132 doubles: 4 (mod 16)
-constexpr int WM = 64, WN = 32, TM = WM / 8, TN = WN / 8;
+constexpr int BM = 128, BN = MEXP_GEMM_SHAPE == 1 ? 64 : 128, BK = MEXP_GEMM_BK,
+              STAGES = BK == 16 ? 4 : 3;
+constexpr int LDA = BK + 4;   // 4 (mod 16) doubles
+constexpr int LDB = BN + 4;   // 4 (mod 16) doubles
+constexpr int WM = MEXP_GEMM_SHAPE == 1 ? 32 : 64, WN = 32, TM = WM / 8, TN = WN / 8;
+constexpr int WARPS_N = BN / WN;
 constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_MIN_CTAS = MEXP_GEMM_SHAPE == 1 ? 2 : 1;
+static_assert((BM / WM) * WARPS_N * 32 == GEMM_THREADS, "warp cover");
 #if MEXP_GEMM_TMA == 2
 // X stage: BK / 16 boxes of 128 rows x 16 doubles (128 B), TMA's 128B swizzle
 // (16-byte chunk c of row r at c ^ (r & 7)): conflict-free fragment loads
@@ -82,7 +92,8 @@ static_assert(BK % XBOX == 0 && (BM * XBOX * 8) % 1024 == 0, "swizzled boxes sta
 #else
 constexpr size_t A_DOUBLES = size_t(BM) * LDA;
 #endif
-constexpr size_t STAGE_DOUBLES = A_DOUBLES + size_t(BK) * LDB;
+// stages stay 1024 B aligned (TMA 128B-swizzle destinations)
+constexpr size_t STAGE_DOUBLES = (A_DOUBLES + size_t(BK) * LDB + 127) / 128 * 128;
 // + the stages' mbarriers and slack to align the ring to 1024 B
 constexpr size_t GEMM_SMEM = STAGES * STAGE_DOUBLES * sizeof(double) + 64 + 1024;
 
@@ -335,13 +346,13 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, GEMM_MIN_CTAS)
     gemm_dmma_kernel(GemmArgs g, const __grid_constant__ CUtensorMap tmx) {
     extern __shared__ __align__(16) double smem_raw[];
     double* const smem = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 2, wn = warp & 3;
+    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
     const int r = lane >> 2, q = lane & 3;
     const int32_t entry = g.list[blockIdx.z];
     const int64_t mat = entry & 0x7fffffff;
@@ -365,7 +376,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
 #pragma unroll
         for (int c = tid; c < BK * BN / 2; c += GEMM_THREADS) {
-            const int row = c >> 6, cc = (c & 63) * 2;
+            const int row = c / (BN / 2), cc = (c % (BN / 2)) * 2;
             cp_async16(sb + row * LDB + cc, Y + int64_t(k0 + row) * g.np + n0 + cc);
         }
     };
