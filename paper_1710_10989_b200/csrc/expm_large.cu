@@ -59,14 +59,15 @@ thread_local std::string g_err;
         }                                                                        \
     } while (0)
 
-// CTA shape. 0: 128 x 128 tiles, 8 warps of 64 x 32, one CTA per SM;
-// 1: 128 x 64 tiles, 8 warps of 32 x 32, k-tiles of 16, two CTAs per SM (one
-// CTA's epilogue overlaps the other's mainloop)
+// CTA shape. 0: 128 x 128 tiles, 8 warps of 64 x 32, k-tiles of 32 in 3
+// stages, one CTA per SM; 1: 128 x 64 tiles, 8 warps of 32 x 32, k-tiles of
+// 32 double-buffered, two CTAs per SM (one CTA's epilogue overlaps the
+// other's mainloop). Measured: profiles/gemm_tma_r1.txt.
 #ifndef MEXP_GEMM_SHAPE
 #define MEXP_GEMM_SHAPE 1
 #endif
 #ifndef MEXP_GEMM_BK
-#define MEXP_GEMM_BK (MEXP_GEMM_SHAPE == 1 ? 16 : 32)
+#define MEXP_GEMM_BK 32
 #endif
 // 0: cp.async (LDGSTS) for both operands; 1: row-wise cp.async.bulk for both;
 // 2: X tiles by tensor-map TMA (cp.async.bulk.tensor, 128B swizzle), Y rows
@@ -74,8 +75,11 @@ thread_local std::string g_err;
 #ifndef MEXP_GEMM_TMA
 #define MEXP_GEMM_TMA 2
 #endif
+#ifndef MEXP_GEMM_STAGES
+#define MEXP_GEMM_STAGES (MEXP_GEMM_SHAPE == 1 ? (MEXP_GEMM_BK == 16 ? 4 : 2) : (MEXP_GEMM_BK == 16 ? 4 : 3))
+#endif
 constexpr int BM = 128, BN = MEXP_GEMM_SHAPE == 1 ? 64 : 128, BK = MEXP_GEMM_BK,
-              STAGES = BK == 16 ? 4 : 3;
+              STAGES = MEXP_GEMM_STAGES;
 constexpr int LDA = BK + 4;   // 4 (mod 16) doubles
 constexpr int LDB = BN + 4;   // 4 (mod 16) doubles
 constexpr int WM = MEXP_GEMM_SHAPE == 1 ? 32 : 64, WN = 32, TM = WM / 8, TN = WN / 8;
