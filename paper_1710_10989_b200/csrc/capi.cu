@@ -6,6 +6,7 @@
 // block unchanged, since each padded term adds an exact +0 to a sum that is
 // never -0). n > 64 runs the DMMA GEMM engine (expm_large.cu).
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -607,6 +608,12 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
 }  // extern "C"
 
 namespace {
+double host_us() {
+    return 1e-3 * double(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                             std::chrono::steady_clock::now().time_since_epoch())
+                             .count());
+}
+
 // device-accessible address of mapped pinned host memory, or nullptr if p is
 // pageable
 void* mapped_device_ptr(const void* p) {
@@ -677,15 +684,15 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
     const size_t mat_bytes = size_t(n) * n * esz;
     // Chunks keep three in flight on three streams (H2D, compute, D2H): 16 MiB
     // for the small-n kernels (measured best, profiles/e2e_chunks_r1.txt);
-    // 512 MiB for large n, whose ragged squaring steps need enough matrices
-    // per chunk to fill the GPU
+    // 128 MiB for large n (cfg4: 64 matrices of 512^2 per chunk, measured
+    // best in profiles/e2e_pipeline_r1.txt)
     static const size_t chunk_small = [] {
         const char* e = std::getenv("MEXP_HOST_CHUNK_MB");
         return size_t(e ? std::atoi(e) : 16) << 20;
     }();
     static const size_t chunk_large = [] {
         const char* e = std::getenv("MEXP_HOST_CHUNK_MB_LARGE");
-        return size_t(e ? std::atoi(e) : 512) << 20;
+        return size_t(e ? std::atoi(e) : 128) << 20;
     }();
     // Small calls (n <= 64, up to MEXP_SMALL_CALL_KB each way, default 1 MiB):
     // one stream and one synchronisation instead of the three-stream copy
@@ -816,11 +823,16 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
         const int64_t b0 = plan[c].first, nb = plan[c].second;
         cudaStream_t st = p.st[k];
         mark(st);
+        const double h0 = trace ? host_us() : 0.0;
         if (!prefetch && (r = h2d(c)) != MEXP_OK) return r;
         if (prefetch && c + 1 < nchunks && (r = h2d(c + 1)) != MEXP_OK) return r;
+        const double h1 = trace ? host_us() : 0.0;
         mark(st);
         r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, aarg, rounding, p.d_sel[k], st);
         if (r != MEXP_OK) return r;
+        if (trace)
+            std::fprintf(stderr, "host chunk %2lld: h2d enqueue %8.1f-%8.1f, expm_device returns %8.1f us\n",
+                         (long long)c, h0, h1, host_us());
         mark(st);
         MEXP_CUDA(cudaMemcpyAsync(dst + b0 * mat_bytes, p.d_out[k], nb * mat_bytes,
                                   cudaMemcpyDeviceToHost, st));

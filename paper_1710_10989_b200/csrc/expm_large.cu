@@ -31,6 +31,7 @@
 // 32 independent DMMAs per k-step keep all four pipes saturated.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -511,9 +512,16 @@ __global__ void norm_cols_kernel(const double* __restrict__ a, int n, int64_t ba
     else atomicMax(maxbits + m, static_cast<unsigned long long>(__double_as_longlong(s)));
 }
 
+// device copy of n int32 from mapped pinned host memory: a kernel, not a
+// cudaMemcpy, so it never waits behind the copy engine's queue
+__global__ void upload_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+
 __global__ void select_kernel(const unsigned long long* __restrict__ maxbits,
                               const int* __restrict__ bad, int64_t batch, int acc_arg,
-                              mexp_selection* __restrict__ sel) {
+                              mexp_selection* __restrict__ sel, mexp_selection* __restrict__ host_sel) {
     const int accuracy = acc_arg & 15, family = acc_arg >> 4;  // mexp_accuracy | mexp_family << 4
     const int64_t m = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (m >= batch) return;
@@ -532,6 +540,7 @@ __global__ void select_kernel(const unsigned long long* __restrict__ maxbits,
         r.status = s.status;
     }
     sel[m] = r;
+    host_sel[m] = r;  // mapped pinned host memory: no copy-engine queue to wait in
 }
 
 // W0[m] = 2^-s A (zero padded), for the listed matrices; one block row-strip
@@ -699,6 +708,10 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
 struct Workspace {
     double* buf = nullptr;
     size_t bytes = 0;
+    mexp_selection* h_sel = nullptr;  // pinned (mapped) copy of the selections
+    int64_t h_sel_cap = 0;
+    int32_t* h_lists = nullptr;       // pinned (mapped) staging of the host-built lists
+    size_t h_lists_cap = 0;
     int device = -1;
     std::mutex mu;  // one large-n call per device at a time owns the buffers
 };
@@ -733,6 +746,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     Workspace& ws = workspace();
     std::lock_guard<std::mutex> ws_lock(ws.mu);  // the call synchronises its stream before returning
     if (ws.bytes < need) {
+        AsyncBuffer::retain_pool();
         if (ws.buf) LCUDA(cudaFreeAsync(ws.buf, st));
         LCUDA(cudaMallocAsync(&ws.buf, need, st));
         ws.bytes = need;
@@ -757,14 +771,24 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     sliced(batch, [&](int64_t y0, unsigned ny) {
         norm_cols_kernel<<<dim3((n + 255) / 256, ny), 256, 0, st>>>(d_a, n, batch, maxbits, bad, y0);
     });
-    select_kernel<<<unsigned((batch + 255) / 256), 256, 0, st>>>(maxbits, bad, batch, acc_arg, d_sel);
+    // (m, s) per matrix to the host: the schedule depends on them. The
+    // selection kernel writes them straight into mapped pinned memory: a
+    // cudaMemcpy would queue behind whatever the copy engine is moving (the
+    // host pipeline's previous chunk D2H) and serialise the pipeline.
+    if (ws.h_sel_cap < batch) {
+        if (ws.h_sel) LCUDA(cudaFreeHost(ws.h_sel));
+        ws.h_sel = nullptr;
+        ws.h_sel_cap = 0;
+        LCUDA(cudaHostAlloc(&ws.h_sel, sizeof(mexp_selection) * batch, cudaHostAllocMapped));
+        ws.h_sel_cap = batch;
+    }
+    mexp_selection* d_hsel = nullptr;
+    LCUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hsel), ws.h_sel, 0));
+    select_kernel<<<unsigned((batch + 255) / 256), 256, 0, st>>>(maxbits, bad, batch, acc_arg, d_sel,
+                                                                  d_hsel);
     launches->fetch_add(2, std::memory_order_relaxed);
-
-    // (m, s) per matrix to the host: the schedule depends on them
-    std::vector<mexp_selection> h_sel(batch);
-    LCUDA(cudaMemcpyAsync(h_sel.data(), d_sel, sizeof(mexp_selection) * batch,
-                          cudaMemcpyDeviceToHost, st));
     LCUDA(cudaStreamSynchronize(st));
+    const mexp_selection* h_sel = ws.h_sel;
     constexpr int kMaxDeg = 26;
     std::vector<int32_t> by_deg[kMaxDeg + 1];
     int max_s = 0;
@@ -846,11 +870,31 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         if (h_sel[m].status != MEXP_OK) bad_list.push_back(int32_t(m));
     const size_t off_bad = append(bad_list);
     const size_t off_all2 = append(all_ok);
+    // host-built lists reach the device through mapped pinned staging and a
+    // copy kernel (room for a second upload of up to batch entries below)
+    const size_t lists_need = host_lists.size() + size_t(batch);
+    if (ws.h_lists_cap < lists_need) {
+        LCUDA(cudaStreamSynchronize(st));
+        if (ws.h_lists) LCUDA(cudaFreeHost(ws.h_lists));
+        ws.h_lists = nullptr;
+        ws.h_lists_cap = 0;
+        LCUDA(cudaHostAlloc(&ws.h_lists, sizeof(int32_t) * lists_need, cudaHostAllocMapped));
+        ws.h_lists_cap = lists_need;
+    }
+    auto upload = [&](const std::vector<int32_t>& v, size_t pinned_off, int32_t* dst) -> int {
+        if (v.empty()) return MEXP_OK;
+        std::memcpy(ws.h_lists + pinned_off, v.data(), sizeof(int32_t) * v.size());
+        int32_t* src = nullptr;
+        LCUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&src), ws.h_lists + pinned_off, 0));
+        const int64_t cnt = int64_t(v.size());
+        upload_kernel<<<unsigned(std::min<int64_t>((cnt + 255) / 256, 1024)), 256, 0, st>>>(src, dst, cnt);
+        launches->fetch_add(1, std::memory_order_relaxed);
+        return MEXP_OK;
+    };
     if (!host_lists.empty()) {
         LCUDA(lists_buf.alloc(sizeof(int32_t) * host_lists.size()));
         d_lists = lists_buf.get<int32_t>();
-        LCUDA(cudaMemcpyAsync(d_lists, host_lists.data(), sizeof(int32_t) * host_lists.size(),
-                              cudaMemcpyHostToDevice, st));
+        if ((r = upload(host_lists, 0, d_lists)) != MEXP_OK) return r;
     }
     auto L = [&](size_t off) { return d_lists + off; };
     const dim3 ew_block(256);
@@ -1099,8 +1143,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         both.insert(both.end(), od.begin(), od.end());
         LCUDA(extra_buf.alloc(sizeof(int32_t) * both.size()));
         int32_t* d_extra = extra_buf.get<int32_t>();
-        LCUDA(cudaMemcpyAsync(d_extra, both.data(), sizeof(int32_t) * both.size(),
-                              cudaMemcpyHostToDevice, st));
+        if ((r = upload(both, host_lists.size(), d_extra)) != MEXP_OK) return r;
         sliced(int64_t(ev.size()), [&](int64_t y0, unsigned ny) {
             unpad_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(R, d_out, n, np, d_extra + y0);
         });
@@ -1108,7 +1151,6 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
             unpad_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(S, d_out, n, np, d_extra + ev.size() + y0);
         });
         launches->fetch_add(2, std::memory_order_relaxed);
-        LCUDA(cudaStreamSynchronize(st));  // `both` must outlive the async copy
     }
     if (!bad_list.empty()) {
         sliced(int64_t(bad_list.size()), [&](int64_t y0, unsigned ny) {
