@@ -155,3 +155,52 @@ def test_large_n_reference_rounding_refuses_pade(cuda):
     a = np.zeros((1, 70, 70))
     with pytest.raises(ValueError, match="unsupported"):
         mx.expm_batched_host(a, rounding=mx.ROUND_REFERENCE, family=mx.Family.PadeDiagonal)
+
+
+_CHUNKED_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+import paper_1710_10989_b200 as mx
+from paper_1710_10989_b200 import workloads
+rng = np.random.default_rng(77)
+n = 130
+norms = np.exp(rng.uniform(np.log(1e-6), np.log(60.0), 23))
+a = rng.standard_normal((23, n, n))
+a *= (norms / workloads.one_norm_batched(a))[:, None, None]
+a[9, 3, 4] = np.nan
+a[17, 0, 0] = np.inf
+out, sel, st = mx.expm_batched_host(a, raise_on_error=False)
+d = torch.from_numpy(a).cuda()
+od = torch.empty_like(d)
+sd = torch.empty(16 * len(a), dtype=torch.uint8, device="cuda")
+try:
+    mx.expm_batched(d, od, sd)
+except Exception:
+    pass
+torch.cuda.synchronize()
+ref_sel = sd.cpu().numpy().view(mx.SELECTION_DTYPE)
+ok = [i for i in range(len(a)) if i not in (9, 17)]
+assert st == mx.ERR_NONFINITE, st
+assert list(np.nonzero(sel["status"])[0]) == [9, 17]
+assert np.array_equal(sel["degree"], ref_sel["degree"]) and np.array_equal(sel["s"], ref_sel["s"])
+assert np.array_equal(out[ok].view(np.uint64), od.cpu().numpy()[ok].view(np.uint64))
+assert np.isnan(out[9]).all() and np.isnan(out[17]).all()
+print("chunked ok")
+"""
+
+
+def test_large_n_host_pipeline_many_chunks(cuda):
+    """The large-n host pipeline over many chunks (MEXP_HOST_CHUNK_MB_LARGE=1:
+    7 matrices of 130^2 per chunk, 4 chunks): selections read back through
+    mapped memory and lists uploaded by the copy kernel give the same bits as
+    one device call, with non-finite matrices in two different chunks."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MEXP_HOST_CHUNK_MB_LARGE="1")
+    r = subprocess.run([sys.executable, "-c", _CHUNKED_SCRIPT, root], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "chunked ok" in r.stdout, r.stdout + r.stderr
