@@ -18,7 +18,10 @@
 // Pivot order and multipliers follow the reference; the trailing updates use
 // FMA/DMMA rounding (the large-n path is FAST-only).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
+
+#include <cooperative_groups.h>
 
 #include "async_buffer.hpp"
 #include "expm_common.cuh"
@@ -173,6 +176,180 @@ __global__ void __launch_bounds__(COL_THREADS) lu_col_kernel(
         *rc = b;
         *rp = a;
     }
+}
+
+// Whole-panel factorisation for np - c0 <= 512: one cluster of G = ceil((np -
+// c0) / 64) CTAs per matrix, CTA b holding rows [c0 + 64b, c0 + 64b + 64) of
+// the panel in registers (warp w, slot t: row c0 + 64b + w + 8t; lane: columns
+// lane and 32 + lane), so the panel is read and written once instead of once
+// per column. Per column: CTA-local best candidate -> cluster barrier -> every
+// CTA reduces the G candidates (DSMEM) in rank order to the same pivot -> the
+// pivot row is broadcast (DSMEM stores) and the displaced row c sent to the
+// pivot's owner -> cluster barrier -> swap and eliminate. The arithmetic, the
+// pivot rule and the swaps are lu_col_kernel's, so the factors are bit-equal.
+constexpr int PANEL_MAX_CTAS = 8;
+// a value select that keeps both arrays in registers (a ternary on two array
+// elements can become a select of the array addresses, i.e. local memory)
+__device__ __forceinline__ double pick(bool hi, double a, double b) {
+    const long long mask = -static_cast<long long>(hi);
+    return __longlong_as_double((__double_as_longlong(b) & mask) | (__double_as_longlong(a) & ~mask));
+}
+// v[idx] for a runtime idx without indexing the register array (an indexed
+// access would move the array to local memory)
+template <int R>
+__device__ __forceinline__ double slot(const double (&v)[R], int idx) {
+    long long acc = 0;
+#pragma unroll
+    for (int t = 0; t < R; ++t) acc |= __double_as_longlong(v[t]) & -static_cast<long long>(t == idx);
+    return __longlong_as_double(acc);
+}
+template <int G>
+__global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(COL_THREADS)
+    lu_panel_cluster_kernel(double* __restrict__ Mb, int np, const int32_t* __restrict__ list, int c0,
+                            int* __restrict__ piv, mexp_selection* __restrict__ sel) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int b = int(cluster.block_rank());
+    const int64_t m = list[blockIdx.y];
+    double* M = Mb + m * int64_t(np) * np;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int W = COL_THREADS / 32, RPW = COL_ROWS / W;
+    __shared__ double cand_v, cand_d;   // this CTA's best |value| and (CTA 0) |diagonal|
+    __shared__ int cand_r;
+    __shared__ double wv[W];
+    __shared__ int wr[W];
+    __shared__ __align__(16) double prow[NB];  // the pivot row (new row c), from its owner
+    __shared__ __align__(16) double crow[NB];  // old row c, at the pivot's owner
+    __shared__ int s_p;
+    const int rb = c0 + COL_ROWS * b;  // first row of this CTA
+    double v0[RPW], v1[RPW];
+#pragma unroll
+    for (int t = 0; t < RPW; ++t) {
+        const int r = rb + warp + W * t;
+        v0[t] = v1[t] = 0.0;
+        if (r < np) {
+            const double* row = M + int64_t(r) * np + c0;
+            v0[t] = row[lane];
+            v1[t] = row[32 + lane];
+        }
+    }
+    for (int j = 0; j < NB; ++j) {
+        const int c = c0 + j;
+        const bool hi = j >= 32;  // column j is in v1 (lanes hold columns lane, 32 + lane)
+        // 1. local candidates: the lane holding column j scans its warp's rows >= c
+        if (lane == (j & 31)) {
+            double best = -1.0;
+            int brow = np;
+#pragma unroll
+            for (int t = 0; t < RPW; ++t) {
+                const int r = rb + warp + W * t;
+                if (r >= c && r < np) {
+                    const double cv = fabs(pick(hi, v0[t], v1[t]));
+                    if (better(cv, r, best, brow)) {
+                        best = cv;
+                        brow = r;
+                    }
+                }
+            }
+            wv[warp] = best;
+            wr[warp] = brow;
+            if (b == 0 && warp == (j & 7)) {
+                cand_d = fabs(pick(hi, slot(v0, j >> 3), slot(v1, j >> 3)));
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double best = wv[0];
+            int brow = wr[0];
+            for (int w = 1; w < W; ++w)
+                if (better(wv[w], wr[w], best, brow)) {
+                    best = wv[w];
+                    brow = wr[w];
+                }
+            cand_v = best;
+            cand_r = brow;
+        }
+        cluster.sync();
+        // 2. the pivot, identically in every CTA
+        if (threadIdx.x == 0) {
+            double bv = -1.0;
+            int br = np;
+            for (int q = 0; q < G; ++q) {
+                const double v = *cluster.map_shared_rank(&cand_v, q);
+                const int r = *cluster.map_shared_rank(&cand_r, q);
+                if (better(v, r, bv, br)) {
+                    bv = v;
+                    br = r;
+                }
+            }
+            const double dk = *cluster.map_shared_rank(&cand_d, 0);
+            int p = br;
+            if (dk != dk) p = c;  // a NaN diagonal: the reference's scan never moves
+            else if (bv == 0.0) {  // "singular denominator" (kernels.cpp:71-72)
+                p = c;
+                if (b == 0) sel[m].status = MEXP_ERR_SINGULAR;
+            }
+            if (b == 0) piv[m * int64_t(np) + c] = p;
+            s_p = p;
+        }
+        __syncthreads();
+        const int p = s_p;
+        const int pb = (p - c0) / COL_ROWS, pw = (p - rb) & (W - 1), pt = ((p - c0) % COL_ROWS) / W;
+        // 3. broadcast the pivot row; send row c to the pivot's owner
+        if (b == pb && warp == pw) {
+            const double a0 = slot(v0, pt), a1 = slot(v1, pt);
+            for (int q = 0; q < G; ++q) {
+                double* d = cluster.map_shared_rank(prow, q);
+                d[lane] = a0;
+                d[32 + lane] = a1;
+            }
+        }
+        if (p != c && b == 0 && warp == (j & 7)) {
+            double* d = cluster.map_shared_rank(crow, pb);
+            d[lane] = slot(v0, j >> 3);
+            d[32 + lane] = slot(v1, j >> 3);
+        }
+        cluster.sync();
+        // 4. swap, then eliminate column j from the rows below c
+        if (p != c) {
+            const bool own_c = b == 0 && warp == (j & 7), own_p = b == pb && warp == pw;
+            const double pr0 = prow[lane], pr1 = prow[32 + lane];
+            const double cr0 = crow[lane], cr1 = crow[32 + lane];
+#pragma unroll
+            for (int t = 0; t < RPW; ++t) {
+                const bool tc = own_c && t == (j >> 3), tp = own_p && t == pt;
+                v0[t] = pick(tc, pick(tp, v0[t], cr0), pr0);
+                v1[t] = pick(tc, pick(tp, v1[t], cr1), pr1);
+            }
+        }
+        const double pv = prow[j];
+        const double u0 = prow[lane], u1 = prow[32 + lane];
+#pragma unroll
+        for (int t = 0; t < RPW; ++t) {
+            const int r = rb + warp + W * t;
+            if (r <= c || r >= np) continue;
+            const double mine = pick(hi, v0[t], v1[t]);
+            const double l = __shfl_sync(0xffffffffu, mine, j & 31) / pv;  // row[k] / piv
+            if (j < 32) {
+                if (lane == j) v0[t] = l;
+                if (lane > j) v0[t] = fma(-l, u0, v0[t]);
+                v1[t] = fma(-l, u1, v1[t]);
+            } else {
+                if (lane == (j & 31)) v1[t] = l;
+                if (lane > (j & 31)) v1[t] = fma(-l, u1, v1[t]);
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < RPW; ++t) {
+        const int r = rb + warp + W * t;
+        if (r < np) {
+            double* row = M + int64_t(r) * np + c0;
+            row[lane] = v0[t];
+            row[32 + lane] = v1[t];
+        }
+    }
+    cluster.sync();  // no CTA exits while a peer may still write its shared memory
 }
 
 // The panel's row swaps (in order) on M's columns outside [c0, c0 + NB)
@@ -338,6 +515,30 @@ int sub(double* C, const double* X, const double* Y, int rc, int cc, int kc, int
     return MEXP_OK;
 }
 
+template <int G>
+void launch_panel(double* M, int np, const int32_t* list, int count, int c0, int* piv,
+                  mexp_selection* sel, cudaStream_t st) {
+    lu_panel_cluster_kernel<G><<<dim3(G, count), COL_THREADS, 0, st>>>(M, np, list, c0, piv, sel);
+}
+
+int panel_cluster(double* M, int np, const int32_t* list, int count, int c0, int G, int* piv,
+                  mexp_selection* sel, cudaStream_t st, std::atomic<uint64_t>* launches) {
+    switch (G) {
+        case 1: launch_panel<1>(M, np, list, count, c0, piv, sel, st); break;
+        case 2: launch_panel<2>(M, np, list, count, c0, piv, sel, st); break;
+        case 3: launch_panel<3>(M, np, list, count, c0, piv, sel, st); break;
+        case 4: launch_panel<4>(M, np, list, count, c0, piv, sel, st); break;
+        case 5: launch_panel<5>(M, np, list, count, c0, piv, sel, st); break;
+        case 6: launch_panel<6>(M, np, list, count, c0, piv, sel, st); break;
+        case 7: launch_panel<7>(M, np, list, count, c0, piv, sel, st); break;
+        case 8: launch_panel<8>(M, np, list, count, c0, piv, sel, st); break;
+        default: return MEXP_ERR_UNSUPPORTED;
+    }
+    launches->fetch_add(1, std::memory_order_relaxed);
+    LUCUDA(cudaGetLastError());
+    return MEXP_OK;
+}
+
 template <bool kLower>
 int trsm(const double* M, double* X, int np, const int32_t* list, int count, int r0, int cb,
          int ncols, cudaStream_t st, std::atomic<uint64_t>* launches) {
@@ -373,7 +574,17 @@ int lu_solve_batched(double* M, double* R, int np, int64_t batch, const int32_t*
     unsigned* counter = reinterpret_cast<unsigned*>(scratch + pv_b + piv_b + pr_b);
     LUCUDA(cudaMemsetAsync(counter, 0, ct_b, st));
     int r;
+    // panels of at most 512 rows: one cluster kernel per panel (MEXP_LU_PANEL=0
+    // forces the per-column kernels)
+    static const bool panel_ok = [] {
+        const char* e = std::getenv("MEXP_LU_PANEL");
+        return !(e && std::atoi(e) == 0);
+    }();
     for (int c0 = 0; c0 < np; c0 += NB) {
+        const int G = (np - c0 + COL_ROWS - 1) / COL_ROWS;
+        if (panel_ok && G <= PANEL_MAX_CTAS) {
+            if ((r = panel_cluster(M, np, d_list, count, c0, G, piv, d_sel, st, launches))) return r;
+        } else
         for (int c = c0; c <= c0 + NB; ++c) {
             if (c >= np) break;
             const dim3 grid((np - c + COL_ROWS - 1) / COL_ROWS, count);

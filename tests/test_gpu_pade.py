@@ -125,3 +125,45 @@ def test_pade_large_n_pivoting(cuda, oracle):
     out, sel, st = mx.expm_batched_host(a, family=PADE)
     assert st == mx.OK and np.array_equal(sel["s"], ref.s)
     assert rel_fro(out, ref.out).max() <= 50 * n * U53
+
+
+_LU_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1710_10989_b200 as mx
+from paper_1710_10989_b200 import workloads
+out_path = sys.argv[2]
+res = {}
+for n in (130, 500, 600):
+    rng = np.random.default_rng(n)
+    perm = rng.permutation(n)
+    a = rng.standard_normal((4, n, n)) * 0.05
+    a[0][np.arange(n), perm] += 1.0          # row exchanges at every column
+    a[1] = np.triu(a[1])                     # triangular: no exchanges
+    a *= (np.array([4.0, 30.0, 0.7, 9.0]) / workloads.one_norm_batched(a))[:, None, None]
+    out, sel, st = mx.expm_batched_host(a, family=mx.Family.PadeDiagonal, raise_on_error=False)
+    res[f"out{n}"] = out
+    res[f"st{n}"] = sel["status"]
+np.savez(out_path, **res)
+"""
+
+
+def test_pade_lu_panel_kernel_bitwise(cuda, tmp_path):
+    """The cluster panel factorisation (lu_panel_cluster_kernel, panels of <=
+    512 rows) and the per-column kernels (MEXP_LU_PANEL=0) give the same bits:
+    same pivots, multipliers and updates; n = 600 mixes both paths."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        path = str(tmp_path / f"lu{flag}.npz")
+        env = dict(os.environ, MEXP_LU_PANEL=flag)
+        r = subprocess.run([sys.executable, "-c", _LU_SCRIPT, root, path], env=env,
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        outs.append(np.load(path))
+    for k in outs[0].files:
+        assert np.array_equal(outs[0][k].view(np.uint8), outs[1][k].view(np.uint8)), k
