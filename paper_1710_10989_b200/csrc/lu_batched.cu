@@ -204,7 +204,7 @@ __device__ __forceinline__ double slot(const double (&v)[R], int idx) {
     return __longlong_as_double(acc);
 }
 template <int G>
-__global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(COL_THREADS)
+__global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(COL_THREADS, 3)
     lu_panel_cluster_kernel(double* __restrict__ Mb, int np, const int32_t* __restrict__ list, int c0,
                             int* __restrict__ piv, mexp_selection* __restrict__ sel) {
     namespace cg = cooperative_groups;
