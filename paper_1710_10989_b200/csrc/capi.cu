@@ -801,19 +801,23 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
             const int k = int(c % nslots);
             const int64_t b0 = plan[c].first, nb = plan[c].second;
             if (c >= nslots) MEXP_CUDA(cudaStreamWaitEvent(s_in, p.ev_k[c - nslots], 0));
+            mark(s_in);
             MEXP_CUDA(cudaMemcpyAsync(p.d_in[k], src + b0 * mat_bytes, nb * mat_bytes,
                                       cudaMemcpyHostToDevice, s_in));
+            mark(s_in);
             MEXP_CUDA(cudaEventRecord(p.ev_in[c], s_in));
             MEXP_CUDA(cudaStreamWaitEvent(s_k, p.ev_in[c], 0));
             if (c >= nslots) MEXP_CUDA(cudaStreamWaitEvent(s_k, p.ev[c - nslots], 0));
             r = expm_device(p.d_in[k], p.d_out[k], dtype, n, nb, aarg, rounding, p.d_sel[k], s_k);
             if (r != MEXP_OK) return r;
+            mark(s_k);
             MEXP_CUDA(cudaEventRecord(p.ev_k[c], s_k));
             MEXP_CUDA(cudaStreamWaitEvent(s_out, p.ev_k[c], 0));
             MEXP_CUDA(cudaMemcpyAsync(dst + b0 * mat_bytes, p.d_out[k], nb * mat_bytes,
                                       cudaMemcpyDeviceToHost, s_out));
             MEXP_CUDA(cudaMemcpyAsync(hs + b0, p.d_sel[k], nb * sizeof(mexp_selection),
                                       cudaMemcpyDeviceToHost, s_out));
+            mark(s_out);
             MEXP_CUDA(cudaEventRecord(p.ev[c], s_out));
         }
     }
