@@ -272,9 +272,13 @@ __device__ __forceinline__ void epilogue_pair(const GemmArgs& g, double* out0, i
 // Reference-rounded batched product (REFERENCE policy, n > 64): every output
 // is 0.0 + x_i0*y_0j + x_i1*y_1j + ... over k < n in order, each multiply and
 // add rounded (kernels.cpp:16-27), i.e. the reference's i-k-j loop bit for
-// bit. 64 x 64 CTA tiles, 256 threads of 4 x 4 outputs (16 independent
-// chains each), k-tiles of 16 double-buffered in shared memory.
-constexpr int XB = 64, XK = 16, XLDA = XK + 2, XLDB = XB + 2;  // rows 16-byte aligned
+// bit. 64 x 128 CTA tiles, 256 threads of 4 x 8 outputs (32 independent
+// chains each: rows 4ty.., columns 2tx + {0, 1} + 32g), k-tiles of 16
+// double-buffered in shared memory. Per k a thread loads 4 + 8 operands for
+// 64 FP64 operations, which keeps shared memory at ~3/4 of the FP64 pipe's
+// pace (a 4 x 4 tile loaded 8 for 32 and the two were co-bound).
+constexpr int XBM = 64, XBN = 128, XK = 16, XLDA = XK + 2, XLDB = XBN + 2;  // rows 16-byte aligned
+constexpr size_t EXACT_SMEM = (size_t(2) * XBM * XLDA + size_t(2) * XK * XLDB) * sizeof(double);
 
 // 16-byte async copy of the first `bytes` (0, 8 or 16) of src, zero-filling the rest
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, int bytes) {
@@ -284,9 +288,10 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, i
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
-    __shared__ __align__(16) double sa[2][XB][XLDA];
-    __shared__ __align__(16) double sb[2][XK][XLDB];
+__global__ void __launch_bounds__(256, 2) gemm_exact_kernel(GemmArgs g) {
+    extern __shared__ __align__(16) double xsm[];
+    double (*sa)[XBM][XLDA] = reinterpret_cast<double (*)[XBM][XLDA]>(xsm);
+    double (*sb)[XK][XLDB] = reinterpret_cast<double (*)[XK][XLDB]>(xsm + 2 * XBM * XLDA);
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int32_t entry = g.list[blockIdx.z];
     const int64_t mat = entry & 0x7fffffff;
@@ -294,28 +299,28 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
     const int64_t base = mat * g.mstride;
     const double* X = g.X + base;
     const double* Y = g.Y + base;
-    const int m0 = blockIdx.y * XB, n0 = blockIdx.x * XB;
+    const int m0 = blockIdx.y * XBM, n0 = blockIdx.x * XBN;
     const int ktiles = (g.n + XK - 1) / XK;
     // k >= n is zero-filled (and never summed: the k loop stops at n)
     auto load = [&](int s, int kt) {
         const int k0 = kt * XK;
-        for (int e = tid; e < XB * XK / 2; e += 256) {
+        for (int e = tid; e < XBM * XK / 2; e += 256) {
             const int r = e / (XK / 2), k = (e % (XK / 2)) * 2;
             const int valid = min(max(g.n - (k0 + k), 0), 2);
             cp_async16_zfill(&sa[s][r][k], X + int64_t(m0 + r) * g.np + min(k0 + k, g.np - 2), 8 * valid);
         }
-        for (int e = tid; e < XK * XB / 2; e += 256) {
-            const int k = e / (XB / 2), c = (e % (XB / 2)) * 2;
+        for (int e = tid; e < XK * XBN / 2; e += 256) {
+            const int k = e / (XBN / 2), c = (e % (XBN / 2)) * 2;
             const bool ok = k0 + k < g.n;
             cp_async16_zfill(&sb[s][k][c], Y + int64_t(ok ? k0 + k : 0) * g.np + n0 + c, ok ? 16 : 0);
         }
         cp_commit();
     };
-    double acc[4][4];
+    double acc[4][8];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
     load(0, 0);
     for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt & 1;
@@ -328,26 +333,30 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(GemmArgs g) {
         __syncthreads();
         const int kend = min(XK, g.n - kt * XK);  // never a padded term
         for (int k = 0; k < kend; ++k) {
-            double a[4], b[4];
+            double a[4], b[8];
 #pragma unroll
             for (int i = 0; i < 4; ++i) a[i] = sa[s][4 * ty + i][k];
-            const double2 b01 = *reinterpret_cast<const double2*>(&sb[s][k][4 * tx]);
-            const double2 b23 = *reinterpret_cast<const double2*>(&sb[s][k][4 * tx + 2]);
-            b[0] = b01.x, b[1] = b01.y, b[2] = b23.x, b[3] = b23.y;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double2 v = *reinterpret_cast<const double2*>(&sb[s][k][2 * tx + 32 * q]);
+                b[2 * q] = v.x;
+                b[2 * q + 1] = v.y;
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
+                for (int j = 0; j < 8; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
         }
         __syncthreads();
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; j += 2)
-            epilogue_pair<EPI, ExactOps>(g, out0, base, m0 + 4 * ty + i, n0 + 4 * tx + j, acc[i][j],
-                                         acc[i][j + 1],
-                                         epi_load<EPI>(g, base, m0 + 4 * ty + i, n0 + 4 * tx + j));
+        for (int q = 0; q < 4; ++q) {
+            const int row = m0 + 4 * ty + i, col = n0 + 2 * tx + 32 * q;
+            epilogue_pair<EPI, ExactOps>(g, out0, base, row, col, acc[i][2 * q], acc[i][2 * q + 1],
+                                         epi_load<EPI>(g, base, row, col));
+        }
 }
 
 template <int EPI>
@@ -652,6 +661,8 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
     static bool attr = [] {
         cudaFuncSetAttribute(gemm_dmma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(GEMM_SMEM));
+        cudaFuncSetAttribute(gemm_exact_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(EXACT_SMEM));
         return true;
     }();
     (void)attr;
@@ -681,7 +692,7 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
         for (int z0 = 0; z0 < count; z0 += 65535) {
             const int zc = std::min(count - z0, 65535);
             g.list = d_list + z0;
-            gemm_exact_kernel<EPI><<<dim3(np / XB, np / XB, zc), 256, 0, st>>>(g);
+            gemm_exact_kernel<EPI><<<dim3(np / XBN, np / XBM, zc), 256, EXACT_SMEM, st>>>(g);
             launches->fetch_add(1, std::memory_order_relaxed);
         }
         LCUDA(cudaGetLastError());
