@@ -706,7 +706,10 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
     }();
     if (n <= 64 && size_t(batch) * mat_bytes <= small_call)
         return small_call_impl(p, h_a, h_out, dtype, n, batch, aarg, rounding, h_sel, first_error);
-    int64_t chunk = int64_t((n > 64 ? chunk_large : chunk_small) / mat_bytes);
+    // (the Pade family's blocked LU costs ~600 launches per chunk at n = 512:
+    // it takes 4x the large-n chunk, measured best in profiles/e2e_pipeline_r1.txt)
+    const size_t chunk_bytes = n <= 64 ? chunk_small : is_pade(aarg) ? 4 * chunk_large : chunk_large;
+    int64_t chunk = int64_t(chunk_bytes / mat_bytes);
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     int r = ensure_pipe(p, size_t(chunk) * mat_bytes, chunk);
