@@ -331,3 +331,27 @@ def test_small_call_path(cuda, oracle, n, kind):
     bad[3, 0, n - 1] = np.nan
     _, sel, st = mx.expm_batched_host(bad, raise_on_error=False)
     assert st == mx.ERR_NONFINITE and list(sel["status"]) == [0, 0, 0, 1, 0]
+
+
+@pytest.mark.parametrize("family", [mx.Family.TaylorPS, mx.Family.PadeDiagonal])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_small_call_path_families_and_fp32(cuda, family, dtype):
+    """The small-call path with the other families and fp32 storage (the fp32
+    Pade route pads into fp64 device buffers straight from host memory): same
+    results and records as the device API."""
+    import torch
+    rng = np.random.default_rng(11)
+    n = 24
+    norms = np.array([1e-6, 0.3, 2.0, 11.0])
+    a = rng.standard_normal((len(norms), n, n))
+    a = (a * (norms / workloads.one_norm_batched(a))[:, None, None]).astype(dtype)
+    acc = mx.Accuracy.Single if dtype == np.float32 else mx.Accuracy.Double
+    out, sel, st = mx.expm_batched_host(a, accuracy=acc, family=family)
+    assert st == mx.OK
+    d = torch.from_numpy(a).cuda()
+    od = torch.empty_like(d)
+    sd = torch.empty(16 * len(a), dtype=torch.uint8, device="cuda")
+    mx.expm_batched(d, od, sd, accuracy=acc, family=family)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.view(np.uint8), od.cpu().numpy().view(np.uint8))
+    assert np.array_equal(sel.view(np.uint8), sd.cpu().numpy()[: 16 * len(a)])
