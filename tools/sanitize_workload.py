@@ -25,6 +25,23 @@ def main():
         mx.expm_batched_host(b)
         if n <= 64:
             mx.expm_batched_host(b.astype(np.float32), accuracy=mx.Accuracy.Single)
+    # one 64x64 (4-CTA cluster kernel), every family at small and large n,
+    # reference-rounded large n (exact GEMM), Pade panels on clusters of
+    # 2..8 CTAs (n = 130, 500) and per-column steps (n = 600)
+    mx.expm_batched_host(workloads.generate("cfg1", 0, 1))
+    for fam in (mx.Family.TaylorPS, mx.Family.PadeDiagonal):
+        for n in (8, 24, 64, 130):
+            norms = np.array([1e-9, 0.2, 3.0, 60.0])
+            b = rng.uniform(-1, 1, (4, n, n))
+            b *= (norms / workloads.one_norm_batched(b))[:, None, None]
+            mx.expm_batched_host(b, family=fam)
+    for n in (500, 600):
+        b = rng.uniform(-1, 1, (2, n, n))
+        b *= (np.array([0.5, 7.0]) / workloads.one_norm_batched(b))[:, None, None]
+        mx.expm_batched_host(b, family=mx.Family.PadeDiagonal)
+    b = rng.uniform(-1, 1, (3, 100, 100))
+    b *= (np.array([0.01, 1.0, 40.0]) / workloads.one_norm_batched(b))[:, None, None]
+    mx.expm_batched_host(b, rounding=mx.ROUND_REFERENCE)
     print("sanitize workload ok")
 
 
