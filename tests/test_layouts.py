@@ -52,3 +52,70 @@ def test_exact_path_and_norm_loads():
             assert len({u % 8 for u in units}) == len(units)
     for i in range(8):
         assert len({word(i, l) % 16 for l in range(8)}) == 8
+
+
+# ---- fp32 operand buffers (expm_small_f32.cu, n = 32 and 64) ----
+# chunk c (16 bytes) of row i is stored at chunk c ^ swz(i); a lane (ti, tj)
+# owns rows 4 ti + r and the column chunks tj and tj + GC (GC = n / 8).
+
+def swz32(i):
+    t = (i >> 2) & 7
+    return ((t & 1) << 2) | (t >> 1)
+
+
+def quad(n, i, c):
+    """bank quad (16-byte bank group, 8 per 128 bytes) of chunk c of row i"""
+    return (i * n // 4 + (c ^ swz32(i))) % 8
+
+
+def lanes(n, warp):
+    gc = n // 8
+    for l in range(32):
+        tid = 32 * warp + l
+        yield l, tid // gc, tid % gc
+
+
+def test_fp32_swizzle_formula_matches_kernel_source():
+    src = open(f"{ROOT}/paper_1710_10989_b200/csrc/expm_small_f32.cu").read()
+    assert "const int t = (i >> 2) & 7;" in src
+    assert "return ((t & 1) << 2) | (t >> 1);" in src
+
+
+def test_fp32_swizzle_is_a_row_permutation():
+    for n in (32, 64):
+        for i in range(n):
+            assert sorted(c ^ swz32(i) for c in range(n // 4)) == list(range(n // 4))
+
+
+def test_fp32_fragment_stores_conflict_free():
+    """STS.128 of (row 4ti + r, chunk tj + h GC): 8 distinct bank quads per
+    quarter warp."""
+    for n, warps in ((32, 1), (64, 4)):
+        gc = n // 8
+        for w in range(warps):
+            ls = list(lanes(n, w))
+            for r in range(4):
+                for h in range(2):
+                    for p in range(4):
+                        q = {quad(n, 4 * ti + r, tj + h * gc) for l, ti, tj in ls[8 * p:8 * p + 8]}
+                        assert len(q) == 8, (n, w, r, h, p)
+
+
+def test_fp32_operand_loads_conflict_free():
+    """X chunk loads (rows 4ti + r, chunk q) and Y row loads (row k, chunks
+    tj + h GC): per quarter warp, distinct addresses sit in distinct bank
+    quads (lanes sharing an address are a broadcast)."""
+    for n, warps in ((32, 1), (64, 4)):
+        gc = n // 8
+        for w in range(warps):
+            ls = list(lanes(n, w))
+            for p in range(4):
+                ph = ls[8 * p:8 * p + 8]
+                for r in range(4):
+                    for q in range(n // 4):
+                        addrs = {(4 * ti + r, q) for l, ti, tj in ph}
+                        assert len({quad(n, i, c) for i, c in addrs}) == len(addrs)
+                for k in range(n):
+                    for h in range(2):
+                        addrs = {(k, tj + h * gc) for l, ti, tj in ph}
+                        assert len({quad(n, i, c) for i, c in addrs}) == len(addrs)
