@@ -14,7 +14,7 @@ OBJDIR   := build/obj
 OBJS := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(CU_SRCS)) \
         $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.cpp.o,$(CXX_SRCS))
 
-all: $(LIB) oracle tests/cpp/dropin_kats tests/cpp/gallery_dump bin/mexp
+all: $(LIB) oracle tests/cpp/dropin_kats tests/cpp/gallery_dump bin/mexp bin/call_latency
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -43,5 +43,9 @@ tests/cpp/gallery_dump: tests/cpp/gallery_dump.cpp $(LIB) $(wildcard include/mex
 	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/_lib -lmexp_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/_lib'
 
 bin/mexp: tools/cli/mexp_cli.cpp $(LIB) $(wildcard include/mexp/*.hpp)
+	@mkdir -p bin
+	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/_lib -lmexp_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)/_lib'
+
+bin/call_latency: tools/cli/call_latency.cpp $(LIB) $(wildcard include/mexp/*.hpp)
 	@mkdir -p bin
 	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/_lib -lmexp_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)/_lib'
