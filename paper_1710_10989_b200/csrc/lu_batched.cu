@@ -373,6 +373,13 @@ __global__ void laswp_kernel(double* __restrict__ Mb, double* __restrict__ Rb, i
     }
 }
 
+// 16-byte cp.async, zero-filled when !ok
+__device__ __forceinline__ void cp_async16_z(double* smem, const double* gmem, bool ok) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+
 // X[r0 .. r0 + NB) x [cb, cb + ncols) <- T^-1 X with T the NB x NB diagonal
 // block of M at (r0, r0): unit lower (kLower) or upper. One column per thread.
 template <bool kLower>
@@ -383,9 +390,15 @@ __global__ void __launch_bounds__(TRSM_THREADS) trsm_kernel(const double* __rest
     const int64_t m = list[blockIdx.y];
     const double* M = Mb + m * int64_t(np) * np;
     double* X = Xb + m * int64_t(np) * np;
-    __shared__ double T[NB][NB + 1];
-    for (int e = threadIdx.x; e < NB * NB; e += TRSM_THREADS)
-        T[e / NB][e % NB] = M[int64_t(r0 + e / NB) * np + r0 + e % NB];
+    // the diagonal block by cp.async: all of it in flight at once (a load ->
+    // shared store loop waits one memory round trip per iteration)
+    __shared__ __align__(16) double T[NB][NB + 2];
+    for (int e = threadIdx.x; e < NB * NB / 2; e += TRSM_THREADS) {
+        const int i = e / (NB / 2), k = (e % (NB / 2)) * 2;
+        cp_async16_z(&T[i][k], M + int64_t(r0 + i) * np + r0 + k, true);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const int col = cb + blockIdx.x * TRSM_THREADS + threadIdx.x;
     if (col >= cb + ncols) return;
@@ -436,9 +449,22 @@ __global__ void __launch_bounds__(256, 2) gemm_sub_kernel(SubArgs a) {
     const int wm = warp >> 1, wn = warp & 1;
     const int r = lane >> 2, q = lane & 3;
     const int tr = blockIdx.y * GBM, tc = blockIdx.x * GBN;  // tile origin within the block
-    // The accumulators start as C (D = (-X) Y + C on DMMA): C's loads are
-    // issued with the operand loads, before any store, so the tile costs one
-    // memory round trip instead of one per read-modify-write of the epilogue.
+    // The operand tiles stream into shared memory by cp.async (no registers,
+    // no ordering against the shared stores), and the accumulators start as
+    // -C (D = X Y + (-C) on DMMA, so the tile result is -D = C - X Y exactly,
+    // rounding being sign-symmetric): every load of the tile is in flight at
+    // once, one memory round trip per tile.
+    for (int e = tid; e < GBM * NB / 2; e += 256) {
+        const int i = e / (NB / 2), k = (e % (NB / 2)) * 2;
+        const bool ok = tr + i < a.rows;
+        cp_async16_z(sx + i * GLDX + k, a.X + base + int64_t(a.rc + (ok ? tr + i : 0)) * a.np + a.kc + k, ok);
+    }
+    for (int e = tid; e < NB * GBN / 2; e += 256) {
+        const int k = e / (GBN / 2), j = (e % (GBN / 2)) * 2;
+        const bool ok = tc + j < a.cols;
+        cp_async16_z(sy + k * GLDY + j, a.Y + base + int64_t(a.kc + k) * a.np + a.cc + (ok ? tc + j : 0), ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -449,24 +475,11 @@ __global__ void __launch_bounds__(256, 2) gemm_sub_kernel(SubArgs a) {
             double2 v = make_double2(0.0, 0.0);
             if (row < a.rows && col < a.cols)
                 v = *reinterpret_cast<const double2*>(a.C + base + int64_t(a.rc + row) * a.np + a.cc + col);
-            acc[i][j][0] = v.x;
-            acc[i][j][1] = v.y;
+            acc[i][j][0] = -v.x;
+            acc[i][j][1] = -v.y;
         }
     }
-    for (int e = tid; e < GBM * NB / 2; e += 256) {
-        const int i = e / (NB / 2), k = (e % (NB / 2)) * 2;
-        double2 v = make_double2(0.0, 0.0);
-        if (tr + i < a.rows)
-            v = *reinterpret_cast<const double2*>(a.X + base + int64_t(a.rc + tr + i) * a.np + a.kc + k);
-        *reinterpret_cast<double2*>(sx + i * GLDX + k) = make_double2(-v.x, -v.y);
-    }
-    for (int e = tid; e < NB * GBN / 2; e += 256) {
-        const int k = e / (GBN / 2), j = (e % (GBN / 2)) * 2;
-        double2 v = make_double2(0.0, 0.0);
-        if (tc + j < a.cols)
-            v = *reinterpret_cast<const double2*>(a.Y + base + int64_t(a.kc + k) * a.np + a.cc + tc + j);
-        *reinterpret_cast<double2*>(sy + k * GLDY + j) = v;
-    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const double* px = sx + (wm * 32 + r) * GLDX + q;
     const double* py = sy + q * GLDY + wn * 32 + r;
@@ -491,7 +504,7 @@ __global__ void __launch_bounds__(256, 2) gemm_sub_kernel(SubArgs a) {
             const int col = tc + wn * 32 + j * 8 + 2 * q;
             if (col >= a.cols) continue;
             *reinterpret_cast<double2*>(a.C + base + int64_t(a.rc + row) * a.np + a.cc + col) =
-                make_double2(acc[i][j][0], acc[i][j][1]);
+                make_double2(-acc[i][j][0], -acc[i][j][1]);
         }
     }
 }
