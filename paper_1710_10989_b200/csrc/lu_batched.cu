@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(COL_THREADS) lu_col_kernel(
 
 // Whole-panel factorisation for np - c0 <= 512: one cluster of G = ceil((np -
 // c0) / 64) CTAs per matrix, CTA b holding rows [c0 + 64b, c0 + 64b + 64) of
-// the panel in registers (warp w, slot t: row c0 + 64b + w + 8t; lane: columns
+// the panel in registers (4 warps; warp w, slot t: row c0 + 64b + w + 4t; lane: columns
 // lane and 32 + lane), so the panel is read and written once instead of once
 // per column. Per column: CTA-local best candidate -> cluster barrier -> every
 // CTA reduces the G candidates (DSMEM) in rank order to the same pivot -> the
@@ -203,8 +203,15 @@ __device__ __forceinline__ double slot(const double (&v)[R], int idx) {
     for (int t = 0; t < R; ++t) acc |= __double_as_longlong(v[t]) & -static_cast<long long>(t == idx);
     return __longlong_as_double(acc);
 }
+#ifndef MEXP_PANEL_WARPS
+#define MEXP_PANEL_WARPS 4
+#endif
+#ifndef MEXP_PANEL_MINB
+#define MEXP_PANEL_MINB 4
+#endif
+constexpr int PANEL_THREADS = 32 * MEXP_PANEL_WARPS;
 template <int G>
-__global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(COL_THREADS, 3)
+__global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(PANEL_THREADS, MEXP_PANEL_MINB)
     lu_panel_cluster_kernel(double* __restrict__ Mb, int np, const int32_t* __restrict__ list, int c0,
                             int* __restrict__ piv, mexp_selection* __restrict__ sel) {
     namespace cg = cooperative_groups;
@@ -213,7 +220,7 @@ __global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(COL_THREADS, 3)
     const int64_t m = list[blockIdx.y];
     double* M = Mb + m * int64_t(np) * np;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int W = COL_THREADS / 32, RPW = COL_ROWS / W;
+    constexpr int W = PANEL_THREADS / 32, RPW = COL_ROWS / W;
     __shared__ double cand_v, cand_d;   // this CTA's best |value| and (CTA 0) |diagonal|
     __shared__ int cand_r;
     __shared__ double wv[W];
@@ -253,8 +260,8 @@ __global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(COL_THREADS, 3)
             }
             wv[warp] = best;
             wr[warp] = brow;
-            if (b == 0 && warp == (j & 7)) {
-                cand_d = fabs(pick(hi, slot(v0, j >> 3), slot(v1, j >> 3)));
+            if (b == 0 && warp == (j & (W - 1))) {
+                cand_d = fabs(pick(hi, slot(v0, j / W), slot(v1, j / W)));
             }
         }
         __syncthreads();
@@ -304,20 +311,20 @@ __global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(COL_THREADS, 3)
                 d[32 + lane] = a1;
             }
         }
-        if (p != c && b == 0 && warp == (j & 7)) {
+        if (p != c && b == 0 && warp == (j & (W - 1))) {
             double* d = cluster.map_shared_rank(crow, pb);
-            d[lane] = slot(v0, j >> 3);
-            d[32 + lane] = slot(v1, j >> 3);
+            d[lane] = slot(v0, j / W);
+            d[32 + lane] = slot(v1, j / W);
         }
         cluster.sync();
         // 4. swap, then eliminate column j from the rows below c
         if (p != c) {
-            const bool own_c = b == 0 && warp == (j & 7), own_p = b == pb && warp == pw;
+            const bool own_c = b == 0 && warp == (j & (W - 1)), own_p = b == pb && warp == pw;
             const double pr0 = prow[lane], pr1 = prow[32 + lane];
             const double cr0 = crow[lane], cr1 = crow[32 + lane];
 #pragma unroll
             for (int t = 0; t < RPW; ++t) {
-                const bool tc = own_c && t == (j >> 3), tp = own_p && t == pt;
+                const bool tc = own_c && t == (j / W), tp = own_p && t == pt;
                 v0[t] = pick(tc, pick(tp, v0[t], cr0), pr0);
                 v1[t] = pick(tc, pick(tp, v1[t], cr1), pr1);
             }
@@ -531,7 +538,7 @@ int sub(double* C, const double* X, const double* Y, int rc, int cc, int kc, int
 template <int G>
 void launch_panel(double* M, int np, const int32_t* list, int count, int c0, int* piv,
                   mexp_selection* sel, cudaStream_t st) {
-    lu_panel_cluster_kernel<G><<<dim3(G, count), COL_THREADS, 0, st>>>(M, np, list, c0, piv, sel);
+    lu_panel_cluster_kernel<G><<<dim3(G, count), PANEL_THREADS, 0, st>>>(M, np, list, c0, piv, sel);
 }
 
 int panel_cluster(double* M, int np, const int32_t* list, int count, int c0, int G, int* piv,
