@@ -182,11 +182,13 @@ __global__ void __launch_bounds__(COL_THREADS) lu_col_kernel(
 // c0) / 64) CTAs per matrix, CTA b holding rows [c0 + 64b, c0 + 64b + 64) of
 // the panel in registers (4 warps; warp w, slot t: row c0 + 64b + w + 4t; lane: columns
 // lane and 32 + lane), so the panel is read and written once instead of once
-// per column. Per column: CTA-local best candidate -> cluster barrier -> every
-// CTA reduces the G candidates (DSMEM) in rank order to the same pivot -> the
-// pivot row is broadcast (DSMEM stores) and the displaced row c sent to the
-// pivot's owner -> cluster barrier -> swap and eliminate. The arithmetic, the
-// pivot rule and the swaps are lu_col_kernel's, so the factors are bit-equal.
+// per column. Per column, each CTA posts in its shared memory its best
+// candidate (value, row and row data; CTA 0 also |diagonal| and row c),
+// double-buffered by column parity -> one cluster barrier -> warp 0 of every
+// CTA reduces the G posts (DSMEM) to the same pivot and copies the pivot row
+// (and, at the pivot's owner, old row c) into local shared memory -> swap and
+// eliminate. The arithmetic, the pivot rule and the swaps are lu_col_kernel's,
+// so the factors are bit-equal.
 constexpr int PANEL_MAX_CTAS = 8;
 // a value select that keeps both arrays in registers (a ternary on two array
 // elements can become a select of the array addresses, i.e. local memory)
@@ -221,11 +223,9 @@ __global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(PANEL_THREADS, MEXP_
     double* M = Mb + m * int64_t(np) * np;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int W = PANEL_THREADS / 32, RPW = COL_ROWS / W;
-    __shared__ double cand_v, cand_d;   // this CTA's best |value| and (CTA 0) |diagonal|
-    __shared__ int cand_r;
     __shared__ double wv[W];
     __shared__ int wr[W];
-    __shared__ __align__(16) double prow[NB];  // the pivot row (new row c), from its owner
+    __shared__ __align__(16) double prow[NB];  // the pivot row (new row c), copied from its post
     __shared__ __align__(16) double crow[NB];  // old row c, at the pivot's owner
     __shared__ int s_p;
     const int rb = c0 + COL_ROWS * b;  // first row of this CTA
@@ -240,10 +240,17 @@ __global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(PANEL_THREADS, MEXP_
             v1[t] = row[32 + lane];
         }
     }
+    // posts, double-buffered by column parity: this CTA's best candidate
+    // (value, row, row data) and, in CTA 0, |diagonal| and row c
+    __shared__ double post_v[2], post_d[2];
+    __shared__ int post_r[2];
+    __shared__ __align__(16) double post_row[2][NB];
+    __shared__ __align__(16) double post_crow[2][NB];
+    __shared__ int s_w, s_t, s_q;
     for (int j = 0; j < NB; ++j) {
-        const int c = c0 + j;
+        const int c = c0 + j, par = j & 1;
         const bool hi = j >= 32;  // column j is in v1 (lanes hold columns lane, 32 + lane)
-        // 1. local candidates: the lane holding column j scans its warp's rows >= c
+        const bool own_c = b == 0 && warp == (j & (W - 1));
         if (lane == (j & 31)) {
             double best = -1.0;
             int brow = np;
@@ -260,9 +267,11 @@ __global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(PANEL_THREADS, MEXP_
             }
             wv[warp] = best;
             wr[warp] = brow;
-            if (b == 0 && warp == (j & (W - 1))) {
-                cand_d = fabs(pick(hi, slot(v0, j / W), slot(v1, j / W)));
-            }
+            if (own_c) post_d[par] = fabs(pick(hi, slot(v0, j / W), slot(v1, j / W)));
+        }
+        if (own_c) {
+            post_crow[par][lane] = slot(v0, j / W);
+            post_crow[par][32 + lane] = slot(v1, j / W);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -273,64 +282,74 @@ __global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(PANEL_THREADS, MEXP_
                     best = wv[w];
                     brow = wr[w];
                 }
-            cand_v = best;
-            cand_r = brow;
+            post_v[par] = best;
+            post_r[par] = brow;
+            s_w = brow < np ? (brow - rb) & (W - 1) : -1;
+            s_t = brow < np ? (brow - rb) / W : 0;
+        }
+        __syncthreads();
+        if (warp == s_w) {
+            post_row[par][lane] = slot(v0, s_t);
+            post_row[par][32 + lane] = slot(v1, s_t);
         }
         cluster.sync();
-        // 2. the pivot, identically in every CTA
-        if (threadIdx.x == 0) {
+        // warp 0: the pivot from the G posts (lane q reads CTA q's), then the
+        // pivot row and, at the pivot's owner, old row c into local memory
+        if (warp == 0) {
             double bv = -1.0;
-            int br = np;
-            for (int q = 0; q < G; ++q) {
-                const double v = *cluster.map_shared_rank(&cand_v, q);
-                const int r = *cluster.map_shared_rank(&cand_r, q);
-                if (better(v, r, bv, br)) {
-                    bv = v;
-                    br = r;
+            int br = np, bq = 0;
+            if (lane < G) {
+                bv = *cluster.map_shared_rank(&post_v[par], lane);
+                br = *cluster.map_shared_rank(&post_r[par], lane);
+                bq = lane;
+            }
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int orow = __shfl_xor_sync(0xffffffffu, br, o);
+                const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+                if (better(ov, orow, bv, br)) {
+                    bv = ov;
+                    br = orow;
+                    bq = oq;
                 }
             }
-            const double dk = *cluster.map_shared_rank(&cand_d, 0);
+            const double dk = *cluster.map_shared_rank(&post_d[par], 0);
             int p = br;
-            if (dk != dk) p = c;  // a NaN diagonal: the reference's scan never moves
-            else if (bv == 0.0) {  // "singular denominator" (kernels.cpp:71-72)
+            if (dk != dk || bv == 0.0) {  // NaN diagonal / "singular denominator"
                 p = c;
-                if (b == 0) sel[m].status = MEXP_ERR_SINGULAR;
+                bq = 0;
             }
-            if (b == 0) piv[m * int64_t(np) + c] = p;
-            s_p = p;
+            if (b == 0 && lane == 0) {
+                piv[m * int64_t(np) + c] = p;
+                if (dk == dk && bv == 0.0) sel[m].status = MEXP_ERR_SINGULAR;
+            }
+            const double* src = p == c ? cluster.map_shared_rank(post_crow[par], 0)
+                                       : cluster.map_shared_rank(post_row[par], bq);
+            prow[lane] = src[lane];
+            prow[32 + lane] = src[32 + lane];
+            if (p != c && b == bq) {
+                const double* cr = cluster.map_shared_rank(post_crow[par], 0);
+                crow[lane] = cr[lane];
+                crow[32 + lane] = cr[32 + lane];
+            }
+            if (lane == 0) s_p = p;
         }
         __syncthreads();
         const int p = s_p;
-        const int pb = (p - c0) / COL_ROWS, pw = (p - rb) & (W - 1), pt = ((p - c0) % COL_ROWS) / W;
-        // 3. broadcast the pivot row; send row c to the pivot's owner
-        if (b == pb && warp == pw) {
-            const double a0 = slot(v0, pt), a1 = slot(v1, pt);
-            for (int q = 0; q < G; ++q) {
-                double* d = cluster.map_shared_rank(prow, q);
-                d[lane] = a0;
-                d[32 + lane] = a1;
-            }
-        }
-        if (p != c && b == 0 && warp == (j & (W - 1))) {
-            double* d = cluster.map_shared_rank(crow, pb);
-            d[lane] = slot(v0, j / W);
-            d[32 + lane] = slot(v1, j / W);
-        }
-        cluster.sync();
-        // 4. swap, then eliminate column j from the rows below c
+        const double u0 = prow[lane], u1 = prow[32 + lane];
         if (p != c) {
-            const bool own_c = b == 0 && warp == (j & (W - 1)), own_p = b == pb && warp == pw;
-            const double pr0 = prow[lane], pr1 = prow[32 + lane];
+            const int pb = (p - c0) / COL_ROWS, pw = (p - rb) & (W - 1), pt = ((p - c0) % COL_ROWS) / W;
+            const bool own_p = b == pb && warp == pw;
             const double cr0 = crow[lane], cr1 = crow[32 + lane];
 #pragma unroll
             for (int t = 0; t < RPW; ++t) {
                 const bool tc = own_c && t == (j / W), tp = own_p && t == pt;
-                v0[t] = pick(tc, pick(tp, v0[t], cr0), pr0);
-                v1[t] = pick(tc, pick(tp, v1[t], cr1), pr1);
+                v0[t] = pick(tc, pick(tp, v0[t], cr0), u0);
+                v1[t] = pick(tc, pick(tp, v1[t], cr1), u1);
             }
         }
         const double pv = prow[j];
-        const double u0 = prow[lane], u1 = prow[32 + lane];
 #pragma unroll
         for (int t = 0; t < RPW; ++t) {
             const int r = rb + warp + W * t;
@@ -346,6 +365,7 @@ __global__ void __cluster_dims__(G, 1, 1) __launch_bounds__(PANEL_THREADS, MEXP_
                 if (lane > (j & 31)) v1[t] = fma(-l, u1, v1[t]);
             }
         }
+        __syncthreads();  // prow / crow / s_p are rewritten in the next column
     }
 #pragma unroll
     for (int t = 0; t < RPW; ++t) {
