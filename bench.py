@@ -208,7 +208,9 @@ def per_worker_sample(key):
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--steps", type=int, default=None,
+                   help="timed steps (default per config: a timed region of ~0.1-1 s so clock samples "
+                        "and transients average out; the reference arm: 20)")
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--config", default="cfg2", choices=sorted(workloads.CONFIGS))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -220,7 +222,11 @@ def parse():
     p.add_argument("--strong", action="store_true",
                    help="split the config's batch across the ranks (strong scaling) instead of "
                         "one full batch per rank (weak, the default)")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.steps is None:
+        a.steps = 20 if a.impl == "reference" else {"cfg1": 1000, "cfg2": 1000, "cfg3": 300,
+                                                     "cfg4": 10, "cfg5": 3}[a.config]
+    return a
 
 
 def dist_env():
