@@ -59,6 +59,40 @@ def test_cfg4_subset(cuda, oracle):
     assert err.max() <= tol
 
 
+def test_cfg4_full_batch_properties(cuda):
+    """All 1,024 cfg4 matrices at full size, through size-independent
+    properties: e^A e^-A = I within 50 n u of ||e^A|| ||e^-A|| (the GEMM
+    check in fp64 on the device), (m, s) of -A equal to those of A (same
+    1-norm), and the selection records bit-equal to the host's mexp_select
+    on the same norms."""
+    import torch
+    a = torch.from_numpy(workloads.generate("cfg4")).cuda()
+    B, n, _ = a.shape
+    e1, e2 = torch.empty_like(a), torch.empty_like(a)
+    s1 = torch.empty(16 * B, dtype=torch.uint8, device="cuda")
+    s2 = torch.empty_like(s1)
+    mx.expm_batched(a, e1, s1)
+    mx.expm_batched(-a, e2, s2)
+    torch.cuda.synchronize()
+    r1 = s1.cpu().numpy().view(mx.SELECTION_DTYPE)
+    r2 = s2.cpu().numpy().view(mx.SELECTION_DTYPE)
+    assert (r1["status"] == 0).all() and (r2["status"] == 0).all()
+    assert np.array_equal(r1.view(np.uint8), r2.view(np.uint8))
+    table = mx.selection_table(mx.Family.TaylorNew, mx.Accuracy.Double)
+    for i in range(0, B, 97):
+        assert mx.select(float(r1["norm_in"][i]), table) == (r1["degree"][i], r1["s"][i])
+    tol = workloads.CONFIGS["cfg4"].tolerance
+    eye = torch.eye(n, dtype=a.dtype, device="cuda")
+    worst = 0.0
+    for c in range(0, B, 64):
+        p = torch.bmm(e1[c:c + 64], e2[c:c + 64]) - eye
+        rel = torch.linalg.matrix_norm(p) / (torch.linalg.matrix_norm(e1[c:c + 64]) *
+                                              torch.linalg.matrix_norm(e2[c:c + 64]))
+        worst = max(worst, float(rel.max()))
+    print(f"cfg4 full batch: max ||e^A e^-A - I|| / (||e^A|| ||e^-A||) = {worst:.3e} (tol {tol:.3e})")
+    assert worst <= tol
+
+
 def test_cfg5_leading_block_and_structure(cuda, oracle):
     """cfg5 (8192^2, upper triangular + U(-5,0) diagonal, ||A||_1 = 30) is
     too large for the CPU oracle; checked through size-independent properties:
