@@ -93,6 +93,28 @@ def test_cfg4_full_batch_properties(cuda):
     assert worst <= tol
 
 
+def test_cfg5_full_size_inverse_property(cuda):
+    """The whole 8192 x 8192 cfg5 matrix: e^A e^-A = I within 50 n u of
+    ||e^A|| ||e^-A|| (cuBLAS fp64 GEMM as the checker), same (m, s) for -A."""
+    import torch
+    a = torch.from_numpy(workloads.generate("cfg5")).cuda()
+    e1, e2 = torch.empty_like(a), torch.empty_like(a)
+    s1 = torch.empty(16, dtype=torch.uint8, device="cuda")
+    s2 = torch.empty_like(s1)
+    mx.expm_batched(a, e1, s1)
+    mx.expm_batched(-a, e2, s2)
+    torch.cuda.synchronize()
+    r1 = s1.cpu().numpy().view(mx.SELECTION_DTYPE)
+    r2 = s2.cpu().numpy().view(mx.SELECTION_DTYPE)
+    assert (r1["degree"][0], r1["s"][0]) == (r2["degree"][0], r2["s"][0]) == (18, 5)
+    p = torch.matmul(e1[0], e2[0])
+    p.diagonal().sub_(1.0)
+    rel = float(torch.linalg.matrix_norm(p) / (torch.linalg.matrix_norm(e1[0]) * torch.linalg.matrix_norm(e2[0])))
+    tol = workloads.CONFIGS["cfg5"].tolerance
+    print(f"cfg5: ||e^A e^-A - I|| / (||e^A|| ||e^-A||) = {rel:.3e} (tol {tol:.3e})")
+    assert rel <= tol
+
+
 def test_cfg5_leading_block_and_structure(cuda, oracle):
     """cfg5 (8192^2, upper triangular + U(-5,0) diagonal, ||A||_1 = 30) is
     too large for the CPU oracle; checked through size-independent properties:
