@@ -579,10 +579,122 @@ int panel_cluster(double* M, int np, const int32_t* list, int count, int c0, int
     return MEXP_OK;
 }
 
+// T^-1 for the NB x NB diagonal block T of M at (r0, r0) (unit lower or
+// upper), one column per thread by substitution on e_j, into W (list
+// position z: W + z NB^2, row-major).
+template <bool kLower>
+__global__ void __launch_bounds__(NB) tri_inv_kernel(const double* __restrict__ Mb, int np,
+                                                     const int32_t* __restrict__ list, int r0,
+                                                     double* __restrict__ Wb) {
+    const int64_t m = list[blockIdx.y];
+    const double* M = Mb + m * int64_t(np) * np;
+    double* W = Wb + int64_t(blockIdx.y) * NB * NB;
+    __shared__ __align__(16) double T[NB][NB + 2];
+    for (int e = threadIdx.x; e < NB * NB / 2; e += NB) {
+        const int i = e / (NB / 2), k = (e % (NB / 2)) * 2;
+        cp_async16_z(&T[i][k], M + int64_t(r0 + i) * np + r0 + k, true);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const int j = threadIdx.x;
+    double x[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) x[i] = i == j ? 1.0 : 0.0;
+    if constexpr (kLower) {
+#pragma unroll
+        for (int i = 1; i < NB; ++i)
+#pragma unroll
+            for (int q = 0; q < i; ++q) x[i] = fma(-T[i][q], x[q], x[i]);
+    } else {
+#pragma unroll
+        for (int i = NB - 1; i >= 0; --i) {
+#pragma unroll
+            for (int q = i + 1; q < NB; ++q) x[i] = fma(-T[i][q], x[q], x[i]);
+            x[i] = x[i] / T[i][i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) W[i * NB + j] = x[i];
+}
+
+// X[r0 .. r0 + NB) x [cb + 64 bx, ..+64) <- W_z X (in place: a CTA loads its
+// whole 64-column tile before it stores) on DMMA; 8 warps of 16 x 32.
+constexpr int TM_LD = NB + 4;
+constexpr size_t TRI_MM_SMEM = size_t(2) * NB * TM_LD * sizeof(double);
+__global__ void __launch_bounds__(256) tri_mm_kernel(const double* __restrict__ Wb, double* __restrict__ Xb,
+                                                     int np, const int32_t* __restrict__ list, int r0,
+                                                     int cb) {
+    extern __shared__ __align__(16) double tsm[];
+    double* sw = tsm;               // NB x TM_LD
+    double* sxt = tsm + NB * TM_LD;  // NB x TM_LD
+    const int64_t m = list[blockIdx.y];
+    double* X = Xb + m * int64_t(np) * np;
+    const double* W = Wb + int64_t(blockIdx.y) * NB * NB;
+    const int c0 = cb + 64 * blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < NB * NB / 2; e += 256) {
+        const int i = e / (NB / 2), k = (e % (NB / 2)) * 2;
+        cp_async16_z(sw + i * TM_LD + k, W + i * NB + k, true);
+        cp_async16_z(sxt + i * TM_LD + k, X + int64_t(r0 + i) * np + c0 + k, true);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps of 16 x 32
+    const int r = lane >> 2, q = lane & 3;
+    double acc[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const double* pa = sw + (16 * wm + r) * TM_LD + q;
+    const double* pb = sxt + q * TM_LD + 32 * wn + r;
+#pragma unroll 4
+    for (int k = 0; k < NB; k += 4) {
+        double af[2], bf[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) af[i] = pa[8 * i * TM_LD + k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = pb[k * TM_LD + 8 * j];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();  // every warp is done reading the tile before it is overwritten
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<double2*>(X + int64_t(r0 + 16 * wm + 8 * i + r) * np + c0 + 32 * wn + 8 * j + 2 * q) =
+                make_double2(acc[i][j][0], acc[i][j][1]);
+}
+
 template <bool kLower>
 int trsm(const double* M, double* X, int np, const int32_t* list, int count, int r0, int cb,
-         int ncols, cudaStream_t st, std::atomic<uint64_t>* launches) {
+         int ncols, cudaStream_t st, std::atomic<uint64_t>* launches, double* W = nullptr) {
     if (ncols <= 0) return MEXP_OK;
+    // DMMA path (MEXP_TRSM_DMMA=0: per-column substitution): T^-1 by
+    // substitution on the identity, then X <- T^-1 X on the tensor pipe
+    static const bool dmma_path = [] {
+        const char* e = std::getenv("MEXP_TRSM_DMMA");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (dmma_path && W && ncols % 64 == 0) {
+        static bool attr = [] {
+            cudaFuncSetAttribute(tri_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TRI_MM_SMEM));
+            return true;
+        }();
+        (void)attr;
+        for (int z0 = 0; z0 < count; z0 += 65535) {
+            const int zc = std::min(count - z0, 65535);
+            tri_inv_kernel<kLower><<<dim3(1, zc), NB, 0, st>>>(M, np, list + z0, r0, W);
+            tri_mm_kernel<<<dim3(ncols / 64, zc), 256, TRI_MM_SMEM, st>>>(W, X, np, list + z0, r0, cb);
+            launches->fetch_add(2, std::memory_order_relaxed);
+        }
+        return MEXP_OK;
+    }
     for (int z0 = 0; z0 < count; z0 += 65535) {
         const dim3 grid((ncols + TRSM_THREADS - 1) / TRSM_THREADS, std::min(count - z0, 65535));
         trsm_kernel<kLower><<<grid, TRSM_THREADS, 0, st>>>(M, X, np, list + z0, r0, cb, ncols);
@@ -607,6 +719,10 @@ int lu_solve_batched(double* M, double* R, int np, int64_t batch, const int32_t*
     const size_t ct_b = sizeof(unsigned) * size_t(batch);
     AsyncBuffer scratch_buf(st);
     LUCUDA(scratch_buf.alloc(piv_b + pv_b + pr_b + ct_b + 64));
+    // the diagonal blocks' inverses for the DMMA triangular solves
+    AsyncBuffer tinv_buf(st);
+    LUCUDA(tinv_buf.alloc(sizeof(double) * size_t(count) * NB * NB));
+    double* tinv = tinv_buf.get<double>();
     char* scratch = scratch_buf.get<char>();
     double* part_v = reinterpret_cast<double*>(scratch);
     int* piv = reinterpret_cast<int*>(scratch + pv_b);
@@ -636,19 +752,19 @@ int lu_solve_batched(double* M, double* R, int np, int64_t batch, const int32_t*
         launches->fetch_add(1, std::memory_order_relaxed);
         const int rest = np - c0 - NB;
         if (rest > 0) {
-            if ((r = trsm<true>(M, M, np, d_list, count, c0, c0 + NB, rest, st, launches))) return r;
+            if ((r = trsm<true>(M, M, np, d_list, count, c0, c0 + NB, rest, st, launches, tinv))) return r;
             if ((r = sub(M, M, M, c0 + NB, c0 + NB, c0, rest, rest, np, d_list, count, st, launches)))
                 return r;
         }
     }
     // forward: L Y = P R
     for (int j = 0; j < np; j += NB) {
-        if ((r = trsm<true>(M, R, np, d_list, count, j, 0, np, st, launches))) return r;
+        if ((r = trsm<true>(M, R, np, d_list, count, j, 0, np, st, launches, tinv))) return r;
         if ((r = sub(R, M, R, j + NB, 0, j, np - j - NB, np, np, d_list, count, st, launches))) return r;
     }
     // backward: U X = Y
     for (int j = np - NB; j >= 0; j -= NB) {
-        if ((r = trsm<false>(M, R, np, d_list, count, j, 0, np, st, launches))) return r;
+        if ((r = trsm<false>(M, R, np, d_list, count, j, 0, np, st, launches, tinv))) return r;
         if ((r = sub(R, M, R, 0, 0, j, j, np, np, d_list, count, st, launches))) return r;
     }
     LUCUDA(cudaGetLastError());
