@@ -130,9 +130,18 @@ class ClockSampler:
         if self.nv:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            # the first sample is taken before the timed work starts
+            t0 = time.perf_counter()
+            while not self.samples and time.perf_counter() - t0 < 0.05:
+                time.sleep(0.0005)
         return self
 
     def __exit__(self, *a):
+        if self.nv:
+            try:  # one sample at the end of the timed region as well
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            except Exception:
+                pass
         self._stop.set()
         if self.nv:
             self.t.join()
