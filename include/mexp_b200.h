@@ -137,6 +137,24 @@ int mexp_expm_batched_host(const void* h_a, void* h_out, int dtype, int n, int64
                            int accuracy, int family, int rounding, mexp_selection* h_sel,
                            int64_t* first_error);
 
+/* mexp_expm_batched_host sharded by matrix across several GPUs of this node
+ * (the reference's only parallelism is the OpenMP
+ * row split of one product, kernels.cpp:16-27, so the split is this path's
+ * own). Device k of `devices` (k = 0..ndevices-1) owns the contiguous range
+ * [k*B/G + min(k, B%G), ...) -- the first B%G devices one matrix more -- and
+ * runs the single-device host pipeline on its own host thread, i.e. over its
+ * own PCIe link; no data moves between GPUs. Results, records and the
+ * returned status / *first_error (lowest failing global index) equal those of
+ * the single-device call bit for bit. devices == NULL or ndevices <= 0 uses
+ * every visible device. A device may appear more than once (its shards then
+ * run one after another). */
+int mexp_expm_batched_host_multi(const void* h_a, void* h_out, int dtype, int n, int64_t batch,
+                                 int accuracy, int family, int rounding, mexp_selection* h_sel,
+                                 int64_t* first_error, const int* devices, int ndevices);
+
+/* Number of CUDA devices this library can use (0 without a driver/device). */
+int mexp_device_count(void);
+
 /* mexp::squarings (expm.hpp:21, expm.cpp:31-35) on device: X <- X^(2^s) for
  * each of `batch` fp64 matrices, in place, s squarings each. */
 int mexp_squarings_batched(double* d_x, int n, int64_t batch, int s, int rounding,

@@ -9,6 +9,8 @@ proj/include/mexp/expm.hpp, theta_tables.hpp) over the C ABI in
 * ``selection_table(family, accuracy)``            theta_tables.hpp:32
 * ``expm_batched(a, out, ...)``                    batched, device tensors
 * ``expm_batched_host(a, ...)``                    batched, host arrays (e2e)
+* ``expm_batched_host_multi(a, devices=...)``      the same, sharded by matrix
+                                                   across several GPUs
 
 Errors follow the reference: ``std::invalid_argument`` becomes ``ValueError``
 with the reference's message. There is no CPU fallback: without the CUDA
@@ -123,6 +125,8 @@ def library() -> C.CDLL:
         "mexp_expm_batched": (I, [P, P, I, I, I64, I, I, I, P, P]),
         "mexp_expm_batched_host": (I, [P, P, I, I, I64, I, I, I, P, P]),
         "mexp_squarings_batched": (I, [P, I, I64, I, I, P]),
+        "mexp_expm_batched_host_multi": (I, [P, P, I, I, I64, I, I, I, P, P, P, I]),
+        "mexp_device_count": (I, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -136,6 +140,7 @@ EXPORTED_SYMBOLS = (
     "mexp_abi_version", "mexp_device_check", "mexp_status_string", "mexp_last_cuda_error",
     "mexp_launch_count", "mexp_unit_roundoff", "mexp_selection_table", "mexp_select",
     "mexp_expm", "mexp_expm_batched", "mexp_expm_batched_host", "mexp_squarings_batched",
+    "mexp_expm_batched_host_multi", "mexp_device_count",
 )
 
 
@@ -209,10 +214,21 @@ def expm_batched(a, out, sel=None, accuracy: Accuracy = Accuracy.Double,
     records). Asynchronous on ``stream`` (default: torch's current stream).
     """
     import torch
-    assert a.is_cuda and out.is_cuda and a.is_contiguous() and out.is_contiguous()
-    batch, n, n2 = a.shape
-    if n != n2 or out.shape != a.shape or out.dtype != a.dtype:
+    if not (a.is_cuda and out.is_cuda):
+        raise ValueError("expm_batched takes CUDA tensors (expm_batched_host takes host buffers)")
+    if a.dim() != 3 or a.shape[1] != a.shape[2]:
+        raise ValueError("a must be a (batch, n, n) stack of square matrices")
+    batch, n, _ = a.shape
+    if out.shape != a.shape or out.dtype != a.dtype:
         raise ValueError("dimension mismatch")
+    if not (a.is_contiguous() and out.is_contiguous()):
+        raise ValueError("a and out must be contiguous")
+    if a.device != out.device or a.device.index != torch.cuda.current_device():
+        raise ValueError("a and out must live on the current CUDA device")
+    if sel is not None and (not sel.is_cuda or sel.device != a.device or not sel.is_contiguous()
+                            or sel.numel() * sel.element_size() < SELECTION_DTYPE.itemsize * batch):
+        raise ValueError(f"sel must be a contiguous device buffer of >= {SELECTION_DTYPE.itemsize} "
+                         "bytes per matrix on a's device")
     if stream is None:
         stream = torch.cuda.current_stream(a.device)
     st = library().mexp_expm_batched(a.data_ptr(), out.data_ptr(), _dtype_code(a.dtype), n,
@@ -237,6 +253,53 @@ def _pinned_selection(batch: int):
     return buf
 
 
+def _host_args(a, out):
+    """Validate host (numpy or CPU torch) buffers; returns (a, out, ptrs, batch, n, dtype code)."""
+    if isinstance(a, np.ndarray):
+        if a.ndim != 3 or a.shape[1] != a.shape[2]:
+            raise ValueError("a must be a (batch, n, n) stack of square matrices")
+        a = np.ascontiguousarray(a)
+        dt = _dtype_code(a.dtype)
+        if out is None:
+            out = np.empty_like(a)
+        elif not isinstance(out, np.ndarray) or out.shape != a.shape or out.dtype != a.dtype \
+                or not out.flags.c_contiguous or not out.flags.writeable:
+            raise ValueError("out must be a writeable C-contiguous array of a's shape and dtype")
+        return a, out, a.ctypes.data, out.ctypes.data, a.shape[0], a.shape[1], dt
+    import torch
+    if not isinstance(a, torch.Tensor) or a.is_cuda:
+        raise ValueError("expm_batched_host takes host buffers (numpy arrays or CPU tensors)")
+    if a.dim() != 3 or a.shape[1] != a.shape[2]:
+        raise ValueError("a must be a (batch, n, n) stack of square matrices")
+    a = a.contiguous()
+    dt = _dtype_code(a.dtype)
+    if out is None:
+        out = a.new_empty(a.shape)
+    elif not isinstance(out, torch.Tensor) or out.is_cuda or out.shape != a.shape \
+            or out.dtype != a.dtype or not out.is_contiguous():
+        raise ValueError("out must be a contiguous CPU tensor of a's shape and dtype")
+    return a, out, a.data_ptr(), out.data_ptr(), a.shape[0], a.shape[1], dt
+
+
+def _host_sel(a, batch, sel_out):
+    if isinstance(a, np.ndarray):
+        sel = np.zeros(batch, SELECTION_DTYPE)
+        return sel, sel.ctypes.data
+    import torch
+    # pinned like the caller's tensors, so the records are DMA'd straight
+    # in; the pinned buffer is cached (cudaHostAlloc costs ~ms per call)
+    if sel_out is None:
+        sel_t = _pinned_selection(batch) if a.is_pinned() else \
+            torch.empty(batch * SELECTION_DTYPE.itemsize, dtype=torch.uint8)
+    else:
+        if not isinstance(sel_out, torch.Tensor) or sel_out.is_cuda or sel_out.dtype != torch.uint8 \
+                or not sel_out.is_contiguous() or sel_out.numel() < batch * SELECTION_DTYPE.itemsize:
+            raise ValueError(f"sel_out must be a contiguous CPU uint8 tensor of >= "
+                             f"{SELECTION_DTYPE.itemsize} bytes per matrix")
+        sel_t = sel_out
+    return sel_t.numpy().view(SELECTION_DTYPE)[:batch], sel_t.data_ptr()
+
+
 def expm_batched_host(a, out=None, accuracy: Accuracy = Accuracy.Double,
                       rounding: int = ROUND_AUTO, family: Family = Family.TaylorNew,
                       raise_on_error: bool = True, sel_out=None):
@@ -248,41 +311,37 @@ def expm_batched_host(a, out=None, accuracy: Accuracy = Accuracy.Double,
 
     Returns (out, selection records as a numpy structured array, status).
     """
-    is_np = isinstance(a, np.ndarray)
-    if is_np:
-        a = np.ascontiguousarray(a)
-        if out is None:
-            out = np.empty_like(a)
-        pa, po = a.ctypes.data, out.ctypes.data
-        batch, n, _ = a.shape
-        dt = _dtype_code(a.dtype)
-    else:
-        if out is None:
-            out = a.new_empty(a.shape)
-        pa, po = a.data_ptr(), out.data_ptr()
-        batch, n, _ = a.shape
-        dt = _dtype_code(a.dtype)
-    if is_np:
-        sel = np.zeros(batch, SELECTION_DTYPE)
-        psel = sel.ctypes.data
-    else:
-        # pinned like the caller's tensors, so the records are DMA'd straight
-        # in; the pinned buffer is cached (cudaHostAlloc costs ~ms per call)
-        if sel_out is None:
-            sel_t = _pinned_selection(batch) if a.is_pinned() else None
-            if sel_t is None:
-                import torch
-                sel_t = torch.empty(batch * SELECTION_DTYPE.itemsize, dtype=torch.uint8)
-        else:
-            sel_t = sel_out
-        sel = sel_t.numpy().view(SELECTION_DTYPE)[:batch]
-        psel = sel_t.data_ptr()
+    a, out, pa, po, batch, n, dt = _host_args(a, out)
+    sel, psel = _host_sel(a, batch, sel_out)
     first = C.c_int64(-1)
     st = library().mexp_expm_batched_host(pa, po, dt, n, batch, int(accuracy), int(family),
                                           int(rounding), psel, C.byref(first))
     if st not in (OK, ERR_NONFINITE, ERR_NORM_NONFINITE) or (st != OK and raise_on_error):
         _raise(st)
     return out, sel, st
+
+
+def expm_batched_host_multi(a, out=None, devices=None, accuracy: Accuracy = Accuracy.Double,
+                            rounding: int = ROUND_AUTO, family: Family = Family.TaylorNew,
+                            raise_on_error: bool = True, sel_out=None):
+    """``expm_batched_host`` sharded by matrix across ``devices`` (default: all
+    visible GPUs), one host thread and copy pipeline per GPU
+    (``mexp_expm_batched_host_multi``). Same results, records and status as
+    the single-device call. Returns (out, records, status, first_error)."""
+    a, out, pa, po, batch, n, dt = _host_args(a, out)
+    sel, psel = _host_sel(a, batch, sel_out)
+    devs = None if devices is None else np.ascontiguousarray(devices, dtype=np.int32)
+    first = C.c_int64(-1)
+    st = library().mexp_expm_batched_host_multi(
+        pa, po, dt, n, batch, int(accuracy), int(family), int(rounding), psel, C.byref(first),
+        None if devs is None else devs.ctypes.data, 0 if devs is None else len(devs))
+    if st not in (OK, ERR_NONFINITE, ERR_NORM_NONFINITE) or (st != OK and raise_on_error):
+        _raise(st)
+    return out, sel, st, first.value
+
+
+def device_count() -> int:
+    return int(library().mexp_device_count())
 
 
 def launch_count() -> int:

@@ -40,6 +40,7 @@
 #include <cudaTypedefs.h>
 
 #include "async_buffer.hpp"
+#include "device_once.hpp"
 #include "expm_common.cuh"
 #include "expm_large.cuh"
 #include "lu_batched.cuh"
@@ -658,14 +659,13 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
          cudaStream_t st, std::atomic<uint64_t>* launches, double* final_out = nullptr,
          const double (*lc)[5] = nullptr, int nlc = 0) {
     if (count == 0) return MEXP_OK;
-    static bool attr = [] {
+    static PerDevice attr_once;
+    attr_once([] {
         cudaFuncSetAttribute(gemm_dmma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(GEMM_SMEM));
         cudaFuncSetAttribute(gemm_exact_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(EXACT_SMEM));
-        return true;
-    }();
-    (void)attr;
+    });
     GemmArgs g{};
     g.X = X;
     g.Y = Y;
@@ -738,8 +738,16 @@ Workspace& workspace() {
 const char* large_last_error() { return g_err.c_str(); }
 
 int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user, int n,
-                   int64_t batch, int acc_arg, int rounding, cudaStream_t st,
+                   int64_t batch, int acc_arg, int rounding, int smin, cudaStream_t st,
                    std::atomic<uint64_t>* launches) {
+    // the schedule is built on the host from the selections (one stream
+    // synchronisation per call), which a CUDA-graph capture cannot contain
+    cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+    LCUDA(cudaStreamIsCapturing(st, &capturing));
+    if (capturing != cudaStreamCaptureStatusNone) {
+        g_err = "n > 64 is host-synchronous (schedule from the selections): not capturable";
+        return MEXP_ERR_UNSUPPORTED;
+    }
     const int np = (n + BM - 1) / BM * BM;
     const int64_t mat = int64_t(np) * np;
     const bool pade = (acc_arg >> 4) == MEXP_FAMILY_PADE || (acc_arg >> 4) == kFamilyPadeReference;
@@ -756,6 +764,12 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     const size_t need = size_t(kBuffers) * batch * mat * sizeof(double);
     Workspace& ws = workspace();
     std::lock_guard<std::mutex> ws_lock(ws.mu);  // the call synchronises its stream before returning
+    // error exits too: work already enqueued on `st` still uses the workspace
+    // and the pinned staging, so they are fenced before the lock is released
+    struct SyncOnExit {
+        cudaStream_t s;
+        ~SyncOnExit() { cudaStreamSynchronize(s); }
+    } fence{st};
     if (ws.bytes < need) {
         AsyncBuffer::retain_pool();
         if (ws.buf) LCUDA(cudaFreeAsync(ws.buf, st));
@@ -767,7 +781,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     g_map_batch = batch;
 
     // per-call scratch, released on every exit path
-    AsyncBuffer maxbits_buf(st), sel_buf(st), lists_buf(st), extra_buf(st);
+    AsyncBuffer maxbits_buf(st), sel_buf(st);
     LCUDA(maxbits_buf.alloc(sizeof(unsigned long long) * batch + sizeof(int) * batch));
     unsigned long long* maxbits = maxbits_buf.get<unsigned long long>();
     int* bad = reinterpret_cast<int*>(maxbits + batch);
@@ -777,7 +791,6 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         LCUDA(sel_buf.alloc(sizeof(mexp_selection) * batch));
         d_sel = sel_buf.get<mexp_selection>();
     }
-    int32_t* d_lists = nullptr;
 
     sliced(batch, [&](int64_t y0, unsigned ny) {
         norm_cols_kernel<<<dim3((n + 255) / 256, ny), 256, 0, st>>>(d_a, n, batch, maxbits, bad, y0);
@@ -800,11 +813,33 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     launches->fetch_add(2, std::memory_order_relaxed);
     LCUDA(cudaStreamSynchronize(st));
     const mexp_selection* h_sel = ws.h_sel;
+    // AUTO (Taylor families): a matrix with s >= smin runs every product and
+    // lincomb in the reference's rounding (pass 0, bit-identical to the
+    // reference), the rest on DMMA (pass 1). Squarings amplify the difference
+    // between two roundings of T_m by up to ||X||^2/||X^2|| each, which the
+    // non-normal gallery kinds (rank one at s = 12: 2.5x over 50 n u on DMMA)
+    // make large; tests/test_gpu_auto_stress.py.
+    const bool split_auto = rounding == MEXP_ROUND_AUTO && !pade;
+    const int npasses = split_auto ? 2 : 1;
+    int r = MEXP_OK;
+    for (int pass = 0; pass < npasses; ++pass) {
+    const bool last_pass = pass == npasses - 1;
+    g_exact_n = (rounding == MEXP_ROUND_REFERENCE || (split_auto && pass == 0)) ? n : 0;
+    auto active = [&](int64_t m) {
+        return h_sel[m].status == MEXP_OK && (!split_auto || ((h_sel[m].s >= smin) == (pass == 0)));
+    };
+    bool any = false;
+    for (int64_t m = 0; m < batch && !any; ++m) any = active(m);
+    if (!any && !last_pass) continue;
+    // the host lists' pinned staging is reused by the next pass
+    if (pass > 0) LCUDA(cudaStreamSynchronize(st));
+    AsyncBuffer lists_buf(st), extra_buf(st);
+    int32_t* d_lists = nullptr;
     constexpr int kMaxDeg = 26;
     std::vector<int32_t> by_deg[kMaxDeg + 1];
     int max_s = 0;
     for (int64_t m = 0; m < batch; ++m) {
-        if (h_sel[m].status != MEXP_OK) continue;
+        if (!active(m)) continue;
         by_deg[h_sel[m].degree].push_back(int32_t(m));
         max_s = std::max(max_s, int(h_sel[m].s));
     }
@@ -827,7 +862,6 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     const bool direct = (np == n);
     double* R = W[1];
     double* S = W[2];
-    int r;
     // split a list into (finishing here, continuing) by s == k
     auto split = [&](const std::vector<int32_t>& v, int k) {
         std::vector<int32_t> fin, cont;
@@ -877,8 +911,9 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         sq_flag[k] = flagged(v, k);
     }
     std::vector<int32_t> bad_list, all_list;
-    for (int64_t m = 0; m < batch; ++m)
-        if (h_sel[m].status != MEXP_OK) bad_list.push_back(int32_t(m));
+    if (last_pass)
+        for (int64_t m = 0; m < batch; ++m)
+            if (h_sel[m].status != MEXP_OK) bad_list.push_back(int32_t(m));
     const size_t off_bad = append(bad_list);
     const size_t off_all2 = append(all_ok);
     // host-built lists reach the device through mapped pinned staging and a
@@ -1176,6 +1211,7 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         launches->fetch_add(1, std::memory_order_relaxed);
     }
     LCUDA(cudaGetLastError());
+    }  // passes
     LCUDA(cudaStreamSynchronize(st));  // host lists must outlive their async upload
     return MEXP_OK;
 }

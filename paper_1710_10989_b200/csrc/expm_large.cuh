@@ -14,9 +14,12 @@ namespace mexp_b200 {
 
 // acc_arg = mexp_accuracy | mexp_family << 4; rounding: MEXP_ROUND_REFERENCE
 // runs every product and lincomb in the reference's arithmetic (bit-identical
-// e^A; not for the Pade family), anything else the DMMA path
+// e^A; not for the Pade family), FAST the DMMA path, AUTO the reference's
+// arithmetic for the matrices with s >= smin and DMMA for the rest (Taylor
+// families; Pade is DMMA). Host-synchronous: returns MEXP_ERR_UNSUPPORTED
+// when `st` is capturing a CUDA graph.
 int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel, int n,
-                   int64_t batch, int acc_arg, int rounding, cudaStream_t st,
+                   int64_t batch, int acc_arg, int rounding, int smin, cudaStream_t st,
                    std::atomic<uint64_t>* launches);
 
 // X <- X^(2^s), in place, for `batch` n x n fp64 matrices.

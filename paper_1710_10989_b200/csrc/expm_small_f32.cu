@@ -13,6 +13,7 @@
 // column). The exact 1-norm and the (m, s) selection run in fp64 on the fp32
 // values promoted to double, i.e. exactly the reference's norm of the same
 // data (kernels.cpp:44-53), so (m, s) match bit for bit.
+#include "device_once.hpp"
 #include "expm_small.cuh"
 #include "expm_small_f32.cuh"
 
@@ -425,8 +426,9 @@ int launch_f32(const float* a, float* out, mexp_selection* sel, int64_t batch, i
     using G = GroupF32<N>;
     auto kern = expm_small_f32_kernel<N, GPC, kFamily>;
     const size_t smem = size_t(G::SMEM_FLOATS) * GPC * sizeof(float);
+    static PerDevice attr_once;
+    attr_once([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); });
     static int bps = [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         int b = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, G::THREADS * GPC, smem);
         return b > 0 ? b : 1;

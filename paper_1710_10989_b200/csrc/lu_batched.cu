@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include "async_buffer.hpp"
+#include "device_once.hpp"
 #include "expm_common.cuh"
 #include "lu_batched.cuh"
 
@@ -539,12 +540,11 @@ __global__ void __launch_bounds__(256, 2) gemm_sub_kernel(SubArgs a) {
 int sub(double* C, const double* X, const double* Y, int rc, int cc, int kc, int rows, int cols,
         int np, const int32_t* list, int count, cudaStream_t st, std::atomic<uint64_t>* launches) {
     if (rows <= 0 || cols <= 0 || count == 0) return MEXP_OK;
-    static bool attr = [] {
+    static PerDevice attr_once;
+    attr_once([] {
         cudaFuncSetAttribute(gemm_sub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(GEMM_SUB_SMEM));
-        return true;
-    }();
-    (void)attr;
+    });
     SubArgs a{C, X, Y, rc, cc, kc, rows, cols, np, list};
     for (int z0 = 0; z0 < count; z0 += 65535) {
         a.list = list + z0;
@@ -682,11 +682,10 @@ int trsm(const double* M, double* X, int np, const int32_t* list, int count, int
         return !(e && std::atoi(e) == 0);
     }();
     if (dmma_path && W && ncols % 64 == 0) {
-        static bool attr = [] {
+        static PerDevice attr_once;
+        attr_once([] {
             cudaFuncSetAttribute(tri_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TRI_MM_SMEM));
-            return true;
-        }();
-        (void)attr;
+        });
         for (int z0 = 0; z0 < count; z0 += 65535) {
             const int zc = std::min(count - z0, 65535);
             tri_inv_kernel<kLower><<<dim3(1, zc), NB, 0, st>>>(M, np, list + z0, r0, W);
