@@ -197,3 +197,37 @@ def test_no_cpu_fallback_without_gpu(lib):
 
 def test_selection_record_layout():
     assert C.sizeof(mx.Selection) == 16 and mx.SELECTION_DTYPE.itemsize == 16
+
+
+def test_multi_device_entry_without_gpu(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    a = np.zeros((4, 8, 8))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        mx.expm_batched_host_multi(a, devices=[0, 0])
+    assert lib.mexp_device_count() == 0
+
+
+def test_host_buffer_validation():
+    """Caller buffers are checked before any pointer reaches the C ABI (a
+    wrong-sized or wrong-typed `out` would otherwise be written past its end)."""
+    import torch
+    a = np.zeros((3, 8, 8))
+    with pytest.raises(ValueError, match="out must be"):
+        mx.expm_batched_host(a, out=np.empty((2, 8, 8)))
+    with pytest.raises(ValueError, match="out must be"):
+        mx.expm_batched_host(a, out=np.empty((3, 8, 8), np.float32))
+    with pytest.raises(ValueError, match="out must be"):
+        mx.expm_batched_host(a, out=np.empty((3, 8, 16))[:, :, ::2])
+    with pytest.raises(ValueError, match="square"):
+        mx.expm_batched_host(np.zeros((3, 8, 7)))
+    with pytest.raises(ValueError, match="unsupported dtype"):
+        mx.expm_batched_host(np.zeros((3, 8, 8), np.int64))
+    t = torch.zeros(3, 8, 8, dtype=torch.float64)
+    with pytest.raises(ValueError, match="out must be"):
+        mx.expm_batched_host(t, out=torch.zeros(3, 8, 8, dtype=torch.float32))
+    with pytest.raises(ValueError, match="sel_out"):
+        mx.expm_batched_host(t, sel_out=torch.zeros(16, dtype=torch.uint8))
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        mx.expm_batched(t, torch.empty_like(t))
