@@ -621,7 +621,7 @@ def run_ours(args):
         # drop-in on a host DenseMatrix, 2000 calls) instead of through
         # Python's ctypes overhead.
         native = os.path.join(ROOT, "bin", "call_latency")
-        if Bl == 1 and cfg.dtype == "f64" and fam == 0 and args.rounding == "auto" \
+        if Bl == 1 and n <= 64 and cfg.dtype == "f64" and fam == 0 and args.rounding == "auto" \
                 and os.path.exists(native):
             import tempfile
             with tempfile.NamedTemporaryFile(suffix=".bin", delete=False) as tf:

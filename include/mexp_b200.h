@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define MEXP_B200_ABI_VERSION 2
+#define MEXP_B200_ABI_VERSION 3
 
 /* Status codes. The C++ drop-in maps 1-3 to std::invalid_argument with the
  * reference's messages (expm.cpp:13, expm.cpp:38, taylor_schemes.cpp:225)
@@ -59,20 +59,20 @@ typedef enum { MEXP_ACCURACY_SINGLE = 0, MEXP_ACCURACY_DOUBLE = 1 } mexp_accurac
  * engine on the widened values and rounds e^A once to float. */
 typedef enum { MEXP_F64 = 0, MEXP_F32 = 1 } mexp_dtype;
 
-/* Rounding policy of the fp64 small-N path (n <= 64):
+/* Rounding policy of the fp64 path:
  *   REFERENCE: products and linear combinations with separately rounded
  *              multiplies and adds in the reference's accumulation order
  *              (kernels.cpp:16-37, -ffp-contract=off) -> e^A bit-identical
- *              to the reference;
+ *              to the reference (n > 64: k-ordered DMUL+DADD GEMMs on the
+ *              CUDA cores; the Pade LU is DMMA-only and refuses it);
  *   FAST:      FP64 tensor-core DMMA products, FMA combinations;
  *   AUTO:      FAST, except matrices with s >= 3 + floor(log2 n) squarings
- *              (n >= 8; every matrix for n < 8), whose rounding differences
- *              the squarings amplify: those run REFERENCE, all but their
- *              last 2 squarings (the 8x8 kernel).
- * For n > 64, REFERENCE runs the products as k-ordered DMUL+DADD chains on
- * the CUDA cores and the lincombs literally (bit-identical for TaylorNew and
- * TaylorPS; the Pade LU is DMMA-only and refuses it), AUTO and FAST the
- * tensor-core DMMA GEMMs. F32 with n <= 64 ignores it. */
+ *              (every matrix for n < 8), whose rounding differences the
+ *              squarings amplify: those run REFERENCE end to end (so they are
+ *              bit-identical to the reference), for every n. Checked within
+ *              50 n u on all nine reference gallery kinds, n = 2..512, s <= 14
+ *              (tests/test_gpu_auto_stress.py).
+ * F32 with n <= 64 ignores it. */
 typedef enum { MEXP_ROUND_AUTO = 0, MEXP_ROUND_REFERENCE = 1, MEXP_ROUND_FAST = 2 } mexp_rounding;
 
 /* Per-matrix selection record written by the batched calls (16 bytes).
@@ -159,6 +159,35 @@ int mexp_device_count(void);
  * each of `batch` fp64 matrices, in place, s squarings each. */
 int mexp_squarings_batched(double* d_x, int n, int64_t batch, int s, int rounding,
                            void* stream);
+
+/* ---- the reference's dense-matrix layer (kernels.hpp:15-24) ------------
+ * Device buffers of `batch` row-major n x n fp64 matrices, asynchronous on
+ * `stream` unless noted. Every operation runs in the reference's arithmetic
+ * (separately rounded multiplies and adds in the reference's order), so the
+ * results are bit-identical to the reference's kernels. */
+
+/* kernels::matmul (kernels.cpp:16-27): C = A B, k ascending from 0.0.
+ * REFERENCE rounding: bit-identical; FAST / AUTO: FMA (n <= 64) or the DMMA
+ * GEMM (n > 64). For n > 64 the call is host-synchronous. */
+int mexp_matmul_batched(const double* d_a, const double* d_b, double* d_c, int n, int64_t batch,
+                        int rounding, void* stream);
+
+/* kernels::lincomb (kernels.cpp:29-37): d_out[e] = sum_i coeffs[i] * d_mats[i][e]
+ * for e < len, summed left to right. `coeffs` and the array `d_mats` of k
+ * device pointers are host arrays; kernels::scale is k = 1. */
+int mexp_lincomb_batched(const double* coeffs, const double* const* d_mats, int k, double* d_out,
+                         int64_t len, void* stream);
+
+/* kernels::one_norm (kernels.cpp:44-53): d_norms[i] = max column sum of |A_i|,
+ * exactly the reference's value. */
+int mexp_one_norm_batched(const double* d_a, int n, int64_t batch, double* d_norms, void* stream);
+
+/* lu_solve (dense_matrix.cpp:112-118, kernels.cpp:55-112): X = M^-1 R with
+ * partial pivoting, one pivoted LU per matrix in the reference's arithmetic.
+ * d_status[i] = MEXP_OK, or MEXP_ERR_SINGULAR on an exactly zero pivot
+ * (X_i is then NaN). */
+int mexp_lu_solve_batched(const double* d_m, const double* d_rhs, double* d_x, int n, int64_t batch,
+                          int32_t* d_status, void* stream);
 
 /* ---- runtime ---------------------------------------------------------- */
 

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <random>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -273,6 +274,82 @@ void ref_coefficients(double* t8, double* t12, double* t18a, double* t18b) {
     std::memcpy(t12, mexp::kT12, sizeof(double) * 16);
     std::memcpy(t18a, mexp::kT18A, sizeof(double) * 4);
     std::memcpy(t18b, mexp::kT18B, sizeof(double) * 20);
+}
+
+
+// The reference's dense layer and scheme evaluators behind one entry with the
+// operation codes of the product's mexp_b200_dense_call (dense_ops.cu), so a
+// test can run both on the same inputs: 0 matmul, 1 lincomb (arg 1: n is the
+// flat length), 2 one_norm, 3 lu_solve, 4 squarings, 5 eval_t8, 6 eval_t12,
+// 7 eval_t18, 8 eval_ps(arg), 9 psi9, 10 taylor_oracle(arg), 11
+// psi_oracle(arg), 12 eval_pade(arg), 13 eval_taylor_new(arg), 14
+// eval_taylor_ps(arg), 15 kernels::lu_factor, 16 kernels::lu_apply. Returns
+// 0, 3 (invalid argument) or 7 (singular denominator).
+int ref_dense_call(int op, int arg, const double* const* in, int nin, const double* coeffs, int n,
+                   double* out, const int32_t* iin, int32_t* iout, int64_t* products,
+                   int64_t* solves) {
+    try {
+        mexp::CostContext ctx;
+        const std::size_t nn = std::size_t(n) * n;
+        auto put = [&](const mexp::DenseMatrix& r) { std::memcpy(out, r.data(), sizeof(double) * nn); };
+        switch (op) {
+            case 0: put(mexp::matmul(to_dense(in[0], n), to_dense(in[1], n))); break;
+            case 1:
+                if (arg == 1) {
+                    mexp::kernels::lincomb(coeffs, in, nin, out, n);
+                } else {
+                    std::vector<mexp::DenseMatrix> ms;
+                    std::vector<const mexp::DenseMatrix*> ps;
+                    for (int i = 0; i < nin; ++i) ms.push_back(to_dense(in[i], n));
+                    for (auto& m : ms) ps.push_back(&m);
+                    put(mexp::lincomb(std::span<const double>(coeffs, nin),
+                                      std::span<const mexp::DenseMatrix* const>(ps.data(), ps.size())));
+                }
+                break;
+            case 2: *out = mexp::one_norm(to_dense(in[0], n)); break;
+            case 3: put(mexp::lu_solve(ctx, to_dense(in[0], n), to_dense(in[1], n))); break;
+            case 4: put(mexp::squarings(ctx, to_dense(in[0], n), arg)); break;
+            case 5: put(mexp::eval_t8(ctx, to_dense(in[0], n))); break;
+            case 6: put(mexp::eval_t12(ctx, to_dense(in[0], n))); break;
+            case 7: put(mexp::eval_t18(ctx, to_dense(in[0], n))); break;
+            case 8: put(mexp::eval_ps(ctx, to_dense(in[0], n), arg)); break;
+            case 9: put(mexp::psi9(ctx, to_dense(in[0], n))); break;
+            case 10: put(mexp::taylor_oracle(to_dense(in[0], n), arg)); break;
+            case 11: put(mexp::psi_oracle(to_dense(in[0], n), arg)); break;
+            case 12: put(mexp::eval_pade(ctx, to_dense(in[0], n), arg)); break;
+            case 13: put(mexp::eval_taylor_new(ctx, to_dense(in[0], n), arg)); break;
+            case 14: put(mexp::eval_taylor_ps(ctx, to_dense(in[0], n), arg)); break;
+            case 15: {
+                const auto f = mexp::kernels::lu_factor(in[0], n);
+                std::memcpy(out, f.lu.data(), sizeof(double) * nn);
+                for (int i = 0; i < n; ++i) iout[i] = f.perm[i];
+                break;
+            }
+            case 16: {
+                mexp::kernels::LuFactors f;
+                f.n = n;
+                f.lu.assign(in[0], in[0] + nn);
+                f.perm.assign(iin, iin + n);
+                mexp::kernels::lu_apply(f, in[1], out, n);
+                break;
+            }
+            default: return kInvalid;
+        }
+        if (products) *products = ctx.products;
+        if (solves) *solves = ctx.solves;
+        return kOk;
+    } catch (const std::invalid_argument&) {
+        return kInvalid;
+    } catch (const std::runtime_error&) {
+        return kSingular;
+    }
+}
+
+// psi9_coefficients (taylor_schemes.cpp:29-42, 57-60): x1..x9
+void ref_psi9_coefficients(double* x) {
+    const auto& c = mexp::psi9_coefficients();
+    const double v[9] = {c.x1, c.x2, c.x3, c.x4, c.x5, c.x6, c.x7, c.x8, c.x9};
+    for (int i = 0; i < 9; ++i) x[i] = v[i];
 }
 
 }  // extern "C"

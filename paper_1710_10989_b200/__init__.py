@@ -127,6 +127,10 @@ def library() -> C.CDLL:
         "mexp_squarings_batched": (I, [P, I, I64, I, I, P]),
         "mexp_expm_batched_host_multi": (I, [P, P, I, I, I64, I, I, I, P, P, P, I]),
         "mexp_device_count": (I, []),
+        "mexp_matmul_batched": (I, [P, P, P, I, I64, I, P]),
+        "mexp_lincomb_batched": (I, [P, P, I, P, I64, P]),
+        "mexp_one_norm_batched": (I, [P, I, I64, P, P]),
+        "mexp_lu_solve_batched": (I, [P, P, P, I, I64, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -141,6 +145,7 @@ EXPORTED_SYMBOLS = (
     "mexp_launch_count", "mexp_unit_roundoff", "mexp_selection_table", "mexp_select",
     "mexp_expm", "mexp_expm_batched", "mexp_expm_batched_host", "mexp_squarings_batched",
     "mexp_expm_batched_host_multi", "mexp_device_count",
+    "mexp_matmul_batched", "mexp_lincomb_batched", "mexp_one_norm_batched", "mexp_lu_solve_batched",
 )
 
 
@@ -342,6 +347,83 @@ def expm_batched_host_multi(a, out=None, devices=None, accuracy: Accuracy = Accu
 
 def device_count() -> int:
     return int(library().mexp_device_count())
+
+
+# ---- the reference's dense-matrix layer on device tensors (kernels.hpp) ----
+def _stream(t, stream):
+    import torch
+    return C.c_void_p((stream or torch.cuda.current_stream(t.device)).cuda_stream)
+
+
+def _dev_f64(*ts):
+    for t in ts:
+        if not (t.is_cuda and t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous()):
+            raise ValueError("expected contiguous float64 CUDA tensors")
+
+
+def matmul_batched(a, b, out=None, rounding: int = ROUND_REFERENCE, stream=None):
+    """kernels::matmul (kernels.cpp:16-27) on (batch, n, n) or (n, n) device
+    tensors; REFERENCE rounding is bit-identical to the reference."""
+    import torch
+    out = torch.empty_like(a) if out is None else out
+    _dev_f64(a, b, out)
+    if a.shape != b.shape or out.shape != a.shape or a.shape[-1] != a.shape[-2]:
+        raise ValueError("dimension mismatch")
+    n = a.shape[-1]
+    st = library().mexp_matmul_batched(a.data_ptr(), b.data_ptr(), out.data_ptr(), n,
+                                       a.numel() // (n * n), int(rounding), _stream(a, stream))
+    if st != OK:
+        _raise(st)
+    return out
+
+
+def lincomb_batched(coeffs, mats, out=None, stream=None):
+    """kernels::lincomb (kernels.cpp:29-37): sum_i coeffs[i] * mats[i], left to right."""
+    import torch
+    if len(coeffs) != len(mats) or not mats:
+        raise ValueError("lincomb needs equally long nonempty lists")
+    out = torch.empty_like(mats[0]) if out is None else out
+    _dev_f64(out, *mats)
+    if any(m.shape != out.shape for m in mats):
+        raise ValueError("dimension mismatch")
+    c = (C.c_double * len(coeffs))(*[float(x) for x in coeffs])
+    p = (C.c_void_p * len(mats))(*[m.data_ptr() for m in mats])
+    st = library().mexp_lincomb_batched(c, p, len(mats), out.data_ptr(), out.numel(),
+                                        _stream(out, stream))
+    if st != OK:
+        _raise(st)
+    return out
+
+
+def one_norm_batched(a, stream=None):
+    """kernels::one_norm (kernels.cpp:44-53) per matrix of a (batch, n, n) tensor."""
+    import torch
+    _dev_f64(a)
+    n = a.shape[-1]
+    batch = a.numel() // (n * n)
+    out = torch.empty(batch, dtype=a.dtype, device=a.device)
+    st = library().mexp_one_norm_batched(a.data_ptr(), n, batch, out.data_ptr(), _stream(a, stream))
+    if st != OK:
+        _raise(st)
+    return out
+
+
+def lu_solve_batched(m, rhs, stream=None):
+    """lu_solve (kernels.cpp:55-112) per matrix: returns (X, status) with
+    status[i] = ERR_SINGULAR where the reference throws "singular denominator"."""
+    import torch
+    _dev_f64(m, rhs)
+    if m.shape != rhs.shape:
+        raise ValueError("dimension mismatch")
+    n = m.shape[-1]
+    batch = m.numel() // (n * n)
+    x = torch.empty_like(m)
+    status = torch.empty(batch, dtype=torch.int32, device=m.device)
+    st = library().mexp_lu_solve_batched(m.data_ptr(), rhs.data_ptr(), x.data_ptr(), n, batch,
+                                         status.data_ptr(), _stream(m, stream))
+    if st != OK:
+        _raise(st)
+    return x, status
 
 
 def launch_count() -> int:

@@ -140,29 +140,47 @@ int launch_small_f64(const double* a, double* out, mexp_selection* sel, int64_t 
     return MEXP_OK;
 }
 
-// Ring of {work counter, finished-CTA counter} slots for kernels that hand out
-// work dynamically: concurrent launches (other streams) get distinct slots;
-// each kernel leaves its slot zeroed (release_ticket), so no memset per launch
-// and CUDA-graph replays of a captured launch find their slot ready.
-int next_ticket(unsigned long long** out) {
+// Slots of {work counter, finished-CTA counter} for kernels that hand out
+// work dynamically; each kernel leaves its slot zeroed (release_ticket), so
+// no memset per launch. Eager launches take the next slot of a 4096-slot ring
+// per device (concurrent launches on other streams get distinct slots). A
+// launch captured into a CUDA graph keeps its slot for the graph's lifetime
+// and its replays may overlap later eager launches, so captured launches take
+// slots of a separate 65536-slot region that is never handed out again
+// (allocated with the ring, outside any capture).
+int next_ticket(cudaStream_t st, unsigned long long** out) {
     constexpr int kSlots = 4096;
-    static unsigned long long* ring[16] = {};
+    constexpr int kCaptureSlots = 65536;
+    static std::atomic<unsigned long long*> ring[16] = {};
     static std::atomic<uint32_t> next[16];
+    static std::atomic<uint32_t> next_captured[16];
     int dev = 0;
     MEXP_CUDA(cudaGetDevice(&dev));
     dev &= 15;
-    if (!ring[dev]) {
+    unsigned long long* base = ring[dev].load(std::memory_order_acquire);
+    if (!base) {
         static std::mutex mu;
         std::lock_guard<std::mutex> lock(mu);
-        if (!ring[dev]) {
-            unsigned long long* r = nullptr;
-            MEXP_CUDA(cudaMalloc(&r, 2 * sizeof(unsigned long long) * kSlots));
-            MEXP_CUDA(cudaMemset(r, 0, 2 * sizeof(unsigned long long) * kSlots));
-            ring[dev] = r;
+        base = ring[dev].load(std::memory_order_acquire);
+        if (!base) {
+            const size_t bytes = 2 * sizeof(unsigned long long) * (kSlots + kCaptureSlots);
+            MEXP_CUDA(cudaMalloc(&base, bytes));
+            MEXP_CUDA(cudaMemset(base, 0, bytes));
+            ring[dev].store(base, std::memory_order_release);
         }
     }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    MEXP_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (cap == cudaStreamCaptureStatusActive) {
+        const uint32_t i = next_captured[dev].fetch_add(1);
+        if (i < uint32_t(kCaptureSlots)) {
+            *out = base + 2 * (kSlots + i);
+            return MEXP_OK;
+        }
+        // more than 65536 captured launches in this process: fall back to the ring
+    }
     const uint32_t i = next[dev].fetch_add(1) % kSlots;
-    *out = ring[dev] + 2 * i;
+    *out = base + 2 * i;
     return MEXP_OK;
 }
 
@@ -235,7 +253,7 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
     // persistent per-device ring, reset in stream order
     unsigned long long* ticket = nullptr;
     {
-        int r = next_ticket(&ticket);
+        int r = next_ticket(st, &ticket);
         if (r != MEXP_OK) return r;
     }
     // AUTO: the last fast_tail() squarings of the reference-rounded matrices
@@ -318,7 +336,7 @@ int launch_pade8(const double* a, double* out, mexp_selection* sel, int64_t batc
     const int64_t want = (batch + 4 * kN8WarpsPerBlock - 1) / (4 * kN8WarpsPerBlock);
     const int grid = int(want < cap ? want : cap);
     unsigned long long* ticket = nullptr;
-    const int r = next_ticket(&ticket);
+    const int r = next_ticket(st, &ticket);
     if (r != MEXP_OK) return r;
     expm8_pade_kernel<8><<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding,
                                                                  smin, ticket);
@@ -533,6 +551,12 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
                    int rounding, mexp_selection* h_sel, int64_t* first_error);
 
 }  // namespace
+
+namespace mexp_b200 {
+// shared with dense_ops.cu: one launch counter and one last-error string
+std::atomic<uint64_t>& library_launch_counter() { return g_launches; }
+void set_last_cuda_error(const std::string& e) { g_last_cuda_error = e; }
+}  // namespace mexp_b200
 
 extern "C" {
 

@@ -771,9 +771,10 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
         ~SyncOnExit() { cudaStreamSynchronize(s); }
     } fence{st};
     if (ws.bytes < need) {
-        AsyncBuffer::retain_pool();
         if (ws.buf) LCUDA(cudaFreeAsync(ws.buf, st));
-        LCUDA(cudaMallocAsync(&ws.buf, need, st));
+        ws.buf = nullptr;
+        ws.bytes = 0;
+        LCUDA(pool_alloc(reinterpret_cast<void**>(&ws.buf), need, st));
         ws.bytes = need;
     }
     double* W[kMaxBuffers] = {};
@@ -1213,6 +1214,55 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     LCUDA(cudaGetLastError());
     }  // passes
     LCUDA(cudaStreamSynchronize(st));  // host lists must outlive their async upload
+    return MEXP_OK;
+}
+
+// C = A B for `batch` n x n fp64 matrices (any n): both operands zero-padded
+// to np, one batched GEMM (REFERENCE rounding: the k-ordered exact product
+// over k < n, bit-identical to kernels::matmul; otherwise DMMA), unpadded.
+// Host-synchronous (the matrix list is uploaded from the host).
+int matmul_f64(const double* d_a, const double* d_b, double* d_c, int n, int64_t batch, int rounding,
+               cudaStream_t st, std::atomic<uint64_t>* launches) {
+    struct ExactScope {
+        explicit ExactScope(int v) { g_exact_n = v; }
+        ~ExactScope() { g_exact_n = 0; }
+    } exact_scope(rounding == MEXP_ROUND_REFERENCE ? n : 0);
+    if (batch == 0) return MEXP_OK;
+    if (batch > INT32_MAX) return MEXP_ERR_INVALID_ARGUMENT;
+    const int np = (n + BM - 1) / BM * BM;
+    const int64_t mat = int64_t(np) * np;
+    AsyncBuffer w_buf(st), list_buf(st), sel0_buf(st);
+    LCUDA(w_buf.alloc(sizeof(double) * 3 * batch * mat));
+    LCUDA(list_buf.alloc(sizeof(int32_t) * batch));
+    LCUDA(sel0_buf.alloc(sizeof(mexp_selection) * batch));  // s = 0: prep copies unscaled
+    double* w = w_buf.get<double>();
+    int32_t* list = list_buf.get<int32_t>();
+    mexp_selection* sel0 = sel0_buf.get<mexp_selection>();
+    g_map_batch = batch;
+    LCUDA(cudaMemsetAsync(sel0, 0, sizeof(mexp_selection) * batch, st));
+    std::vector<int32_t> idx(batch);
+    for (int64_t m = 0; m < batch; ++m) idx[m] = int32_t(m);
+    LCUDA(cudaMemcpyAsync(list, idx.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice, st));
+    const unsigned rows = unsigned(std::min(np, 64));
+    double* wa = w;
+    double* wb = w + batch * mat;
+    double* wc = w + 2 * batch * mat;
+    sliced(batch, [&](int64_t y0, unsigned ny) {
+        prep_kernel<<<dim3(rows, ny), 256, 0, st>>>(d_a, wa, n, np, list + y0, sel0);
+        prep_kernel<<<dim3(rows, ny), 256, 0, st>>>(d_b, wb, n, np, list + y0, sel0);
+    });
+    launches->fetch_add(2, std::memory_order_relaxed);
+    int r = gemm<EPI_STORE>(wa, wb, {}, {wc}, list, int(batch), np, st, launches);
+    if (r) {
+        cudaStreamSynchronize(st);
+        return r;
+    }
+    sliced(batch, [&](int64_t y0, unsigned ny) {
+        unpad_kernel<<<dim3(rows, ny), 256, 0, st>>>(wc, d_c, n, np, list + y0);
+    });
+    launches->fetch_add(1, std::memory_order_relaxed);
+    LCUDA(cudaGetLastError());
+    LCUDA(cudaStreamSynchronize(st));  // idx must outlive the async copy
     return MEXP_OK;
 }
 

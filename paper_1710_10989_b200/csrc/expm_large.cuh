@@ -22,6 +22,11 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel, int 
                    int64_t batch, int acc_arg, int rounding, int smin, cudaStream_t st,
                    std::atomic<uint64_t>* launches);
 
+// C = A B for `batch` n x n fp64 matrices of any n (REFERENCE rounding:
+// bit-identical to the reference's kernels::matmul). Host-synchronous.
+int matmul_f64(const double* d_a, const double* d_b, double* d_c, int n, int64_t batch, int rounding,
+               cudaStream_t st, std::atomic<uint64_t>* launches);
+
 // X <- X^(2^s), in place, for `batch` n x n fp64 matrices.
 int squarings_f64(double* d_x, int n, int64_t batch, int s, int rounding, cudaStream_t st,
                   std::atomic<uint64_t>* launches);

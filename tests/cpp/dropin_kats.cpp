@@ -2,7 +2,8 @@
 // without doctest (absent here) against the C++ drop-in headers
 // (include/mexp/*.hpp) and linked to libmexp_b200.so instead of libmexp.a.
 // Sources of the cases: proj/tests/test_expm.cpp:21-197,
-// test_dense_matrix.cpp:51-55, cli_smoke.sh:10-19.
+// test_dense_matrix.cpp:17-74, test_kernels.cpp:85-100, test_pade.cpp:61-190,
+// cli_smoke.sh:10-19.
 //   dropin_kats                 run everything (needs a B200)
 //   dropin_kats --no-device     check the host-only API and that expm refuses
 //                               with std::runtime_error (no CPU fallback)
@@ -14,6 +15,9 @@
 #include <stdexcept>
 
 #include "mexp/expm.hpp"
+#include "mexp/kernels.hpp"
+#include "mexp/pade.hpp"
+#include "mexp/taylor_schemes.hpp"
 
 using namespace mexp;
 
@@ -180,6 +184,90 @@ static void device_cases() {
     CHECK(eb.degree == 18 && eb.s == 2 && eb.result.all_finite());
 }
 
+// The reference's dense-matrix layer (dense_matrix.hpp:40-58, kernels.hpp,
+// taylor_schemes.hpp, pade.hpp) on the device.
+static void dense_layer_cases() {
+    std::mt19937_64 rng(1);
+    const DenseMatrix x = random_with_norm(5, 2.0, rng);
+    // test_dense_matrix.cpp:17-29
+    CHECK(matmul(DenseMatrix::identity(5), x) == x);
+    const DenseMatrix nil = DenseMatrix::from_rows({{0, 1}, {0, 0}});
+    CHECK(matmul(nil, nil) == DenseMatrix(2));
+    const DenseMatrix a = DenseMatrix::from_rows({{1, 2}, {3, 4}});
+    const DenseMatrix b = DenseMatrix::from_rows({{5, 6}, {7, 8}});
+    CHECK(matmul(a, b) == DenseMatrix::from_rows({{19, 22}, {43, 50}}));
+    CHECK(throws<std::invalid_argument>([&] { matmul(a, DenseMatrix(3)); }));
+    // test_dense_matrix.cpp:31-47
+    const DenseMatrix id2 = DenseMatrix::identity(2);
+    CHECK(lincomb({1.0}, {&id2}) == id2);
+    CHECK(lincomb({2.0, -1.0}, {&x, &x}) == x);
+    CHECK(lincomb({1.0, 1.0}, {&id2, &nil}) == DenseMatrix::from_rows({{1, 1}, {0, 1}}));
+    CHECK(throws<std::invalid_argument>(
+        [] { lincomb(std::span<const double>{}, std::span<const DenseMatrix* const>{}); }));
+    const DenseMatrix b3(3);
+    CHECK(throws<std::invalid_argument>([&] { lincomb({1.0, 1.0}, {&x, &b3}); }));
+    // test_dense_matrix.cpp:49-53
+    CHECK(one_norm(DenseMatrix(3)) == 0.0);
+    CHECK(one_norm(DenseMatrix::identity(5)) == 1.0);
+    CHECK(one_norm(DenseMatrix::from_rows({{1, -2}, {3, 4}})) == 6.0);
+    // test_dense_matrix.cpp:55-71
+    const DenseMatrix x6 = random_with_norm(6, 3.0, rng);
+    CHECK(lu_solve(DenseMatrix::identity(6), x6) == x6);
+    CHECK(lu_solve(DenseMatrix::from_rows({{2, 0}, {0, 4}}), id2) ==
+          DenseMatrix::from_rows({{0.5, 0}, {0, 0.25}}));
+    const DenseMatrix rhs = DenseMatrix::from_rows({{1, 2}, {3, 4}});
+    CHECK(lu_solve(DenseMatrix::from_rows({{0, 1}, {1, 0}}), rhs) ==
+          DenseMatrix::from_rows({{3, 4}, {1, 2}}));
+    bool singular = false;
+    try {
+        lu_solve(DenseMatrix(2), rhs);
+    } catch (const std::runtime_error& e) {
+        singular = std::strcmp(e.what(), "singular denominator") == 0;
+    }
+    CHECK(singular);
+    CHECK(add(a, b) == DenseMatrix::from_rows({{6, 8}, {10, 12}}));
+    CHECK(sub(b, a) == DenseMatrix::from_rows({{4, 4}, {4, 4}}));
+    CHECK(scaled(a, 0.5) == DenseMatrix::from_rows({{0.5, 1}, {1.5, 2}}));
+    // the reference's error_sweep expression (bench.cpp:83) compiles and runs
+    const auto rep = expm(x, Accuracy::Double, Family::TaylorNew);
+    CHECK(one_norm(sub(rep.result, rep.result)) == 0.0);
+    // test_kernels.cpp:85-100: the first maximal row wins the pivot
+    const double tie[9] = {1, 0, 0, -3, 1, 0, 3, 0, 1};
+    const auto f = kernels::lu_factor(tie, 3);
+    CHECK(f.perm[0] == 1);
+    double y[9];
+    kernels::lu_apply(f, tie, y, 3);
+    CHECK(std::abs(y[0] - 1) + std::abs(y[4] - 1) + std::abs(y[8] - 1) <= 1e-15);
+    double c[4];
+    kernels::matmul(a.data(), b.data(), c, 2);
+    CHECK(c[0] == 19 && c[3] == 50 && kernels::one_norm(a.data(), 2) == 6.0);
+    // ledgers: eval_t18 5 products, eval_r10 3 products + 1 solve (test_pade.cpp:142-156)
+    CostContext ctx;
+    const DenseMatrix small = random_with_norm(6, 0.5, rng);
+    eval_t18(ctx, small);
+    CHECK(ctx.products == 5 && ctx.solves == 0);
+    ctx.reset();
+    eval_r10(ctx, small);
+    CHECK(ctx.products == 3 && ctx.solves == 1 && ctx.thirds() == 13);
+    ctx.reset();
+    eval_ps(ctx, small, 16);
+    CHECK(ctx.products == 6);
+    ctx.reset();
+    psi9(ctx, small);
+    CHECK(ctx.products == 3);
+    // schemes agree with the Horner oracle (test_taylor_schemes.cpp:50-100)
+    const DenseMatrix t = taylor_oracle(small, 18);
+    CHECK(norm1(sub(eval_taylor_new(ctx, small, 18), t)) <= 1e-14);
+    CHECK(norm1(sub(psi9(ctx, small), psi_oracle(small, 9))) <= 1e-14);
+    // pade_coeffs (test_pade.cpp:61-79): b_0 = 1, b_1 = 1/2, r_1 of 2x2 zero = I
+    const auto pc = pade_coeffs(13);
+    CHECK(pc.m == 13 && pc.b.size() == 14 && pc.b[0] == 1.0 && pc.b[1] == 0.5);
+    CHECK(throws<std::invalid_argument>([] { pade_coeffs(14); }));
+    CHECK(eval_pade(ctx, DenseMatrix(3), 26) == DenseMatrix::identity(3));
+    CHECK(t8_coefficients().x3 == 2.0 / 3.0 && kT12[0][0] == 9.0198e-16 && kT18B[1][0] < -10.0);
+    CHECK(psi9_coefficients().x2 == -0.25 && psi9_coefficients().x3 == -1.0);
+}
+
 int main(int argc, char** argv) {
     const bool no_device = argc > 1 && std::strcmp(argv[1], "--no-device") == 0;
     host_only();
@@ -187,6 +275,7 @@ int main(int argc, char** argv) {
         CHECK(throws<std::runtime_error>([] { expm(DenseMatrix(2), Accuracy::Double, Family::TaylorNew); }));
     } else {
         device_cases();
+        dense_layer_cases();
     }
     std::printf("%s: %d failure(s)\n", no_device ? "dropin_kats --no-device" : "dropin_kats", failures);
     return failures == 0 ? 0 : 1;

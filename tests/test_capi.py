@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.mexp_abi_version() == 2
+    assert lib.mexp_abi_version() == 3
 
 
 def test_no_torch_types_in_signatures():
@@ -231,3 +231,24 @@ def test_host_buffer_validation():
         mx.expm_batched_host(t, sel_out=torch.zeros(16, dtype=torch.uint8))
     with pytest.raises(ValueError, match="CUDA tensors"):
         mx.expm_batched(t, torch.empty_like(t))
+
+
+def test_dense_layer_coefficient_tables_equal_reference(lib):
+    """The drop-in's psi9_coefficients / pade_coeffs accessors (host tables of
+    the library) are the reference's doubles bit for bit."""
+    from oracle.oracle import REF_SO, Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    ref = C.CDLL(REF_SO)
+    got, want = np.zeros(9), np.zeros(9)
+    lib.mexp_b200_psi9_coefficients.argtypes = [C.c_void_p]
+    lib.mexp_b200_psi9_coefficients(got.ctypes.data)
+    ref.ref_psi9_coefficients.argtypes = [C.c_void_p]
+    ref.ref_psi9_coefficients(want.ctypes.data)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    r = Reference()
+    for m in range(1, 14):
+        b = np.zeros(14)
+        lib.mexp_b200_pade_coefficients.argtypes = [C.c_int, C.c_void_p]
+        assert lib.mexp_b200_pade_coefficients(m, b.ctypes.data) == m + 1
+        assert np.array_equal(b[:m + 1].view(np.uint64), r.pade_coeffs(m).view(np.uint64))

@@ -171,9 +171,23 @@ def test_oracle_coefficients_equal_reference(oracle, golden):
         assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
 
 
+def macro_body(src, name):
+    """The text of a (backslash-continued) #define, without its name."""
+    lines = src[src.index("#define " + name + " "):].splitlines()
+    out = []
+    for ln in lines:
+        out.append(ln.rstrip("\\"))
+        if not ln.endswith("\\"):
+            break
+    return " ".join(out)[len("#define " + name):]
+
+
 def test_device_coefficients_equal_reference(golden):
-    """The CUDA constants (expm_common.cuh) are the reference's doubles bit for bit."""
-    src = open(os.path.join(ROOT, "paper_1710_10989_b200", "csrc", "expm_common.cuh")).read()
+    """The coefficient tables the kernels and the drop-in share (scheme_tables.h,
+    expm_common.cuh) are the reference's doubles bit for bit."""
+    csrc = os.path.join(ROOT, "paper_1710_10989_b200", "csrc")
+    src = open(os.path.join(csrc, "expm_common.cuh")).read() + \
+        open(os.path.join(csrc, "scheme_tables.h")).read()
     g = golden("coefficients.npz")
     t8 = dict(re.findall(r"double (x\d|y\d) = ([^;]+);", src))
     names = ["x1", "x2", "x3", "x4", "x5", "x6", "x7", "y0", "y1", "y2"]
@@ -185,9 +199,13 @@ def test_device_coefficients_equal_reference(golden):
         m = re.search(r"constexpr double " + name + r"\[[^=]*=\s*\{(.*?)\};", src, re.S)
         return np.array([float(v) for v in re.findall(r"[-+]?\d[\d.e+-]*", m.group(1))])
 
-    assert np.array_equal(block("c_t12"), g["t12"].ravel())
-    assert np.array_equal(block("c_t18a"), g["t18a"])
-    assert np.array_equal(block("c_t18b"), g["t18b"].ravel())
+    def macro(name):
+        return np.array([float(v) for v in re.findall(r"[-+]?\d[\d.e+-]*", macro_body(src, name))])
+
+    assert "c_t12[4][4] = MEXP_T12_TABLE" in src and "c_t18b[4][5] = MEXP_T18B_TABLE" in src
+    assert np.array_equal(macro("MEXP_T12_TABLE"), g["t12"].ravel())
+    assert np.array_equal(macro("MEXP_T18A_TABLE"), g["t18a"])
+    assert np.array_equal(macro("MEXP_T18B_TABLE"), g["t18b"].ravel())
     th = block("c_theta")
     assert np.array_equal(th, [1.19e-7, 5.98e-4, 5.12e-2, 5.80e-1, 1.46, 3.01,
                                2.22e-16, 2.58e-8, 3.40e-4, 4.99e-2, 2.99e-1, 1.09])
@@ -361,9 +379,8 @@ def test_pade_coefficients(oracle, golden):
     g = golden("pade.npz")["coeffs"]
     for m in range(1, 14):
         assert np.array_equal(oracle.pade_coeffs(m).view(np.uint64), g[m - 1, :m + 1].view(np.uint64))
-    src = open(os.path.join(ROOT, "paper_1710_10989_b200", "csrc", "expm_common.cuh")).read()
-    body = src[src.index("#define MEXP_PADE_TABLE"):]
-    body = body[body.index("{") + 1:body.index("c_pade[13][14]")]
+    src = open(os.path.join(ROOT, "paper_1710_10989_b200", "csrc", "scheme_tables.h")).read()
+    body = macro_body(src, "MEXP_PADE_TABLE")
     vals = [float.fromhex(t) if "0x" in t else float(t)
             for t in re.findall(r"0x[0-9a-fA-Fp.+-]+|\d+\.\d+", body)]
     dev = np.array(vals).reshape(13, 14)
