@@ -1,11 +1,12 @@
 // Drop-in for the reference's proj/include/mexp/expm.hpp (arXiv 1710.10989
 // scaling and squaring with the reduced-product Taylor schemes), running on a
-// B200: the 1-norm, the (m, s) selection, T_m and the s squarings all happen
-// on the device (C ABI: include/mexp_b200.h, mexp_expm). Same signatures,
-// same ExpmReport, same exceptions: std::invalid_argument("non-finite matrix
-// entry"), ("norm must be finite and nonnegative"); families other than
-// TaylorNew throw std::invalid_argument; a CUDA failure or a missing device
-// throws std::runtime_error.
+// B200: the 1-norm, the (m, s) selection, the scheme and the s squarings all
+// happen on the device (C ABI: include/mexp_b200.h, mexp_expm), for all three
+// families (TaylorNew, TaylorPS, PadeDiagonal). Same signatures, same
+// ExpmReport, same exceptions: std::invalid_argument("non-finite matrix
+// entry"), ("norm must be finite and nonnegative"); std::runtime_error
+// ("singular denominator") from a Pade solve; a CUDA failure or a missing
+// device throws std::runtime_error (there is no CPU fallback).
 #pragma once
 
 #include <cstdint>

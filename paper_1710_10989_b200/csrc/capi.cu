@@ -831,10 +831,40 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
         const char* e = std::getenv("MEXP_HOST_PIPE");
         return !(e && std::strcmp(e, "streams") == 0);
     }();
+    // MEXP_HOST_OUT_ZC=1: the kernels write e^A straight into the caller's
+    // pinned buffer (and the pinned records) over PCIe instead of device
+    // buffers plus a D2H copy per chunk, so the copy engines carry only the
+    // H2D stream. Measured (profiles/e2e_pipeline_r2.txt): cfg2 3.63 vs 3.45
+    // ms/batch (slower), cfg3 +3%; off by default.
+    static const bool out_zc_env = [] {
+        const char* e = std::getenv("MEXP_HOST_OUT_ZC");
+        return e && std::atoi(e) != 0;
+    }();
+    char* dst_dev = nullptr;
+    mexp_selection* hs_dev = nullptr;
+    if (!prefetch && staged && out_zc_env) {
+        dst_dev = static_cast<char*>(mapped_device_ptr(h_out));
+        hs_dev = static_cast<mexp_selection*>(mapped_device_ptr(hs));
+        if (!dst_dev || !hs_dev) dst_dev = nullptr, hs_dev = nullptr;
+    }
     if (!prefetch && staged) {
         cudaStream_t s_in = p.st[0], s_k = p.st[1], s_out = p.st[2];
         const int nslots = host_streams();
-        for (int64_t c = 0; c < nchunks; ++c) {
+        for (int64_t c = 0; c < nchunks && dst_dev; ++c) {
+            const int k = int(c % nslots);
+            const int64_t b0 = plan[c].first, nb = plan[c].second;
+            if (c >= nslots) MEXP_CUDA(cudaStreamWaitEvent(s_in, p.ev_k[c - nslots], 0));
+            MEXP_CUDA(cudaMemcpyAsync(p.d_in[k], src + b0 * mat_bytes, nb * mat_bytes,
+                                      cudaMemcpyHostToDevice, s_in));
+            MEXP_CUDA(cudaEventRecord(p.ev_in[c], s_in));
+            MEXP_CUDA(cudaStreamWaitEvent(s_k, p.ev_in[c], 0));
+            r = expm_device(p.d_in[k], dst_dev + b0 * mat_bytes, dtype, n, nb, aarg, rounding, hs_dev + b0,
+                            s_k);
+            if (r != MEXP_OK) return r;
+            MEXP_CUDA(cudaEventRecord(p.ev_k[c], s_k));
+            MEXP_CUDA(cudaEventRecord(p.ev[c], s_k));
+        }
+        for (int64_t c = 0; c < nchunks && !dst_dev; ++c) {
             const int k = int(c % nslots);
             const int64_t b0 = plan[c].first, nb = plan[c].second;
             if (c >= nslots) MEXP_CUDA(cudaStreamWaitEvent(s_in, p.ev_k[c - nslots], 0));

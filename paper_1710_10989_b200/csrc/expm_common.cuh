@@ -51,6 +51,24 @@ __device__ constexpr double c_t18b[4][5] = MEXP_T18B_TABLE;
 constexpr double kInvFact2 = 0.5;
 constexpr double kInvFact3 = 0x1.5555555555555p-3;  // 1.0 / 6.0
 constexpr double kInvFact4 = 0x1.5555555555555p-5;  // 1.0 / 24.0
+// 2^-s for s >= 0 as the reference's ldexp(1.0, -s) gives it (normal,
+// subnormal, or 0 past 2^-1074), built from the exponent bits instead of the
+// library ldexp's range checks
+__host__ __device__ __forceinline__ double pow2_neg(int s) {
+    long long b = 0;
+    if (s <= 1022)
+        b = static_cast<long long>(1023 - s) << 52;
+    else if (s <= 1074)
+        b = 1ll << (1074 - s);
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(b);
+#else
+    double x;
+    memcpy(&x, &b, sizeof x);
+    return x;
+#endif
+}
+
 // 1/k! for the Paterson-Stockmeyer family, as the reference computes it: k!
 // accumulated in double (exact for k <= 18), one correctly rounded division
 // (taylor_schemes.cpp:44-48)

@@ -558,7 +558,7 @@ __global__ void select_kernel(const unsigned long long* __restrict__ maxbits,
 __global__ void prep_kernel(const double* __restrict__ a, double* __restrict__ w, int n, int np,
                             const int32_t* __restrict__ list, const mexp_selection* __restrict__ sel) {
     const int64_t m = list[blockIdx.y];
-    const double f = ldexp(1.0, -sel[m].s);
+    const double f = pow2_neg(sel[m].s);
     for (int i = blockIdx.x; i < np; i += gridDim.x) {
         double* wr = w + m * int64_t(np) * np + int64_t(i) * np;
         const double* ar = a + m * int64_t(n) * n + int64_t(i) * n;

@@ -131,19 +131,23 @@ struct Group8T {
             if (!same) *reinterpret_cast<double2*>(tile + 512 + st) = make_double2(Y.v[0], Y.v[1]);
             __syncwarp();
             const char* ty = same ? tile : tile + 512;
-            double x[8];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const double2 v = *reinterpret_cast<const double2*>(tile + (rowb ^ (c << 4)));
-                x[2 * c] = v.x;
-                x[2 * c + 1] = v.y;
-            }
             double c0 = 0.0, c1 = 0.0;
+            // row r of X in two halves (k ascending): 8 registers live, not 16
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const double2 y = *reinterpret_cast<const double2*>(ty + (unit8(k, 0) ^ qx));
-                c0 = ExactOps::mac(c0, x[k], y.x);
-                c1 = ExactOps::mac(c1, x[k], y.y);
+            for (int h = 0; h < 2; ++h) {
+                double x[4];
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double2 v = *reinterpret_cast<const double2*>(tile + (rowb ^ ((2 * h + c) << 4)));
+                    x[2 * c] = v.x;
+                    x[2 * c + 1] = v.y;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double2 y = *reinterpret_cast<const double2*>(ty + (unit8(4 * h + k, 0) ^ qx));
+                    c0 = ExactOps::mac(c0, x[k], y.x);
+                    c1 = ExactOps::mac(c1, x[k], y.y);
+                }
             }
             C.v[0] = c0;
             C.v[1] = c1;
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
             } else {
                 const bool exact = rounding == MEXP_ROUND_REFERENCE ||
                                    (rounding == MEXP_ROUND_AUTO && s >= exact_s_min);
-                g.fscale = ldexp(1.0, -s);
+                g.fscale = pow2_neg(s);
                 if constexpr (kDefer) {
                     if (exact) {
                         if (lane == 0) worklist[atomicAdd(wcount, 1)] = int32_t(m);
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
         if (sl.status != MEXP_OK) {
             X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
         } else {
-            g.fscale = ldexp(1.0, -sl.s);
+            g.fscale = pow2_neg(sl.s);
             X = run_expm<ExactOps, family>(g, A, sl.degree, sl.s, 0);
         }
         st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));

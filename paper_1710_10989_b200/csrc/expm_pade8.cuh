@@ -91,10 +91,10 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
             const int degree = inf & 31, s = (inf >> 5) & 0x7fff, status = inf >> 20;
             if (status != MEXP_OK) continue;
             g.tile = wt + j * 1024;
-            g.fscale = ldexp(1.0, -s);
+            g.fscale = pow2_neg(s);
             const double2 v = *reinterpret_cast<const double2*>(g.tile + g.st);
             F A;
-            const double f = ldexp(1.0, -s);  // scaled(a, 2^-s), exact
+            const double f = pow2_neg(s);  // scaled(a, 2^-s), exact
             A.v[0] = __dmul_rn(f, v.x);
             A.v[1] = __dmul_rn(f, v.y);
             const bool exact = rounding == MEXP_ROUND_REFERENCE ||

@@ -606,7 +606,7 @@ __device__ __forceinline__ typename G::Frag run_expm(const G& g, const typename 
     using F = typename G::Frag;
     F A = A0;
     if (s > 0) {  // scaled(a, 2^-s) (expm.cpp:47 -> kernels.cpp:39-42), exact
-        const double f = ldexp(1.0, -s);
+        const double f = pow2_neg(s);
 #pragma unroll
         for (int e = 0; e < G::K; ++e) A.v[e] = __dmul_rn(f, A.v[e]);
     }

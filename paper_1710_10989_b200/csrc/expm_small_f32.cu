@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
             for (int e = 0; e < G::K; ++e) X.v[e] = make_float2(nan, nan);
         } else {
             if (sl.s > 0) {  // exact scaling by 2^-s, rounded once to float
-                const double f = ldexp(1.0, -sl.s);
+                const double f = pow2_neg(sl.s);
 #pragma unroll
                 for (int e = 0; e < G::K; ++e)
                     A.v[e] = make_float2(float(f * double(A.v[e].x)), float(f * double(A.v[e].y)));

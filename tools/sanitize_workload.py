@@ -42,6 +42,28 @@ def main():
     b = rng.uniform(-1, 1, (3, 100, 100))
     b *= (np.array([0.01, 1.0, 40.0]) / workloads.one_norm_batched(b))[:, None, None]
     mx.expm_batched_host(b, rounding=mx.ROUND_REFERENCE)
+    # the multi-device host entry (shards on one device), the dense layer
+    # (reference-rounded matmul, lincomb, one_norm, the exact LU) and the
+    # captured-graph ticket slots
+    import torch
+    mx.expm_batched_host_multi(workloads.generate("cfg2", 0, 999), devices=[0, 0, 0])
+    for n in (8, 50, 100):
+        d = torch.from_numpy(rng.uniform(-1, 1, (3, n, n))).cuda()
+        mx.matmul_batched(d, d)
+        mx.matmul_batched(d, d, rounding=mx.ROUND_FAST)
+        mx.lincomb_batched([1.0, -2.0, 0.5], [d, d, d])
+        mx.one_norm_batched(d)
+        mx.lu_solve_batched(d + n * torch.eye(n, dtype=d.dtype, device="cuda"), d)
+    g = torch.from_numpy(workloads.generate("cfg2", 0, 4096)).cuda()
+    o = torch.empty_like(g)
+    graph = torch.cuda.CUDAGraph()
+    mx.expm_batched(g, o)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph):
+        mx.expm_batched(g, o, stream=torch.cuda.current_stream())
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
     print("sanitize workload ok")
 
 
