@@ -428,6 +428,8 @@ def run_reference_arm(args):
     if rank != 0:
         return
     cfg = workloads.CONFIGS[args.config]
+    if cfg.batch == 1 and world > 1:
+        args.weak = True  # single-matrix configs run as replicas (as our arm does)
     value, rec = cpu_reference_measure(args.config, FAMILIES[args.family], args.steps, args.warmup,
                                        args.cpu_sample)
     per_rank = cfg.batch if args.weak else shard_range(0, world, cfg.batch).count
@@ -491,6 +493,11 @@ def run_ours(args):
     cfg = workloads.CONFIGS[args.config]
     n = cfg.n
     B = cfg.batch if not (dry and args.dry_batch) else args.dry_batch
+    if B == 1 and world > 1 and not args.weak:
+        # a single matrix (cfg1, cfg5) does not shard: replicas only
+        args.weak = True
+        if rank == 0:
+            print("bench.py: single-matrix config -> one replica per rank (--weak)", file=sys.stderr)
     shard = shard_range(rank, world, B, weak=args.weak)
     Bl = shard.count
     total = world * B if args.weak else B

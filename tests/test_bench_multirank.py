@@ -73,3 +73,19 @@ def test_reference_arm_config_matches_ours():
     assert "full 262144-matrix batch" in line["cpu_baseline"]["sample"]
     args = argparse.Namespace(config="cfg2", weak=False, rounding="auto", family="taylor-new")
     assert line["config"] == bench.workload_config(args, 1, 262144)
+
+
+def test_bench_dry_run_single_matrix_config_runs_replicas():
+    """cfg1 / cfg5 are one matrix: under N ranks each rank runs a replica
+    (replicas only), reported as weak scaling."""
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run",
+                        "--config", "cfg1", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = _json_line(r.stdout)
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak"
+    assert [x["count"] for x in line["ranks"]] == [1, 1]
+    assert line["config"]["global_batch"] == 2

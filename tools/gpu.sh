@@ -53,8 +53,10 @@ evidence)
     for c in cfg1 cfg3 cfg4 cfg5; do
         timeout 1200 python bench.py --config $c > $out/bench_$c.log 2>&1; line $out/bench_$c.log
     done
-    for c in cfg2 cfg4; do "$0" launches $c; done
-    for c in cfg2 cfg3 cfg4; do "$0" ncu $c; done ;;
+    for c in cfg2 cfg4 cfg5; do "$0" launches $c; done
+    for c in cfg2 cfg3 cfg4 cfg5; do "$0" ncu $c; done
+    "$0" ncu cfg2 fast
+    "$0" ncu cfg2 reference ;;
 launches)
     cfg=${2:-cfg2}
     python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $out/plain_$cfg.log 2>&1 && \
