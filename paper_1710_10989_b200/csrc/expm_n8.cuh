@@ -59,6 +59,9 @@ struct Group8T {
     uint32_t qx;     // q << 4: unit (k, q) = unit8(k, 0) ^ qx
     int r, q;
     double fscale;   // 2^-s, applied to the staged (unscaled) A by sq_first
+    // the scaled A's transposed DMMA operand, kept from sq_first for A3 = A2 A
+    static constexpr bool kKeepsAT = true;
+    mutable double bt0, bt1;
 
     __device__ __forceinline__ void init(char* warp_tile, int lane) {
         tile = warp_tile;
@@ -105,6 +108,8 @@ struct Group8T {
         } else {
             const double y0 = fscale * *reinterpret_cast<const double*>(tile + ld0);
             const double y1 = fscale * *reinterpret_cast<const double*>(tile + ld1);
+            bt0 = y0;
+            bt1 = y1;
             Frag C;
             C.v[0] = C.v[1] = 0.0;
             if constexpr (kSplit) {
@@ -117,6 +122,21 @@ struct Group8T {
                 dmma_8x8x4(C.v[0], C.v[1], A.v[0], y0);
                 dmma_8x8x4(C.v[0], C.v[1], A.v[1], y1);
             }
+            return C;
+        }
+    }
+
+    // X * A with the operand sq_first left in registers (no staging round
+    // trip; the same DMMA operand values, so the same bits)
+    template <class Ops>
+    __device__ __forceinline__ Frag mm_a(const Frag& X, const Frag& A) const {
+        if constexpr (Ops::kExact) {
+            return mm_impl<Ops>(X, A, false, nullptr);
+        } else {
+            Frag C;
+            C.v[0] = C.v[1] = 0.0;
+            dmma_8x8x4(C.v[0], C.v[1], X.v[0], bt0);
+            dmma_8x8x4(C.v[0], C.v[1], X.v[1], bt1);
             return C;
         }
     }

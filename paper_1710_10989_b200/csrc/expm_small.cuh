@@ -15,6 +15,8 @@
 // bit-identical to the reference's no-FMA i-k-j loop).
 #pragma once
 
+#include <type_traits>
+
 #include "expm_common.cuh"
 
 namespace mexp_b200 {
@@ -272,6 +274,21 @@ __device__ __forceinline__ F addm(const F& a, const F& b) {
     return r;
 }
 
+// A3 = A2 * A. Groups that keep the scaled A's product operand from sq_first
+// in registers (kKeepsAT: the 8x8 warp group) skip restaging A.
+template <class G, class = void>
+struct keeps_at : std::false_type {};
+template <class G>
+struct keeps_at<G, std::void_t<decltype(G::kKeepsAT)>> : std::bool_constant<G::kKeepsAT> {};
+template <class Ops, class G>
+__device__ __forceinline__ typename G::Frag mm_by_a(const G& g, const typename G::Frag& X,
+                                                    const typename G::Frag& A) {
+    if constexpr (keeps_at<G>::value)
+        return g.template mm_a<Ops>(X, A);
+    else
+        return g.template mm<Ops>(X, A, false);
+}
+
 // ---- the schemes (reference taylor_schemes.cpp:104-157, 211-227) -----------
 template <class Ops, class G>
 __device__ typename G::Frag eval_taylor_new(const G& g, int degree, const typename G::Frag& A) {
@@ -301,7 +318,7 @@ __device__ typename G::Frag eval_taylor_new(const G& g, int degree, const typena
         }
         case 12: {  // eval_t12, 4 products
             const F A2 = g.template sq_first<Ops>(A);
-            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F A3 = mm_by_a<Ops>(g, A2, A);
             F B[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -311,7 +328,7 @@ __device__ typename G::Frag eval_taylor_new(const G& g, int degree, const typena
         }
         default: {  // 18: eval_t18, 5 products
             const F A2 = g.template sq_first<Ops>(A);
-            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F A3 = mm_by_a<Ops>(g, A2, A);
             const F A6 = g.template mm<Ops>(A3, A3, true);
             if constexpr (G::S::STASH >= 4) {
                 // register-lean order for large fragments: B1, B5, B4, B3 to the
@@ -353,7 +370,7 @@ __device__ typename G::Frag eval_taylor_ps(const G& g, int degree, const typenam
             return eval_taylor_new<Ops>(g, degree, A);  // the same eval_ps(2), eval_ps(4)
         case 6: {
             const F A2 = g.template sq_first<Ops>(A);
-            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F A3 = mm_by_a<Ops>(g, A2, A);
             const F f0 = lc<Ops, true>(1.0, I, 1.0, A, inv_fact(2), A2);
             const F f1 = lc<Ops, true>(inv_fact(3), I, inv_fact(4), A, inv_fact(5), A2);
             const F inner = lc<Ops>(1.0, f1, inv_fact(6), A3);
@@ -361,7 +378,7 @@ __device__ typename G::Frag eval_taylor_ps(const G& g, int degree, const typenam
         }
         case 9: {
             const F A2 = g.template sq_first<Ops>(A);
-            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F A3 = mm_by_a<Ops>(g, A2, A);
             const F f0 = lc<Ops, true>(inv_fact(0), I, inv_fact(1), A, inv_fact(2), A2);
             const F f1 = lc<Ops, true>(inv_fact(3), I, inv_fact(4), A, inv_fact(5), A2);
             const F f2 = lc<Ops, true>(inv_fact(6), I, inv_fact(7), A, inv_fact(8), A2);
@@ -371,7 +388,7 @@ __device__ typename G::Frag eval_taylor_ps(const G& g, int degree, const typenam
         }
         default: {  // 16
             const F A2 = g.template sq_first<Ops>(A);
-            const F A3 = g.template mm<Ops>(A2, A, false);
+            const F A3 = mm_by_a<Ops>(g, A2, A);
             const F A4 = g.template mm<Ops>(A2, A2, true);
             F gk[4];
 #pragma unroll
