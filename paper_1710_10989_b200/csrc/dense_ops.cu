@@ -365,16 +365,13 @@ int lu_solve_dev(const double* m, const double* r, double* x, int n, int64_t bat
 
 // ---- composite routines on one matrix, intermediates on the device -----------
 
-// host copies of the device coefficient tables (expm_common.cuh), read once
+// the scheme coefficients, from the same literals as the kernels' tables
+// (scheme_tables.h)
 struct Tables {
-    double t12[4][4], t18a[4], t18b[4][5];
+    double t12[4][4] = MEXP_T12_TABLE;
+    double t18a[4] = MEXP_T18A_TABLE;
+    double t18b[4][5] = MEXP_T18B_TABLE;
 };
-int load_tables(Tables& t) {
-    DCUDA(cudaMemcpyFromSymbol(t.t12, c_t12, sizeof t.t12));
-    DCUDA(cudaMemcpyFromSymbol(t.t18a, c_t18a, sizeof t.t18a));
-    DCUDA(cudaMemcpyFromSymbol(t.t18b, c_t18b, sizeof t.t18b));
-    return MEXP_OK;
-}
 
 // Psi9 coefficients: closed forms in sqrt(7), rounded once from long double
 // (taylor_schemes.cpp:29-42)
@@ -785,8 +782,7 @@ int mexp_b200_dense_call(int op, int arg, const double* const* in, int nin, cons
         DCUDA(cudaStreamSynchronize(st));
         return MEXP_OK;
     }
-    Tables t{};
-    if (op == 6 || op == 7 || op == 13) TRY(load_tables(t));
+    const Tables t;
     TRY(p.init(in[0], 16));
     constexpr int OUT = 15;
     switch (op) {
