@@ -16,6 +16,7 @@
 #include "device_once.hpp"
 #include "expm_small.cuh"
 #include "expm_small_f32.cuh"
+#include "expm_pairs32.cuh"
 
 namespace mexp_b200 {
 
@@ -450,7 +451,10 @@ int run_small_f32_family(const float* d_a, float* d_out, mexp_selection* d_sel, 
     switch (np) {
         case 8: return launch_f32<8, 8, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
         case 16: return launch_f32<16, 4, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
-        case 32: return launch_f32<32, 2, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
+        case 32:
+            if (kFamily == MEXP_FAMILY_TAYLOR_NEW && pairs32_enabled(batch))
+                return run_pairs32_f32(d_a, d_out, d_sel, batch, acc_arg, st, launches);
+            return launch_f32<32, 2, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
         case 64: return launch_f32<64, 1, kFamily>(d_a, d_out, d_sel, batch, acc_arg, st, launches);
     }
     return MEXP_ERR_UNSUPPORTED;
