@@ -763,6 +763,7 @@ int sm_count_pairs() {
 // chunks of 4096 matrices measured e2e 9.6e6 vs 1.0e7 expm/s). Read per call
 // (a getenv), so tests can compare both kernels in one process.
 bool pairs32_enabled(int64_t batch) {
+    if (batch > (int64_t(1) << 31) - 2) return false;  // the class list holds int32 indices
     const char* e = std::getenv("MEXP_F32_PAIRS");
     if (e) return std::atoi(e) != 0;
     return batch >= 8192;

@@ -4,7 +4,7 @@ runs on buffers carved out of larger allocations filled with a canary
 pattern; after the call the canaries before and after each input, output and
 record buffer must be untouched, and the inputs unchanged. Covers the 8x8
 kernels (every rounding, work tickets, captured graphs), the n <= 64 group
-kernels (padded n, fp32), the 64x64 cluster kernel, the large-n GEMM chain
+kernels (padded n, fp32), the 32x32 fp32 pair kernel, the 64x64 cluster kernel, the large-n GEMM chain
 (TaylorNew, PS, Pade LU), the dense layer and the multi-device host entry.
 """
 import numpy as np
@@ -48,6 +48,17 @@ CASES = [  # (n, batch, dtype, family, rounding)
 
 @pytest.mark.parametrize("n,batch,dt,family,rounding", CASES)
 def test_expm_batched_stays_in_bounds(cuda, n, batch, dt, family, rounding):
+    _in_bounds(n, batch, dt, family, rounding)
+
+
+@pytest.mark.parametrize("n,batch", [(32, 333), (20, 101), (32, 8193)])
+def test_pair_kernel_stays_in_bounds(cuda, n, batch, monkeypatch):
+    # the 32x32 fp32 pair kernel and its pre-pass (csrc/expm32_pairs.cu), forced at any batch
+    monkeypatch.setenv("MEXP_F32_PAIRS", "1")
+    _in_bounds(n, batch, "f32", 0, mx.ROUND_AUTO)
+
+
+def _in_bounds(n, batch, dt, family, rounding):
     import torch
     tdt = torch.float64 if dt == "f64" else torch.float32
     rng = np.random.default_rng(n * 1000 + batch)
