@@ -170,21 +170,20 @@ __global__ void __launch_bounds__(512) scatter32_kernel(const uint32_t* __restri
 // 32x32b shape: thread t of the warp reads / writes TMEM lane (quadrant base +
 // t), consecutive 32-bit columns. Slot k of a lane's matrix = columns
 // [64k, 64k + 64), row r of the lane's 8x8 tile at 64k + 8r.
+// (no "memory" clobbers: TMEM is not generic memory, the tcgen05 asm
+// statements keep their order among themselves as volatile asm, and the
+// compiler stays free to hoist the next row's shared-memory loads above them)
 __device__ __forceinline__ void tm_st8(uint32_t addr, const float (&v)[8]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(addr),
-        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
-        : "memory");
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]));
 }
-__device__ __forceinline__ void tm_wait_st() {
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;"); }
 __device__ __forceinline__ void tm_ld8(uint32_t addr, float (&v)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
                    "=f"(v[6]), "=f"(v[7])
-                 : "r"(addr)
-                 : "memory");
+                 : "r"(addr));
 }
 // completes every outstanding tcgen05.ld of the thread; the operands tie the
 // loaded registers to the wait so no use is scheduled above it
@@ -192,7 +191,7 @@ __device__ __forceinline__ void tm_wait_ld(float (&v)[8], float (&w)[8]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
                    "+f"(v[6]), "+f"(v[7]), "+f"(w[0]), "+f"(w[1]), "+f"(w[2]), "+f"(w[3]),
-                   "+f"(w[4]), "+f"(w[5]), "+f"(w[6]), "+f"(w[7])::"memory");
+                   "+f"(w[4]), "+f"(w[5]), "+f"(w[6]), "+f"(w[7]));
 }
 
 using Acc = float2[32];  // the lane's 8x8 tile: row r = pairs 4r .. 4r+3
