@@ -1048,20 +1048,33 @@ int mexp_b200_reference_expm_host(const double* a, double* out, int n, int64_t b
                           acc_arg(MEXP_ACCURACY_DOUBLE, kFamilyPadeReference), rounding, sel, nullptr);
 }
 
-// library-internal helper for the C++ drop-in mexp::squarings (dropin.cpp)
+// library-internal helper for the C++ drop-in mexp::squarings (dropin.cpp):
+// on the device's host-pipe stream, with the matrix in a stream-ordered
+// buffer of the library's memory pool (no cudaMalloc / cudaFree per call)
 int mexp_b200_squarings_host(double* x, int n, int s) {
     const int dv = device_ok();
     if (dv != MEXP_OK) return dv;
-    double* d = nullptr;
+    if (s <= 0) return MEXP_OK;
+    HostPipe& p = pipe_for_current_device();
+    std::lock_guard<std::mutex> lock(p.mu);
+    {
+        const int e = ensure_pipe(p, 0, 0);  // the streams
+        if (e != MEXP_OK) return e;
+    }
+    cudaStream_t st = p.st[0];
     const size_t bytes = sizeof(double) * size_t(n) * n;
-    MEXP_CUDA(cudaMalloc(&d, bytes));
     int r = MEXP_OK;
-    if (cudaMemcpy(d, x, bytes, cudaMemcpyHostToDevice) != cudaSuccess) r = MEXP_ERR_CUDA;
-    // the reference's squarings (expm.cpp:31-35), bit for bit
-    if (r == MEXP_OK) r = squarings_f64(d, n, 1, s, MEXP_ROUND_REFERENCE, nullptr, &g_launches);
-    if (r == MEXP_OK && cudaMemcpy(x, d, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
-        r = MEXP_ERR_CUDA;
-    cudaFree(d);
+    {
+        AsyncBuffer buf(st);
+        if (buf.alloc(bytes) != cudaSuccess) return cuda_fail(cudaGetLastError(), "squarings alloc");
+        double* d = buf.get<double>();
+        if (cudaMemcpyAsync(d, x, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) r = MEXP_ERR_CUDA;
+        // the reference's squarings (expm.cpp:31-35), bit for bit
+        if (r == MEXP_OK) r = squarings_f64(d, n, 1, s, MEXP_ROUND_REFERENCE, st, &g_launches);
+        if (r == MEXP_OK && cudaMemcpyAsync(x, d, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+            r = MEXP_ERR_CUDA;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess && r == MEXP_OK) r = MEXP_ERR_CUDA;
     if (r == MEXP_ERR_CUDA && g_last_cuda_error.empty()) g_last_cuda_error = large_last_error();
     return r;
 }
