@@ -17,7 +17,7 @@
 // warp-collective), so the two matrices must share (degree, s). A pre-pass
 // (select32_kernel: finite check, exact fp64 1-norm, selection record --
 // kernels.cpp:44-53, expm.cpp:11-29) computes each matrix's class, and a
-// counting sort (scan32_kernel, scatter32_kernel) lists the matrices by class,
+// counting sort (scatter32_kernel) lists the matrices by class,
 // most expensive first; the main kernel takes consecutive pairs of that list.
 // A pair whose classes differ (at most one per class boundary) runs as two
 // passes with both halves on one matrix.
@@ -125,44 +125,38 @@ __global__ void __launch_bounds__(256) select32_kernel(const float* __restrict__
         if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-// exclusive scan of the class histogram -> first list position of each class
-__global__ void __launch_bounds__(1024) scan32_kernel(const int* __restrict__ hist,
-                                                      int* __restrict__ cursor) {
-    __shared__ int s[1024];
+// List position of every matrix. Each block scans the class histogram itself
+// (513 counts: cheaper than a separate launch), reserves one range per class
+// for its chunk from the running per-class counters, then places its
+// matrices in it (order inside a class is irrelevant: every matrix's
+// arithmetic is independent of its partner's).
+__global__ void __launch_bounds__(1024) scatter32_kernel(const uint32_t* __restrict__ info,
+                                                         const int* __restrict__ hist,
+                                                         int* __restrict__ running,
+                                                         int2* __restrict__ list, int64_t batch) {
+    __shared__ int start[1024], lh[kNumKeys], base[kNumKeys];
+    __shared__ int rank[kScatterChunk];
     const int t = threadIdx.x;
     const int v = t < kNumKeys ? hist[t] : 0;
-    s[t] = v;
+    start[t] = v;
+    if (t < kNumKeys) lh[t] = 0;
     __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        const int x = t >= off ? s[t - off] : 0;
+    for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan
+        const int x = t >= off ? start[t - off] : 0;
         __syncthreads();
-        s[t] += x;
+        start[t] += x;
         __syncthreads();
     }
-    if (t < kNumKeys) cursor[t] = s[t] - v;
-}
-
-// list position of every matrix: a block reserves one range per class for its
-// chunk, then places its matrices in it (order inside a class is irrelevant:
-// every matrix's arithmetic is independent of its partner's)
-__global__ void __launch_bounds__(512) scatter32_kernel(const uint32_t* __restrict__ info,
-                                                        int* __restrict__ cursor,
-                                                        int2* __restrict__ list, int64_t batch) {
-    __shared__ int lh[kNumKeys], base[kNumKeys];
-    __shared__ int rank[kScatterChunk];
-    for (int i = threadIdx.x; i < kNumKeys; i += blockDim.x) lh[i] = 0;
-    __syncthreads();
     const int64_t m0 = int64_t(blockIdx.x) * kScatterChunk;
     const int cnt = int(batch - m0 < kScatterChunk ? batch - m0 : kScatterChunk);
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
-        rank[i] = atomicAdd(&lh[info_key(info[m0 + i])], 1);
+    for (int i = t; i < cnt; i += blockDim.x) rank[i] = atomicAdd(&lh[info_key(info[m0 + i])], 1);
     __syncthreads();
-    for (int k = threadIdx.x; k < kNumKeys; k += blockDim.x)
-        if (lh[k]) base[k] = atomicAdd(&cursor[k], lh[k]);
+    for (int k = t; k < kNumKeys; k += blockDim.x)
+        if (lh[k]) base[k] = start[k] - hist[k] + atomicAdd(&running[k], lh[k]);
     __syncthreads();
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-        const uint32_t v = info[m0 + i];
-        list[base[info_key(v)] + rank[i]] = make_int2(int(m0 + i), int(v));
+    for (int i = t; i < cnt; i += blockDim.x) {
+        const uint32_t w = info[m0 + i];
+        list[base[info_key(w)] + rank[i]] = make_int2(int(m0 + i), int(w));
     }
 }
 
@@ -781,7 +775,7 @@ int run_pairs32_f32(const float* d_a, float* d_out, mexp_selection* d_sel, int64
     attr_once([] {
         cudaFuncSetAttribute(expm32_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     });
-    // workspace: [hist | cursor] ints, packed (degree, s, status) per matrix,
+    // workspace: [hist | running] ints, packed (degree, s, status) per matrix,
     // the class-sorted list {m, info}, and selection records when the caller
     // passes none (the pair kernel reads (m, s) from the list)
     const size_t hist_bytes = 2 * 1024 * sizeof(int);
@@ -792,24 +786,23 @@ int run_pairs32_f32(const float* d_a, float* d_out, mexp_selection* d_sel, int64
     if (ws.alloc(hist_bytes + info_bytes + list_bytes + sel_bytes) != cudaSuccess) return MEXP_ERR_CUDA;
     char* w = ws.get<char>();
     int* hist = reinterpret_cast<int*>(w);
-    int* cursor = hist + 1024;
+    int* running = hist + 1024;
     uint32_t* info = reinterpret_cast<uint32_t*>(w + hist_bytes);
     int2* list = reinterpret_cast<int2*>(w + hist_bytes + info_bytes);
     mexp_selection* sel = d_sel ? d_sel
                                 : reinterpret_cast<mexp_selection*>(w + hist_bytes + info_bytes + list_bytes);
-    if (cudaMemsetAsync(hist, 0, 1024 * sizeof(int), st) != cudaSuccess) return MEXP_ERR_CUDA;
+    if (cudaMemsetAsync(hist, 0, 2 * 1024 * sizeof(int), st) != cudaSuccess) return MEXP_ERR_CUDA;
     const int sms = sm_count_pairs();
     const int64_t sblocks = (batch + 7) / 8;
     const int sgrid = int(sblocks < 8 * sms ? sblocks : 8 * sms);
     select32_kernel<<<sgrid, 256, 0, st>>>(d_a, sel, info, hist, batch, accuracy & 15);
-    scan32_kernel<<<1, 1024, 0, st>>>(hist, cursor);
     const int cgrid = int((batch + kScatterChunk - 1) / kScatterChunk);
-    scatter32_kernel<<<cgrid, 512, 0, st>>>(info, cursor, list, batch);
+    scatter32_kernel<<<cgrid, 1024, 0, st>>>(info, hist, running, list, batch);
     const int64_t npairs = (batch + 1) / 2;
     const int64_t want = (npairs + kWarps - 1) / kWarps;
     const int grid = int(want < kCtasPerSm * sms ? want : kCtasPerSm * sms);
     expm32_pairs_kernel<<<grid, 32 * kWarps, kSmemBytes, st>>>(d_a, d_out, list, batch);
-    launches->fetch_add(4, std::memory_order_relaxed);
+    launches->fetch_add(3, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? MEXP_OK : MEXP_ERR_CUDA;
 }
 
