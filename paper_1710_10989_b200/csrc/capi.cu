@@ -767,14 +767,23 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
     mexp_selection* hs = sel_pinned ? h_sel : p.h_sel_scratch;
     const char* src = static_cast<const char*>(h_a);
     char* dst = static_cast<char*>(h_out);
-    // Chunk plan. Small n: chunk sizes taper to 1/8 at both ends, so the
-    // pipeline fills (first H2D before any D2H) and drains (last D2H after
-    // the last H2D) in ~1/8 of a chunk's copy time instead of a whole one.
+    // Chunk plan. Small n: chunk sizes taper (doubling from MEXP_HOST_TAPER_KB,
+    // default 1/8 of a chunk) at both ends, so the pipeline fills (first H2D
+    // before any D2H) and drains (last D2H after the last H2D) in a fraction
+    // of a chunk's copy time instead of a whole one.
+    static const size_t taper_bytes = [] {
+        const char* e = std::getenv("MEXP_HOST_TAPER_KB");
+        return e ? size_t(std::atoi(e)) << 10 : size_t(0);
+    }();
     std::vector<std::pair<int64_t, int64_t>> plan;  // (b0, count)
     {
-        std::vector<int64_t> sizes;
-        const bool taper = n <= 64 && batch >= 4 * chunk && chunk >= 8;
-        const int64_t head[3] = {chunk / 8, chunk / 4, chunk / 2};
+        std::vector<int64_t> sizes, head;
+        int64_t minc = taper_bytes ? int64_t(taper_bytes / mat_bytes) : chunk / 8;
+        if (minc < 1) minc = 1;
+        for (int64_t h = minc; h < chunk; h *= 2) head.push_back(h);
+        int64_t hsum = 0;
+        for (int64_t h : head) hsum += h;
+        const bool taper = n <= 64 && chunk >= 8 && batch >= 2 * hsum + 2 * chunk;
         int64_t left = batch;
         if (taper)
             for (int64_t h : head) {
@@ -787,7 +796,7 @@ int expm_host_impl(const void* h_a, void* h_out, int dtype, int n, int64_t batch
             left -= c;
         }
         if (taper)
-            for (int i = 2; i >= 0; --i) sizes.push_back(head[i]);
+            for (int i = int(head.size()) - 1; i >= 0; --i) sizes.push_back(head[i]);
         int64_t b0 = 0;
         for (int64_t c : sizes) {
             plan.emplace_back(b0, c);

@@ -27,7 +27,7 @@ def main():
         mx.expm_batched_host(a, out)
         ts.append(time.perf_counter() - t0)
     ms = 1e3 * np.median(ts)
-    print(f"streams={os.environ.get('MEXP_HOST_STREAMS', '4')} chunk_mb={os.environ.get('MEXP_HOST_CHUNK_MB', '16')} "
+    print(f"streams={os.environ.get('MEXP_HOST_STREAMS', '4')} chunk_mb={os.environ.get('MEXP_HOST_CHUNK_MB', '16')} taper_kb={os.environ.get('MEXP_HOST_TAPER_KB', '-')} "
           f"median {ms:.3f} ms best {1e3 * min(ts):.3f} ms -> {a.shape[0] / (ms * 1e-3):.3e} expm/s")
 
 

@@ -53,7 +53,7 @@ evidence)
     for c in cfg1 cfg3 cfg4 cfg5; do
         timeout 1200 python bench.py --config $c > $out/bench_$c.log 2>&1; line $out/bench_$c.log
     done
-    for c in cfg2 cfg4 cfg5; do "$0" launches $c; done
+    for c in cfg2 cfg3 cfg4 cfg5; do "$0" launches $c; done
     for c in cfg2 cfg3 cfg4 cfg5; do "$0" ncu $c; done
     "$0" ncu cfg2 fast
     "$0" ncu cfg2 reference ;;
