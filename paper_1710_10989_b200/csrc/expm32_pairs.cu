@@ -49,7 +49,12 @@ constexpr int kTmemCols = 128;               // 2 slots x 64 columns per lane
 #endif
 constexpr int kCtasPerSm = MEXP_PAIRS_CTAS;  // CTAs of 4 warps per SM (TMEM: 128 columns each)
 constexpr int kBufFloats = NN + N;           // a 32x32 operand buffer + one pad row
-constexpr int kHalfFloats = 2 * kBufFloats + NN;  // X, Y, and the next pair's matrix (prefetch)
+#ifndef MEXP_PAIRS_PREFETCH
+#define MEXP_PAIRS_PREFETCH 1
+#endif
+constexpr bool kPrefetch = MEXP_PAIRS_PREFETCH;
+// X, Y, and the next pair's matrix (prefetch)
+constexpr int kHalfFloats = 2 * kBufFloats + (kPrefetch ? NN : 0);
 constexpr int kSmemBytes = kWarps * 2 * kHalfFloats * 4 + 16;
 static_assert(kCtasPerSm * kSmemBytes <= 227 * 1024, "smem");
 static_assert(kCtasPerSm * kTmemCols <= 512, "tmem");
@@ -612,6 +617,7 @@ __device__ __forceinline__ void store_tile(const Lane& L, float* m, const Acc& C
 // into the operand buffers' swizzled layout (each lane later reads back only
 // the chunks it copied itself)
 __device__ __forceinline__ void prefetch_tile(const Lane& L, float* pbuf, const float* m) {
+    if constexpr (!kPrefetch) return;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
         const int i = 8 * L.ti + r;
@@ -700,7 +706,7 @@ __global__ void __launch_bounds__(32 * kWarps, kCtasPerSm)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) C[e] = make_float2(nan, nan);
             } else {
-                if (joint)
+                if (joint && kPrefetch)
                     load_tile_smem(L, pbuf, C);
                 else
                     load_tile(L, a + m * NN, C);
