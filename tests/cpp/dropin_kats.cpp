@@ -13,7 +13,9 @@
 #include <limits>
 #include <random>
 #include <stdexcept>
+#include <vector>
 
+#include "mexp/batched.hpp"
 #include "mexp/expm.hpp"
 #include "mexp/kernels.hpp"
 #include "mexp/pade.hpp"
@@ -268,14 +270,62 @@ static void dense_layer_cases() {
     CHECK(psi9_coefficients().x2 == -0.25 && psi9_coefficients().x3 == -1.0);
 }
 
+// the batched C++ API (include/mexp/batched.hpp): every record and every
+// e^A equals mexp::expm's for the same matrix; per-matrix errors stay in the
+// records, call-level errors throw
+static void batched_cases() {
+    std::mt19937_64 rng(7);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    const int n = 8, batch = 6;
+    std::vector<double> a(size_t(batch) * n * n), out(a.size());
+    const double scale[batch] = {1e-4, 0.02, 0.3, 1.0, 5.0, 40.0};
+    for (int b = 0; b < batch; ++b)
+        for (int e = 0; e < n * n; ++e) a[size_t(b) * n * n + e] = scale[b] * u(rng);
+    a[size_t(3) * n * n + 10] = std::numeric_limits<double>::quiet_NaN();
+    const BatchResult r = expm_batched(a.data(), out.data(), n, batch, Accuracy::Double);
+    CHECK(r.records.size() == size_t(batch) && r.first_error == 3);
+    for (int b = 0; b < batch; ++b) {
+        DenseMatrix m(n);
+        std::memcpy(m.data(), a.data() + size_t(b) * n * n, sizeof(double) * n * n);
+        if (b == 3) {
+            CHECK(r.records[b].status == 1 && std::isnan(out[size_t(b) * n * n]));
+            continue;
+        }
+        const ExpmReport rep = expm(m, Accuracy::Double, Family::TaylorNew);
+        CHECK(r.records[b].status == 0 && r.records[b].degree == rep.degree && r.records[b].s == rep.s);
+        CHECK(r.records[b].norm_in == rep.norm_in);
+        CHECK(std::memcmp(rep.result.data(), out.data() + size_t(b) * n * n, sizeof(double) * n * n) == 0);
+    }
+    // fp32, 32 x 32, Single table: the selection equals mexp::select on the fp64 norm
+    const int m32 = 32, b32 = 3;
+    std::vector<float> f(size_t(b32) * m32 * m32), fo(f.size());
+    for (auto& x : f) x = float(0.05 * u(rng));
+    const BatchResult rf = expm_batched(f.data(), fo.data(), m32, b32, Accuracy::Single);
+    const SelectionTable st = selection_table(Family::TaylorNew, Accuracy::Single);
+    for (int b = 0; b < b32; ++b) {
+        const Selection want = select(rf.records[b].norm_in, st);
+        CHECK(rf.records[b].status == 0 && rf.records[b].degree == want.degree && rf.records[b].s == want.s);
+    }
+    CHECK(rf.first_error == -1);
+    // the multi-device entry gives the same bits (devices: all visible)
+    std::vector<double> out2(a.size());
+    const BatchResult r2 = expm_batched_multi(a.data(), out2.data(), n, batch, Accuracy::Double);
+    CHECK(r2.first_error == 3 && std::memcmp(out.data(), out2.data(), sizeof(double) * n * n * 3) == 0);
+    CHECK(throws<std::invalid_argument>([&] { expm_batched(a.data(), out.data(), 0, 1, Accuracy::Double); }));
+    CHECK(throws<std::invalid_argument>([&] { expm_batched(a.data(), out.data(), n, -1, Accuracy::Double); }));
+}
+
 int main(int argc, char** argv) {
     const bool no_device = argc > 1 && std::strcmp(argv[1], "--no-device") == 0;
     host_only();
     if (no_device) {
         CHECK(throws<std::runtime_error>([] { expm(DenseMatrix(2), Accuracy::Double, Family::TaylorNew); }));
+        double x[4] = {0, 0, 0, 0}, y[4];
+        CHECK(throws<std::runtime_error>([&] { expm_batched(x, y, 2, 1, Accuracy::Double); }));
     } else {
         device_cases();
         dense_layer_cases();
+        batched_cases();
     }
     std::printf("%s: %d failure(s)\n", no_device ? "dropin_kats --no-device" : "dropin_kats", failures);
     return failures == 0 ? 0 : 1;
