@@ -59,7 +59,7 @@ constexpr int kSmemBytes = kWarps * 2 * kHalfFloats * 4 + 16;
 static_assert(kCtasPerSm * kSmemBytes <= 227 * 1024, "smem");
 static_assert(kCtasPerSm * kTmemCols <= 512, "tmem");
 constexpr int kNumKeys = 64 * 8 + 1;
-constexpr int kScatterChunk = 2048;
+constexpr int kScatterChunk = 512;  // matrices per scatter block (>= the SM count of blocks for cfg3)
 
 // class key, ascending = most products first (the main kernel's pairs are
 // handed out in key order, so the expensive ones start first)
