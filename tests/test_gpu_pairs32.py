@@ -22,11 +22,11 @@ pytestmark = pytest.mark.gpu
 U24 = 2.0 ** -24
 
 
-def _run(a, pairs):
+def _run(a, pairs, accuracy=mx.Accuracy.Single):
     old = os.environ.get("MEXP_F32_PAIRS")
     os.environ["MEXP_F32_PAIRS"] = "1" if pairs else "0"
     try:
-        out, sel, st = mx.expm_batched_host(a, accuracy=mx.Accuracy.Single, raise_on_error=False)
+        out, sel, st = mx.expm_batched_host(a, accuracy=accuracy, raise_on_error=False)
     finally:
         if old is None:
             del os.environ["MEXP_F32_PAIRS"]
@@ -133,3 +133,13 @@ def test_pairs_pipelined_under_graph_capture(cuda):
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
     assert torch.equal(sel, sel_ref)
+
+
+def test_pairs_double_table(cuda):
+    # fp32 storage with the Double table: larger s for the same norms, every degree
+    a = _spread(32, 2049, seed=5, lo=1e-12, hi=1e4)
+    o1, s1 = _run(a, True, mx.Accuracy.Double)
+    o0, s0 = _run(a, False, mx.Accuracy.Double)
+    assert np.array_equal(s1.view(np.uint8), s0.view(np.uint8))
+    assert _same_bits(o1, o0)
+    assert s1["s"].max() >= 10
