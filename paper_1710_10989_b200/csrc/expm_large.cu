@@ -368,8 +368,12 @@ template <int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, GEMM_MIN_CTAS)
     gemm_dmma_kernel(GemmArgs g, const __grid_constant__ CUtensorMap tmx) {
     extern __shared__ __align__(16) double smem_raw[];
-    double* const smem = reinterpret_cast<double*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned (the 128-byte TMA swizzle), derived from smem_raw by
+    // pointer arithmetic so the compiler keeps the shared address space: the
+    // fragment loads are LDS, not generic LD (a pointer rebuilt through
+    // uintptr_t loses it)
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+    double* const smem = smem_raw + ((((sbase + 1023u) & ~1023u) - sbase) / sizeof(double));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / WARPS_N, wn = warp % WARPS_N;
     const int r = lane >> 2, q = lane & 3;
