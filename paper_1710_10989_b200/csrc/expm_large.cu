@@ -567,6 +567,19 @@ __global__ void prep_kernel(const double* __restrict__ a, double* __restrict__ w
                             const int32_t* __restrict__ list, const mexp_selection* __restrict__ sel) {
     const int64_t m = list[blockIdx.y];
     const double f = pow2_neg(sel[m].s);
+    if (n == np && (n & 1) == 0) {
+        // unpadded: a flat scaled copy in 16-byte units (the input is read
+        // once: evict-first)
+        const int64_t half = int64_t(n) * n / 2;
+        const double2* src = reinterpret_cast<const double2*>(a + m * int64_t(n) * n);
+        double2* dst = reinterpret_cast<double2*>(w + m * int64_t(np) * np);
+        for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < half;
+             e += int64_t(gridDim.x) * blockDim.x) {
+            const double2 v = __ldcs(src + e);
+            dst[e] = make_double2(f * v.x, f * v.y);
+        }
+        return;
+    }
     for (int i = blockIdx.x; i < np; i += gridDim.x) {
         double* wr = w + m * int64_t(np) * np + int64_t(i) * np;
         const double* ar = a + m * int64_t(n) * n + int64_t(i) * n;
