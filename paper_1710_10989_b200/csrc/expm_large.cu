@@ -136,6 +136,12 @@ struct GemmArgs {
     int np;
     int64_t mstride;      // np * np
     int n;                // the true dimension: the exact product sums k < n only
+    // prep-free T18 on the unscaled input (DMMA pass only): c *= 2^-(scale_c s)
+    // and in[0] *= 2^-s on load, s = sel[matrix].s -- exact power-of-two
+    // scalings, so the values equal those of the scaled copy
+    const mexp_selection* sel;
+    int scale_c;
+    int scale_in0;
 };
 
 // Left-to-right linear combination c0*m0 + c1*m1 + ... in the arithmetic of
@@ -385,6 +391,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, GEMM_MIN_CTAS)
     const double* Y = g.Y + base;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int ktiles = g.np / BK;
+    double fc = 1.0, f0 = 1.0;
+    if (g.scale_c | g.scale_in0) {
+        const int s = g.sel[mat].s;
+        if (g.scale_c) fc = pow2_neg(g.scale_c * s);
+        if (g.scale_in0) f0 = pow2_neg(s);
+    }
 
     auto stage_a = [&](int s) { return smem + s * STAGE_DOUBLES; };
     auto stage_b = [&](int s) { return smem + s * STAGE_DOUBLES + A_DOUBLES; };
@@ -504,10 +516,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, GEMM_MIN_CTAS)
 #pragma unroll
         for (int j = 0; j < TN; ++j)
             pre[j] = epi_load<EPI>(g, base, m0 + wm * WM + i * 8 + r, n0 + wn * WN + j * 8 + 2 * q);
+        if (g.scale_in0)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) pre[j].v[0] = make_double2(f0 * pre[j].v[0].x, f0 * pre[j].v[0].y);
 #pragma unroll
         for (int j = 0; j < TN; ++j)
             epilogue_pair<EPI, FastOps>(g, out0, base, m0 + wm * WM + i * 8 + r,
-                                        n0 + wn * WN + j * 8 + 2 * q, acc[i][j][0], acc[i][j][1], pre[j]);
+                                        n0 + wn * WN + j * 8 + 2 * q, fc * acc[i][j][0], fc * acc[i][j][1],
+                                        pre[j]);
     }
 }
 
@@ -674,11 +690,15 @@ bool make_x_map(CUtensorMap* map, const double* base, int np, int64_t batch) {
 thread_local int64_t g_map_batch = 0;  // matrices per workspace buffer of the current call
 thread_local int g_exact_n = 0;         // > 0: products in reference rounding over k < g_exact_n
 
+struct Scaling {  // the prep-free T18 path's per-matrix power-of-two scalings (GemmArgs)
+    const mexp_selection* sel = nullptr;
+    int c = 0, in0 = 0;
+};
 template <int EPI>
 int gemm(const double* X, const double* Y, std::initializer_list<const double*> in,
          std::initializer_list<double*> out, const int32_t* d_list, int count, int np,
          cudaStream_t st, std::atomic<uint64_t>* launches, double* final_out = nullptr,
-         const double (*lc)[5] = nullptr, int nlc = 0) {
+         const double (*lc)[5] = nullptr, int nlc = 0, Scaling sc = Scaling{}) {
     if (count == 0) return MEXP_OK;
     static PerDevice attr_once;
     attr_once([] {
@@ -709,6 +729,10 @@ int gemm(const double* X, const double* Y, std::initializer_list<const double*> 
     g.np = np;
     g.mstride = int64_t(np) * np;
     g.n = g_exact_n > 0 ? g_exact_n : np;
+    g.sel = sc.sel;
+    g.scale_c = sc.c;
+    g.scale_in0 = sc.in0;
+    if ((sc.c || sc.in0) && g_exact_n > 0) return MEXP_ERR_UNSUPPORTED;  // DMMA pass only
     if (g_exact_n > 0) {  // REFERENCE rounding: the k-ordered DMUL+DADD product
         for (int z0 = 0; z0 < count; z0 += 65535) {
             const int zc = std::min(count - z0, 65535);
@@ -967,7 +991,17 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     auto L = [&](size_t off) { return d_lists + off; };
     const dim3 ew_block(256);
     const unsigned ew_rows = unsigned(std::min(np, 64));
-    if (!all_ok.empty()) {
+    // Prep-free (TaylorNew, unpadded, DMMA pass): the products read the
+    // caller's unscaled A and scale exactly by powers of two instead of going
+    // through a scaled copy -- A2 = 4^-s (A A), A3 = 2^-s (A2 A), and T18's B
+    // epilogue reads A times 2^-s; every other degree has s = 0. (A 2 GB
+    // read + write less for cfg4.) s <= 400 keeps 4^-s normal.
+    const bool noprep = !pade && (acc_arg >> 4) == MEXP_FAMILY_TAYLOR_NEW && n == np && g_exact_n == 0 &&
+                        max_s <= 400 && std::getenv("MEXP_LARGE_PREP") == nullptr;
+    const double* A0 = noprep ? d_a : W[0];
+    const Scaling sc_a2{d_sel, noprep ? 2 : 0, 0}, sc_a3{d_sel, noprep ? 1 : 0, 0},
+        sc_b{d_sel, 0, noprep ? 1 : 0};
+    if (!all_ok.empty() && !noprep) {
         sliced(int64_t(all_ok.size()), [&](int64_t y0, unsigned ny) {
             prep_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(d_a, W[0], n, np, L(off_all2) + y0, d_sel);
         });
@@ -1085,11 +1119,15 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     } else {
     if (int c = int(by_deg[18].size())) {  // T18 (taylor_schemes.cpp:127-141)
         const int32_t* l = L(off_deg[18]);
-        if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
-        if ((r = gemm<EPI_STORE>(W[1], W[0], {}, {W[2]}, l, c, np, st, launches))) return r;  // A3
+        if ((r = gemm<EPI_STORE>(A0, A0, {}, {W[1]}, l, c, np, st, launches, nullptr, nullptr, 0,
+                                 sc_a2)))
+            return r;  // A2
+        if ((r = gemm<EPI_STORE>(W[1], A0, {}, {W[2]}, l, c, np, st, launches, nullptr, nullptr, 0,
+                                 sc_a3)))
+            return r;  // A3
         // A6 = A3*A3 -> B1 W0, B2 W1, B3 W3, B4 W4, B5 W5 (A, A2 read in place)
-        if ((r = gemm<EPI_T18_B>(W[2], W[2], {W[0], W[1], W[2]}, {W[0], W[1], W[3], W[4], W[5]}, l,
-                                 c, np, st, launches)))
+        if ((r = gemm<EPI_T18_B>(W[2], W[2], {A0, W[1], W[2]}, {W[0], W[1], W[3], W[4], W[5]}, l, c, np,
+                                 st, launches, nullptr, nullptr, 0, sc_b)))
             return r;
         // B1*B5: A9 = . + B4 -> W4, L = B3 + A9 -> W3
         if ((r = gemm<EPI_AL>(W[0], W[5], {W[4], W[3]}, {W[4], W[3]}, l, c, np, st, launches)))
@@ -1099,9 +1137,9 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     }
     if (int c = int(by_deg[12].size())) {  // T12 (taylor_schemes.cpp:115-125)
         const int32_t* l = L(off_deg[12]);
-        if ((r = gemm<EPI_STORE>(W[0], W[0], {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
+        if ((r = gemm<EPI_STORE>(A0, A0, {}, {W[1]}, l, c, np, st, launches))) return r;  // A2
         // A3 = A2*A -> B1 W2, B2 W3, B3 W4, B4 W5
-        if ((r = gemm<EPI_T12_B>(W[1], W[0], {W[0], W[1]}, {W[2], W[3], W[4], W[5]}, l, c, np, st,
+        if ((r = gemm<EPI_T12_B>(W[1], A0, {A0, W[1]}, {W[2], W[3], W[4], W[5]}, l, c, np, st,
                                  launches)))
             return r;
         // B4*B4: A6 = . + B3 -> W4, L = B2 + A6 -> W3
@@ -1113,12 +1151,12 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     if (int c = int(by_deg[8].size())) {  // T8 (taylor_schemes.cpp:104-113)
         const int32_t* l = L(off_deg[8]);
         // A2 -> W1, U = x1 A + x2 A2 -> W2
-        if ((r = gemm<EPI_T8_1>(W[0], W[0], {W[0]}, {W[1], W[2]}, l, c, np, st, launches))) return r;
+        if ((r = gemm<EPI_T8_1>(A0, A0, {A0}, {W[1], W[2]}, l, c, np, st, launches))) return r;
         // A4 = A2*U: V1 -> W3, V2 -> W4
-        if ((r = gemm<EPI_T8_2>(W[1], W[2], {W[0], W[1]}, {W[3], W[4]}, l, c, np, st, launches)))
+        if ((r = gemm<EPI_T8_2>(W[1], W[2], {A0, W[1]}, {W[3], W[4]}, l, c, np, st, launches)))
             return r;
         // A8 = V1*V2 -> T (A2 read in place)
-        if ((r = final_step(ET8_3{}, W[3], W[4], {W[0], W[1]}, 8))) return r;
+        if ((r = final_step(ET8_3{}, W[3], W[4], {A0, W[1]}, 8))) return r;
     }
     // Family::TaylorPS degrees 6, 9, 16 (eval_ps, taylor_schemes.cpp:167-198):
     // p = 3 (6, 9) or 4 (16) powers, then the Horner chain
@@ -1169,25 +1207,25 @@ int large_expm_f64(const double* d_a, double* d_out, mexp_selection* d_sel_user,
     if (int c = int(by_deg[4].size())) {  // eval_ps(4) (taylor_schemes.cpp:158-165)
         const int32_t* l = L(off_deg[4]);
         // A2 -> W3, inner -> W2
-        if ((r = gemm<EPI_T4_1>(W[0], W[0], {W[0]}, {W[3], W[2]}, l, c, np, st, launches))) return r;
+        if ((r = gemm<EPI_T4_1>(A0, A0, {A0}, {W[3], W[2]}, l, c, np, st, launches))) return r;
         // T = (I + A) + inner*A2
-        if ((r = final_step(ET4_2{}, W[2], W[3], {W[0]}, 4))) return r;
+        if ((r = final_step(ET4_2{}, W[2], W[3], {A0}, 4))) return r;
     }
     if (by_deg[2].size()) {  // eval_ps(2)
-        if ((r = final_step(ET2{}, W[0], W[0], {W[0]}, 2))) return r;
+        if ((r = final_step(ET2{}, A0, A0, {A0}, 2))) return r;
     }
     {  // degree 1: I + A
         const auto& pp = deg_parts[1];
         if (pp.first.count) {
             sliced(pp.first.count, [&](int64_t y0, unsigned ny) {
-                t1_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(W[0], d_out, n, np, n,
+                t1_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(A0, d_out, n, np, n,
                                                                   L(pp.first.off) + y0);
             });
             launches->fetch_add(1, std::memory_order_relaxed);
         }
         if (pp.second.count) {
             sliced(pp.second.count, [&](int64_t y0, unsigned ny) {
-                t1_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(W[0], R, np, np, np,
+                t1_kernel<<<dim3(ew_rows, ny), ew_block, 0, st>>>(A0, R, np, np, np,
                                                                   L(pp.second.off) + y0);
             });
             launches->fetch_add(1, std::memory_order_relaxed);

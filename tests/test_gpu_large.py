@@ -260,3 +260,23 @@ def test_large_n_host_pipeline_many_chunks(cuda):
     r = subprocess.run([sys.executable, "-c", _CHUNKED_SCRIPT, root], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "chunked ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("rounding", [mx.ROUND_FAST, mx.ROUND_AUTO])
+def test_prep_free_path_bitwise(cuda, rounding, monkeypatch):
+    """Unpadded TaylorNew batches skip the scaled copy of A: the products read
+    the caller's A and scale by exact powers of two (A2 = 4^-s AA, A3 = 2^-s
+    A2 A, T18's B epilogue reads 2^-s A). Same bits as the scaled-copy path
+    (MEXP_LARGE_PREP=1) across every degree and s up to ~6."""
+    rng = np.random.default_rng(11)
+    n, b = 128, 12
+    a = rng.standard_normal((b, n, n)) / np.sqrt(n)
+    norms = np.array([1e-5, 3e-3, 0.03, 0.2, 0.6, 1.0, 2.0, 5.0, 12.0, 30.0, 60.0, 0.9])
+    a *= (norms / workloads.one_norm_batched(a))[:, None, None]
+    out0, sel0, st0 = mx.expm_batched_host(a, rounding=rounding)
+    monkeypatch.setenv("MEXP_LARGE_PREP", "1")
+    out1, sel1, st1 = mx.expm_batched_host(a, rounding=rounding)
+    assert st0 == st1 == mx.OK
+    assert set(sel0["degree"].tolist()) >= {4, 8, 12, 18} and sel0["s"].max() >= 5
+    assert np.array_equal(sel0.view(np.uint8), sel1.view(np.uint8))
+    assert np.array_equal(out0.view(np.uint64), out1.view(np.uint64))
