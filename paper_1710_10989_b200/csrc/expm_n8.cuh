@@ -75,10 +75,16 @@ struct Group8T {
         fscale = 1.0;
     }
 
+    // The diagonal test goes through an opaque (volatile) move, re-evaluated
+    // per matrix: otherwise the compiler hoists every identity term
+    // (diag ? c : 0, one per scheme coefficient) out of the batch loop as
+    // loop-invariant values, keeps them in ~30 registers and spills them.
     __device__ __forceinline__ Frag ident() const {
+        int d;
+        asm volatile("sub.s32 %0, %1, %2;" : "=r"(d) : "r"(r), "r"(2 * q));
         Frag f;
-        f.v[0] = (r == 2 * q) ? 1.0 : 0.0;
-        f.v[1] = (r == 2 * q + 1) ? 1.0 : 0.0;
+        f.v[0] = d == 0 ? 1.0 : 0.0;
+        f.v[1] = d == 1 ? 1.0 : 0.0;
         return f;
     }
 

@@ -10,6 +10,7 @@
 #   tools/gpu.sh ncu CFG [ROUND]       ncu --set full of the config's top kernel
 #   tools/gpu.sh sanitize              compute-sanitizer memcheck/racecheck/synccheck/initcheck
 #   tools/gpu.sh e2e                   e2e variants of the host pipeline (cfg2, cfg3)
+#   tools/gpu.sh envbench CFG R ENV..  one bench line per environment string (knob A/B)
 #
 # Everything lands in gpurun_out/ (scratch); summaries worth keeping are
 # copied to profiles/ by hand.
@@ -57,6 +58,14 @@ evidence)
     for c in cfg2 cfg3 cfg4 cfg5; do "$0" ncu $c; done
     "$0" ncu cfg2 fast
     "$0" ncu cfg2 reference ;;
+envbench)  # envbench CFG ROUNDING "VAR=x VAR2=y" ... : one bench line per environment
+    cfg=$2; r=$3; shift 3
+    for e in "$@"; do
+        tag=$(echo "$e" | tr ' =' '_-')
+        env $e timeout 600 python bench.py --config $cfg --rounding $r --no-cpu-baseline --e2e-steps 1 \
+            > $out/envbench_${cfg}_${r}_$tag.log 2>&1
+        echo -n "[$e] "; line $out/envbench_${cfg}_${r}_$tag.log
+    done ;;
 launches)
     cfg=${2:-cfg2}
     python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $out/plain_$cfg.log 2>&1 && \
