@@ -7,6 +7,7 @@
 // never -0). n > 64 runs the DMMA GEMM engine (expm_large.cu).
 #include <atomic>
 #include <chrono>
+#include <climits>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -206,7 +207,10 @@ int n8_variant() {
     static int v = [] {
         const char* e = std::getenv("MEXP_N8_VARIANT");
         // measured (profiles/cfg2_variants_r1.txt): chained DMMAs with the
-        // reference-rounded matrices inline is fastest for AUTO
+        // reference-rounded matrices inline is fastest for AUTO. 12 / 15: the
+        // pipelined kernel (expm8_pipe_kernel) with the dynamic ticket / static
+        // rounds -- fewer instructions and no exposed load latency, but the
+        // same time (profiles/cfg2_variants_r2.txt), so 0 stays the default
         return e ? std::atoi(e) : 0;
     }();
     return v;
@@ -345,6 +349,41 @@ int launch_pade8(const double* a, double* out, mexp_selection* sel, int64_t batc
     return MEXP_OK;
 }
 
+// The pipelined 8x8 kernel (expm_n8.cuh expm8_pipe_kernel): the default for
+// the Taylor families. kClaimAt / kPF: the matrix of a round before which the
+// next round is claimed / its copy issued.
+template <int kFamily, int kClaimAt, int kPF>
+int launch_n8_pipe(const double* a, double* out, mexp_selection* sel, int64_t batch, int accuracy,
+                   int rounding, int smin, cudaStream_t st) {
+    auto kern = expm8_pipe_kernel<kFamily, kClaimAt, kPF>;
+    static int blocks_per_sm = [&] {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * kN8WarpsPerBlock, 0);
+        return b > 0 ? b : 1;
+    }();
+    const int64_t cap = int64_t(blocks_per_sm) * num_sms();
+    const int64_t want = (batch + 4 * kN8WarpsPerBlock - 1) / (4 * kN8WarpsPerBlock);
+    const int grid = int(want < cap ? want : cap);
+    unsigned long long* ticket = nullptr;
+    {
+        int r = next_ticket(st, &ticket);
+        if (r != MEXP_OK) return r;
+    }
+    N8Params prm;
+    for (int e = 0; e < 6; ++e) prm.theta[e] = theta_entry(kFamily, accuracy & 15, e);
+    prm.accuracy = accuracy & 15;
+    prm.exact_from_s = rounding == MEXP_ROUND_REFERENCE ? 0
+                       : rounding == MEXP_ROUND_AUTO    ? smin
+                                                        : INT_MAX;
+    kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, prm, ticket);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    MEXP_CUDA(cudaGetLastError());
+    return MEXP_OK;
+}
+
+// the pipelined kernel keeps its round index in 32 bits and has no fast tail
+bool n8_pipe_ok(int64_t batch) { return batch < (int64_t(1) << 33) && fast_tail() == 0; }
+
 int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
                   int accuracy, int rounding, int smin, cudaStream_t st) {
     if (batch == 0) return MEXP_OK;
@@ -355,10 +394,17 @@ int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t bat
                                                            smin, st);
         return launch_pade8(a, out, sel, batch, accuracy, rounding, smin, st);
     }
-    if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS)  // the default variant only
+    const int variant = n8_pipe_ok(batch) ? n8_variant() : 0;
+    if ((accuracy >> 4) == MEXP_FAMILY_TAYLOR_PS) {  // the default variants only
+        if (variant == 12)
+            return launch_n8_pipe<MEXP_FAMILY_TAYLOR_PS, 1, 3>(a, out, sel, batch, accuracy, rounding,
+                                                               smin, st);
         return launch_n8_variant<false, 0, 8, MEXP_FAMILY_TAYLOR_PS>(a, out, sel, batch, accuracy,
                                                                      rounding, smin, st);
-    switch (n8_variant()) {
+    }
+    switch (variant) {
+        case 12: return launch_n8_pipe<MEXP_FAMILY_TAYLOR_NEW, 1, 3>(a, out, sel, batch, accuracy, rounding, smin, st);
+        case 15: return launch_n8_pipe<MEXP_FAMILY_TAYLOR_NEW, -1, 3>(a, out, sel, batch, accuracy, rounding, smin, st);
         case 0: return launch_n8_variant<false, 0>(a, out, sel, batch, accuracy, rounding, smin, st);
         case 1: return launch_n8_variant<true, 0>(a, out, sel, batch, accuracy, rounding, smin, st);
         case 2: return launch_n8_variant<false, 1>(a, out, sel, batch, accuracy, rounding, smin, st);

@@ -39,7 +39,9 @@ __host__ __device__ __forceinline__ constexpr uint32_t unit8(int i, int c) {
            << 4;
 }
 
-template <bool kSplit>
+// kSharedY: the reference-rounded product's Y operand goes through a warp-wide
+// scratch tile (ytile) instead of the second half of the matrix's own 1 KB tile.
+template <bool kSplit, bool kSharedY = false>
 struct Group8T {
     struct S {
         static constexpr int STASH = 0;
@@ -52,6 +54,8 @@ struct Group8T {
     };
 
     char* tile;      // this warp's tiles: [0, 512) X / fast, [512, 1024) Y (exact)
+    char* ytile;     // kSharedY: the Y (exact) scratch tile
+    __device__ __forceinline__ char* ybase() const { return kSharedY ? ytile : tile + 512; }
     uint32_t st;     // unit (r, q)
     uint32_t ld0;    // element (2q,   r)
     uint32_t ld1;    // element (2q+1, r)
@@ -59,6 +63,7 @@ struct Group8T {
     uint32_t qx;     // q << 4: unit (k, q) = unit8(k, 0) ^ qx
     int r, q;
     double fscale;   // 2^-s, applied to the staged (unscaled) A by sq_first
+    bool scaled;     // s > 0
     // the scaled A's transposed DMMA operand, kept from sq_first for A3 = A2 A
     static constexpr bool kKeepsAT = true;
     mutable double bt0, bt1;
@@ -73,6 +78,7 @@ struct Group8T {
         rowb = unit8(r, 0);
         qx = uint32_t(q) << 4;
         fscale = 1.0;
+        scaled = true;
     }
 
     // The diagonal test goes through an opaque (volatile) move, re-evaluated
@@ -112,8 +118,12 @@ struct Group8T {
         if constexpr (Ops::kExact) {
             return mm_impl<Ops>(A, A, true, nullptr);
         } else {
-            const double y0 = fscale * *reinterpret_cast<const double*>(tile + ld0);
-            const double y1 = fscale * *reinterpret_cast<const double*>(tile + ld1);
+            double y0 = *reinterpret_cast<const double*>(tile + ld0);
+            double y1 = *reinterpret_cast<const double*>(tile + ld1);
+            if (scaled) {  // s > 0 (predicated: no FP64-pipe slot when s = 0)
+                y0 *= fscale;
+                y1 *= fscale;
+            }
             bt0 = y0;
             bt1 = y1;
             Frag C;
@@ -154,9 +164,9 @@ struct Group8T {
         __syncwarp();  // readers of the previous product are done with the tile
         if constexpr (Ops::kExact) {
             *reinterpret_cast<double2*>(tile + st) = make_double2(X.v[0], X.v[1]);
-            if (!same) *reinterpret_cast<double2*>(tile + 512 + st) = make_double2(Y.v[0], Y.v[1]);
+            if (!same) *reinterpret_cast<double2*>(ybase() + st) = make_double2(Y.v[0], Y.v[1]);
             __syncwarp();
-            const char* ty = same ? tile : tile + 512;
+            const char* ty = same ? tile : ybase();
             double c0 = 0.0, c1 = 0.0;
             // row r of X in two halves (k ascending): 8 registers live, not 16
 #pragma unroll
@@ -335,6 +345,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
                 const bool exact = rounding == MEXP_ROUND_REFERENCE ||
                                    (rounding == MEXP_ROUND_AUTO && s >= exact_s_min);
                 g.fscale = pow2_neg(s);
+                g.scaled = s > 0;
                 if constexpr (kDefer) {
                     if (exact) {
                         if (lane == 0) worklist[atomicAdd(wcount, 1)] = int32_t(m);
@@ -419,10 +430,237 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
             X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
         } else {
             g.fscale = pow2_neg(sl.s);
+            g.scaled = sl.s > 0;
             X = run_expm<ExactOps, family>(g, A, sl.degree, sl.s, 0);
         }
         st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
     }
+}
+
+// ---------------------------------------------------------------------------
+// The pipelined 8x8 kernel (default for TaylorNew / TaylorPS): the same round
+// structure and the same arithmetic as expm8_f64_kernel (bit-identical
+// results), with the global-memory and work-ticket latencies taken off the
+// warps' critical path:
+//   * A round's four matrices arrive by cp.async straight into their swizzled
+//     staging tiles (two alternating sets per warp), issued while the previous
+//     round is still computing; the prologue never waits on DRAM.
+//   * The next round is claimed (atomicAdd on the work ticket) before matrix
+//     kClaimAt of the current round and its copy is issued before matrix kPF,
+//     so neither the L2 atomic round trip nor the DRAM latency stalls a warp.
+//   * all_finite rides on the 1-norm: a column sum of |a_ij| is Inf/NaN iff
+//     the column holds a non-finite entry or the sum overflows, so the per-
+//     entry test (and the two error statuses it separates) runs only for a
+//     round whose norm is non-finite.
+//   * theta_m come in as kernel parameters (constant-bank operands), the
+//     2^-s scale and the rounding decision are made once per round in the
+//     4-wide prologue and handed to the per-matrix loop by shuffle.
+// ---------------------------------------------------------------------------
+struct N8Params {
+    double theta[6];   // theta_entry(family, accuracy, 0..5)
+    int accuracy;      // mexp_accuracy (the rare non-finite path's select_device)
+    int exact_from_s;  // matrices with s >= this run reference rounding
+                       // (0: all, REFERENCE; INT_MAX: none, FAST)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// scaled(a, 2^-s), the scheme, the squarings (run_expm without its own 2^-s:
+// g.fscale holds it)
+template <class Ops, int kFam, class G>
+__device__ __forceinline__ typename G::Frag run_expm8(const G& g, typename G::Frag A, int degree,
+                                                      int s) {
+    using F = typename G::Frag;
+    if (s > 0) {
+        A.v[0] = __dmul_rn(g.fscale, A.v[0]);
+        A.v[1] = __dmul_rn(g.fscale, A.v[1]);
+    }
+    F X;
+    if constexpr (kFam == MEXP_FAMILY_TAYLOR_PS)
+        X = eval_taylor_ps<Ops>(g, degree, A);
+    else
+        X = eval_taylor_new<Ops>(g, degree, A);
+    for (int i = 0; i < s; ++i) X = g.template mm<Ops>(X, X, true);
+    return X;
+}
+
+constexpr int kN8InfoBad = 1 << 30;   // status != MEXP_OK: the result is NaN
+constexpr int kN8InfoSkip = 1 << 29;  // past the end of the batch
+
+template <int kFamily = MEXP_FAMILY_TAYLOR_NEW, int kClaimAt = 1, int kPF = 3>
+__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
+    expm8_pipe_kernel(const double* __restrict__ a, double* __restrict__ out,
+                      mexp_selection* __restrict__ sel, int64_t batch, const N8Params prm,
+                      unsigned long long* __restrict__ ticket) {
+    // kClaimAt < 0: static round-robin rounds (no work ticket; experiments)
+    static_assert(kClaimAt < kPF && kPF < kN8Mpw, "claim before the copy, inside the round");
+    using Group8 = Group8T<false, true>;
+    using F = typename Group8::Frag;
+    // per warp: two sets of four 512-byte staging tiles + the exact path's Y scratch
+    __shared__ __align__(16) char tiles[kN8WarpsPerBlock][2][kN8Mpw][512];
+    __shared__ __align__(16) char yscratch[kN8WarpsPerBlock][512];
+    __shared__ int infos[kN8WarpsPerBlock][kN8Mpw];
+    constexpr int family = kFamily;
+    constexpr bool ps = kFamily == MEXP_FAMILY_TAYLOR_PS;
+    constexpr uint32_t kSet = kN8Mpw * 512;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    Group8 g;
+    g.init(tiles[wib][0][0], lane);
+    g.ytile = yscratch[wib];
+    char* const wbase = tiles[wib][0][0];
+    const uint32_t wbase_s = smem_u32(wbase);
+
+    // 1-norm column reads of lane l: matrix jm = l >> 3, column c8 = l & 7
+    const int jm = lane >> 3, c8 = lane & 7, cp = c8 >> 1;
+    const uint32_t half = uint32_t(c8 & 1) << 3;
+    const uint32_t n0 = jm * 512 + ((((cp >> 1)) << 5) | ((cp & 1) << 4)) + half;
+    const uint32_t n1 = jm * 512 + (((1 ^ (cp >> 1)) << 5) | ((cp & 1) << 4)) + half;
+
+    const uint32_t rounds = uint32_t((batch + kN8Mpw - 1) / kN8Mpw);  // < 2^32: checked by the host
+    const uint32_t rstride = gridDim.x * kN8WarpsPerBlock;
+    uint32_t rd = blockIdx.x * kN8WarpsPerBlock + wib;
+    uint32_t cur = 0;  // byte offset of the current set
+
+    auto copy_round = [&](uint32_t r, uint32_t setoff) {
+        const int64_t mb = int64_t(r) * kN8Mpw;
+        const double* src = a + mb * 64 + lane * 2;
+        const uint32_t dst = wbase_s + setoff + g.st;
+        if (mb + kN8Mpw <= batch) {
+#pragma unroll
+            for (int j = 0; j < kN8Mpw; ++j) cp_async16(dst + j * 512, src + j * 64);
+        } else {  // the last, partial round: zero-filled tiles past the batch
+#pragma unroll
+            for (int j = 0; j < kN8Mpw; ++j) {
+                const bool ok = mb + j < batch;
+                cp_async16_zfill(dst + j * 512, ok ? src + j * 64 : a, ok ? 16u : 0u);
+            }
+        }
+    };
+    if (rd < rounds) copy_round(rd, 0);
+
+    while (rd < rounds) {
+        const int64_t m0 = int64_t(rd) * kN8Mpw;
+        cp_async_wait_all();
+        __syncwarp();
+        char* const set = wbase + cur;
+
+        // exact 1-norm (kernels.cpp:44-53): column sum over rows 0..7 in order
+        double colsum = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const char* p = set + (((i >> 1) & 1) ? n1 : n0) + (unit8(i, 0) & ~0x20u);
+            colsum = __dadd_rn(colsum, fabs(*reinterpret_cast<const double*>(p)));
+        }
+        // max over the 8 columns: non-negative doubles order like their bits,
+        // and a NaN or Inf sum orders above every finite one
+        unsigned long long nb = __double_as_longlong(colsum) & 0x7fffffffffffffffull;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const unsigned long long w = __shfl_xor_sync(0xffffffffu, nb, o);
+            nb = w > nb ? w : nb;
+        }
+        const double norm = __longlong_as_double(nb);
+        int degree = 0, s = 0, status = MEXP_OK;
+        bool allfin = true;
+        if (__any_sync(0xffffffffu, uint32_t(nb >> 32) >= 0x7ff00000u)) {
+            // a non-finite entry (dense_matrix.cpp:54-58) or an overflowing
+            // norm somewhere in the round: the per-entry test decides
+            uint32_t finbits = 0;
+#pragma unroll
+            for (int j = 0; j < kN8Mpw; ++j) {
+                const double2 v = *reinterpret_cast<const double2*>(set + j * 512 + g.st);
+                if (__all_sync(0xffffffffu, isfinite(v.x) && isfinite(v.y))) finbits |= 1u << j;
+            }
+            allfin = (finbits >> jm) & 1u;
+            if (!allfin) {
+                status = MEXP_ERR_NONFINITE;
+            } else {
+                // the norm of matrix jm alone (its own columns' max is what nb holds)
+                const Sel sl = select_device(norm, prm.accuracy, family);
+                degree = sl.degree;
+                s = sl.s;
+                status = sl.status;
+            }
+        } else if (norm <= prm.theta[5]) {
+            // select_device's table walk with the thetas from the parameters
+            const int e = int(prm.theta[0] < norm) + int(prm.theta[1] < norm) +
+                          int(prm.theta[2] < norm) + int(prm.theta[3] < norm) +
+                          int(prm.theta[4] < norm);
+            degree = ps ? ps_degree_of(e) : (e < 4 ? (1 << e) : (e == 4 ? 12 : 18));
+        } else {
+            const long long tb = __double_as_longlong(prm.theta[5]);
+            const int k = int(nb >> 52) - int(tb >> 52);
+            const double t = __longlong_as_double(tb + (static_cast<long long>(k) << 52));
+            degree = ps ? 16 : 18;
+            s = k + int(norm > t);
+        }
+        if (sel && c8 == 0 && m0 + jm < batch) {
+            mexp_selection rec;
+            rec.norm_in = allfin ? norm : __longlong_as_double(0x7ff8000000000000ll);
+            rec.degree = int16_t(degree);
+            rec.s = int16_t(s);
+            rec.status = status;
+            sel[m0 + jm] = rec;
+        }
+        // (degree, s, flags) per matrix through shared memory: the per-matrix
+        // loop reads them back by broadcast, no register lives across it
+        if (c8 == 0)
+            infos[wib][jm] = degree | (s << 5) | (status != MEXP_OK ? kN8InfoBad : 0) |
+                             (m0 + jm >= batch ? kN8InfoSkip : 0) |
+                             (s >= prm.exact_from_s ? int(0x80000000u) : 0);
+        __syncwarp();
+
+        uint32_t t = 0, nrd = 0;
+#pragma unroll 1
+        for (int j = 0; j < kN8Mpw; ++j) {
+            // plain atom (inline asm): the compiler's warp-aggregated form
+            // shuffles the result at once and would wait for the round trip here
+            if (j == kClaimAt && lane == 0)
+                asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(ticket) : "memory");
+            if (j == kPF) {
+                nrd = kClaimAt < 0 ? rd + rstride : rstride + __shfl_sync(0xffffffffu, t, 0);
+                if (nrd < rounds) copy_round(nrd, cur ^ kSet);
+            }
+            const int inf = infos[wib][j];
+            if (inf & kN8InfoSkip) continue;
+            g.tile = set + j * 512;
+            const double2 v = *reinterpret_cast<const double2*>(g.tile + g.st);
+            F A;
+            A.v[0] = v.x;
+            A.v[1] = v.y;
+            F X;
+            if (inf & kN8InfoBad) {
+                X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
+            } else {
+                const int deg = inf & 31, sj = (inf >> 5) & 0x7fff;
+                // 2^-s from its high word (the low word is 0: s <= 1025 for any finite norm)
+                g.fscale = __hiloint2double(
+                    int(sj <= 1022 ? uint32_t(1023 - sj) << 20 : 1u << ((1042 - sj) & 31)), 0);
+                g.scaled = sj > 0;
+                if (inf < 0)
+                    X = run_expm8<ExactOps, family>(g, A, deg, sj);
+                else
+                    X = run_expm8<FastOps, family>(g, A, deg, sj);
+            }
+            st_stream(reinterpret_cast<double2*>(out + (m0 + j) * 64) + lane, make_double2(X.v[0], X.v[1]));
+        }
+        rd = nrd;
+        cur ^= kSet;
+    }
+    release_ticket(ticket);
 }
 
 }  // namespace mexp_b200

@@ -311,6 +311,19 @@ __device__ typename G::Frag eval_taylor_new(const G& g, int degree, const typena
         case 8: {  // eval_t8, 3 products
             const F A2 = g.template sq_first<Ops>(A);
             const F A4 = g.template mm<Ops>(A2, lc<Ops>(T8C::x1, A, T8C::x2, A2), false);
+            if constexpr (!Ops::kExact && std::is_same<typename F::T, double>::value) {
+                // fast rounding (fp64 fragments; the fp32 kernels keep the
+                // order the pair kernel mirrors): x3*A2 + A4 as one FMA per element, and the
+                // final y-combination seeds the last product's accumulator
+                // (4 of the scheme's 20 FP64 instructions per lane less)
+                static_assert(T8C::y0 == 1.0 && T8C::y1 == 1.0, "eval_t8 tail");
+                F L;
+#pragma unroll
+                for (int e = 0; e < F::kCount; ++e) L.v[e] = Ops::mac(A4.v[e], T8C::x3, A2.v[e]);
+                return g.template mm_add<Ops>(
+                    L, lc<Ops, true>(T8C::x4, I, T8C::x5, A, T8C::x6, A2, T8C::x7, A4), false,
+                    lc<Ops, true>(T8C::y0, I, T8C::y1, A, T8C::y2, A2));
+            }
             const F A8 = g.template mm<Ops>(
                 lc<Ops>(T8C::x3, A2, 1.0, A4),
                 lc<Ops, true>(T8C::x4, I, T8C::x5, A, T8C::x6, A2, T8C::x7, A4), false);

@@ -75,7 +75,7 @@ launches)
     echo "launches_$cfg.csv: $(grep -c gpu__time_duration $out/launches_$cfg.csv) rows" ;;
 ncu)
     cfg=${2:-cfg2}; r=${3:-auto}
-    case $cfg in cfg1) k=regex:cluster;; cfg2) k=regex:expm8_f64;; cfg3) k=regex:expm32_pairs;;
+    case $cfg in cfg1) k=regex:cluster;; cfg2) k=regex:expm8_;; cfg3) k=regex:expm32_pairs;;
                  *) k=regex:gemm_dmma;; esac
     python tools/profile_kernel.py $cfg $r 2 > $out/prof_plain_$cfg.log 2>&1 && \
     timeout 900 ncu --set full --import-source on --clock-control none -k $k -s 1 -c 1 \
