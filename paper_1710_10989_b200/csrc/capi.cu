@@ -185,20 +185,11 @@ int next_ticket(cudaStream_t st, unsigned long long** out) {
     return MEXP_OK;
 }
 
-// Squarings at the end of a reference-rounded (AUTO) matrix that may use fast
-// rounding; MEXP_FAST_TAIL overrides. 0: on cfg2's U(-1,1) matrices k <= 3
-// stays inside 50*8*u (profiles/cfg2_fast_tail_r1.txt), but a nearly
-// idempotent X (the gallery's rank-one kind, ||X||^2 >> ||X^2||) amplifies a
-// fast squaring's rounding past the band (k = 2: 2.3x at s = 14,
-// tests/test_gpu_auto_stress.py), so AUTO keeps the reference's rounding to
-// the end: those matrices are bit-identical to the reference.
-int fast_tail() {
-    static int v = [] {
-        const char* e = std::getenv("MEXP_FAST_TAIL");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
+// AUTO keeps the reference's rounding to the last squaring of its
+// reference-rounded matrices: a fast-rounded tail was measured (round 1:
+// profiles/cfg2_fast_tail_r1.txt) and then found to leave the 50*n*u band on
+// nearly idempotent X (the gallery's rank-one kind, 2.3x at s = 14,
+// tests/test_gpu_auto_stress.py), so the knob is gone.
 
 // 8x8 variant (experiments; default chosen from the measurements in
 // profiles/): bit 0 = split DMMA accumulation, bit 1 = defer reference-rounded
@@ -206,12 +197,11 @@ int fast_tail() {
 int n8_variant() {
     static int v = [] {
         const char* e = std::getenv("MEXP_N8_VARIANT");
-        // measured (profiles/cfg2_variants_r1.txt): chained DMMAs with the
-        // reference-rounded matrices inline is fastest for AUTO. 12 / 15: the
-        // pipelined kernel (expm8_pipe_kernel) with the dynamic ticket / static
-        // rounds -- fewer instructions and no exposed load latency, but the
-        // same time (profiles/cfg2_variants_r2.txt), so 0 stays the default
-        return e ? std::atoi(e) : 0;
+        // 12 (default): the pipelined kernel (expm8_pipe_kernel); 15: the same with
+        // static rounds. 0: the round-1/2 kernel (expm8_f64_kernel) with chained
+        // DMMAs and the reference-rounded matrices inline; 1, 2, 4, 5: its split /
+        // deferred / lower-occupancy variants (profiles/cfg2_variants_r1.txt, _r2.txt)
+        return e ? std::atoi(e) : 12;
     }();
     return v;
 }
@@ -260,9 +250,7 @@ int launch_n8_variant(const double* a, double* out, mexp_selection* sel, int64_t
         int r = next_ticket(st, &ticket);
         if (r != MEXP_OK) return r;
     }
-    // AUTO: the last fast_tail() squarings of the reference-rounded matrices
-    // run with FMA/DMMA rounding (expm_small.cuh run_expm)
-    const int rounding_arg = rounding == MEXP_ROUND_AUTO ? (rounding | (fast_tail() << 8)) : rounding;
+    const int rounding_arg = rounding;
     kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, accuracy, rounding_arg, smin,
                                                  work, defer ? work + batch : nullptr, ticket);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -381,8 +369,8 @@ int launch_n8_pipe(const double* a, double* out, mexp_selection* sel, int64_t ba
     return MEXP_OK;
 }
 
-// the pipelined kernel keeps its round index in 32 bits and has no fast tail
-bool n8_pipe_ok(int64_t batch) { return batch < (int64_t(1) << 33) && fast_tail() == 0; }
+// the pipelined kernel keeps its round index in 32 bits
+bool n8_pipe_ok(int64_t batch) { return batch < (int64_t(1) << 33); }
 
 int launch_n8_f64(const double* a, double* out, mexp_selection* sel, int64_t batch,
                   int accuracy, int rounding, int smin, cudaStream_t st) {

@@ -53,8 +53,13 @@ constexpr int kBufFloats = NN + N;           // a 32x32 operand buffer + one pad
 #define MEXP_PAIRS_PREFETCH 1
 #endif
 constexpr bool kPrefetch = MEXP_PAIRS_PREFETCH;
-// X, Y, and the next pair's matrix (prefetch)
-constexpr int kHalfFloats = 2 * kBufFloats + (kPrefetch ? NN : 0);
+// X, Y, and the next pair's matrix (prefetch), plus 64 bytes: the second
+// half's buffers sit half a bank row from the first half's, so the X loads of
+// the two halves (one LDS.64 wavefront for the warp) hit different banks
+#ifndef MEXP_PAIRS_SKEW
+#define MEXP_PAIRS_SKEW 16
+#endif
+constexpr int kHalfFloats = 2 * kBufFloats + (kPrefetch ? NN : 0) + MEXP_PAIRS_SKEW;
 constexpr int kSmemBytes = kWarps * 2 * kHalfFloats * 4 + 16;
 static_assert(kCtasPerSm * kSmemBytes <= 227 * 1024, "smem");
 static_assert(kCtasPerSm * kTmemCols <= 512, "tmem");
@@ -649,7 +654,7 @@ __device__ __forceinline__ int4 pair_at(const int2* __restrict__ list, int64_t q
 
 __global__ void __launch_bounds__(32 * kWarps, kCtasPerSm)
     expm32_pairs_kernel(const float* __restrict__ a, float* __restrict__ out,
-                        const int2* __restrict__ list, int64_t batch) {
+                        const int2* __restrict__ list, int64_t batch, int quad_lanes) {
     extern __shared__ __align__(16) float smem[];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kWarps * 2 * kHalfFloats);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -667,8 +672,16 @@ __global__ void __launch_bounds__(32 * kWarps, kCtasPerSm)
 
     const int h = lane >> 4, hl = lane & 15;
     Lane L;
-    L.ti = hl >> 2;
-    L.tj = hl & 3;
+    // An aligned quad of lanes owns a 2x2 block of tiles. The shared-memory
+    // pipe merges identical addresses only inside an aligned lane quad and
+    // serves 16 (quad, address) requests per 64-bit wavefront, 8 per 128-bit
+    // one (tools/lds_patterns.cu): with two ti and two tj per quad an X load
+    // (address by ti, LDS.64) is 1 wavefront and a Y load (address by tj,
+    // LDS.128) 2, against 1-2 and 4 with (ti, tj) = (hl >> 2, hl & 3) --
+    // 16 instead of 24-32 wavefronts per two k of the product loop.
+    // (quad_lanes = 0, MEXP_PAIRS_LANES=0: the row-major lane order, for A/B runs)
+    L.ti = quad_lanes ? ((hl >> 3) << 1) | ((hl >> 1) & 1) : hl >> 2;
+    L.tj = quad_lanes ? (((hl >> 2) & 1) << 1) | (hl & 1) : hl & 3;
     L.diag = L.ti == L.tj;
     L.xbuf = smem + (warp * 2 + h) * kHalfFloats;
     L.ybuf = L.xbuf + kBufFloats;
@@ -807,7 +820,11 @@ int run_pairs32_f32(const float* d_a, float* d_out, mexp_selection* d_sel, int64
     const int64_t npairs = (batch + 1) / 2;
     const int64_t want = (npairs + kWarps - 1) / kWarps;
     const int grid = int(want < kCtasPerSm * sms ? want : kCtasPerSm * sms);
-    expm32_pairs_kernel<<<grid, 32 * kWarps, kSmemBytes, st>>>(d_a, d_out, list, batch);
+    static const int quad_lanes = [] {
+        const char* e = std::getenv("MEXP_PAIRS_LANES");
+        return e ? std::atoi(e) : 1;
+    }();
+    expm32_pairs_kernel<<<grid, 32 * kWarps, kSmemBytes, st>>>(d_a, d_out, list, batch, quad_lanes);
     launches->fetch_add(3, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? MEXP_OK : MEXP_ERR_CUDA;
 }

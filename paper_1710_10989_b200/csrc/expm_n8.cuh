@@ -70,16 +70,33 @@ struct Group8T {
 
     __device__ __forceinline__ void init(char* warp_tile, int lane) {
         tile = warp_tile;
-        r = lane >> 2;
-        q = lane & 3;
+        set_lanes(lane, false);
+        fscale = 1.0;
+        scaled = true;
+    }
+    // Which unit (r, q) = (M[r][2q], M[r][2q+1]) a lane owns.
+    //   DMMA mapping (quads = false): lane = 4r + q, the m8n8k4 accumulator layout.
+    //   Quad mapping (quads = true; reference-rounded products only): an aligned
+    //   quad of lanes owns a 2x2 block of units, r = 2(l>>3) + ((l>>1)&1),
+    //   q = 2((l>>2)&1) + (l&1). The shared-memory pipe merges identical addresses
+    //   only inside an aligned lane quad and serves 8 (quad, address) requests
+    //   per LDS.128 wavefront (tools/lds_patterns.cu), so the X-row loads
+    //   (address by r) and the Y column-pair loads (address by q) cost 2
+    //   wavefronts each, against 2 and 4 with lane = 4r + q: 28 instead of 44
+    //   wavefronts per product, which is what bounds the reference-rounded
+    //   product (profiles/cfg2_variants_r2.txt). Same arithmetic per element,
+    //   so the same bits; the owner of unit (r, q) loads and stores it at
+    //   row-major position 4r + q either way.
+    __device__ __forceinline__ void set_lanes(int lane, bool quads) {
+        r = quads ? ((lane >> 3) << 1) | ((lane >> 1) & 1) : lane >> 2;
+        q = quads ? (((lane >> 2) & 1) << 1) | (lane & 1) : lane & 3;
         st = unit8(r, q);
         ld0 = unit8(2 * q, r >> 1) + ((r & 1) << 3);
         ld1 = unit8(2 * q + 1, r >> 1) + ((r & 1) << 3);
         rowb = unit8(r, 0);
         qx = uint32_t(q) << 4;
-        fscale = 1.0;
-        scaled = true;
     }
+    __device__ __forceinline__ int unit_index() const { return 4 * r + q; }
 
     // The diagonal test goes through an opaque (volatile) move, re-evaluated
     // per matrix: otherwise the compiler hoists every identity term
@@ -249,8 +266,7 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     using Group8 = Group8T<kSplit>;
     using F = typename Group8::Frag;
     __shared__ __align__(16) char tiles[kN8WarpsPerBlock][kN8Mpw][1024];
-    // rounding policy in the low byte; AUTO's fast squaring tail above it
-    const int rounding = rounding_arg & 0xff, fast_tail = rounding_arg >> 8;
+    const int rounding = rounding_arg & 0xff;  // mexp_rounding
     // accuracy in the low 4 bits (mexp_accuracy); the family is kFamily
     const int accuracy = acc_arg & 15;
     constexpr int family = kFamily;
@@ -334,6 +350,31 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
             const int inf = __shfl_sync(0xffffffffu, info, 8 * j);
             const int degree = inf & 31, s = (inf >> 5) & 0x7fff, status = inf >> 20;
             g.tile = wt + j * 1024;
+            const bool exact = status == MEXP_OK &&
+                               (rounding == MEXP_ROUND_REFERENCE ||
+                                (rounding == MEXP_ROUND_AUTO && s >= exact_s_min));
+            if constexpr (kDefer) {
+                if (exact) {
+                    if (lane == 0) worklist[atomicAdd(wcount, 1)] = int32_t(m);
+                    continue;
+                }
+            } else {
+                if (exact) {
+                    // reference rounding on the quad lane mapping (set_lanes)
+                    g.set_lanes(lane, true);
+                    const double2 v = *reinterpret_cast<const double2*>(g.tile + g.st);
+                    F A;
+                    A.v[0] = v.x;
+                    A.v[1] = v.y;
+                    g.fscale = pow2_neg(s);
+                    g.scaled = s > 0;
+                    const F X = run_expm<ExactOps, family>(g, A, degree, s, 0);
+                    st_stream(reinterpret_cast<double2*>(out + m * 64) + g.unit_index(),
+                              make_double2(X.v[0], X.v[1]));
+                    g.set_lanes(lane, false);
+                    continue;
+                }
+            }
             F A;  // back from the staged tile (keeps 16 registers free)
             const double2 v = *reinterpret_cast<const double2*>(g.tile + g.st);
             A.v[0] = v.x;
@@ -342,22 +383,9 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
             if (status != MEXP_OK) {
                 X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
             } else {
-                const bool exact = rounding == MEXP_ROUND_REFERENCE ||
-                                   (rounding == MEXP_ROUND_AUTO && s >= exact_s_min);
                 g.fscale = pow2_neg(s);
                 g.scaled = s > 0;
-                if constexpr (kDefer) {
-                    if (exact) {
-                        if (lane == 0) worklist[atomicAdd(wcount, 1)] = int32_t(m);
-                        continue;
-                    }
-                    X = run_expm<FastOps, family>(g, A, degree, s, 0);
-                } else {
-                    if (exact)
-                        X = run_expm<ExactOps, family>(g, A, degree, s, fast_tail);
-                    else
-                        X = run_expm<FastOps, family>(g, A, degree, s, 0);
-                }
+                X = run_expm<FastOps, family>(g, A, degree, s, 0);
             }
             st_stream(reinterpret_cast<double2*>(out + m * 64) + lane, make_double2(X.v[0], X.v[1]));
         }
@@ -637,24 +665,33 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
             const int inf = infos[wib][j];
             if (inf & kN8InfoSkip) continue;
             g.tile = set + j * 512;
+            const int deg = inf & 31, sj = (inf >> 5) & 0x7fff;
+            // 2^-s from its high word (the low word is 0: s <= 1025 for any finite norm)
+            g.fscale = __hiloint2double(
+                int(sj <= 1022 ? uint32_t(1023 - sj) << 20 : 1u << ((1042 - sj) & 31)), 0);
+            g.scaled = sj > 0;
+            if (inf < 0 && !(inf & kN8InfoBad)) {
+                // reference rounding on the quad lane mapping (set_lanes)
+                g.set_lanes(lane, true);
+                const double2 v = *reinterpret_cast<const double2*>(g.tile + g.st);
+                F A;
+                A.v[0] = v.x;
+                A.v[1] = v.y;
+                const F X = run_expm8<ExactOps, family>(g, A, deg, sj);
+                st_stream(reinterpret_cast<double2*>(out + (m0 + j) * 64) + g.unit_index(),
+                          make_double2(X.v[0], X.v[1]));
+                g.set_lanes(lane, false);
+                continue;
+            }
             const double2 v = *reinterpret_cast<const double2*>(g.tile + g.st);
             F A;
             A.v[0] = v.x;
             A.v[1] = v.y;
             F X;
-            if (inf & kN8InfoBad) {
+            if (inf & kN8InfoBad)
                 X.v[0] = X.v[1] = __longlong_as_double(0x7ff8000000000000ll);
-            } else {
-                const int deg = inf & 31, sj = (inf >> 5) & 0x7fff;
-                // 2^-s from its high word (the low word is 0: s <= 1025 for any finite norm)
-                g.fscale = __hiloint2double(
-                    int(sj <= 1022 ? uint32_t(1023 - sj) << 20 : 1u << ((1042 - sj) & 31)), 0);
-                g.scaled = sj > 0;
-                if (inf < 0)
-                    X = run_expm8<ExactOps, family>(g, A, deg, sj);
-                else
-                    X = run_expm8<FastOps, family>(g, A, deg, sj);
-            }
+            else
+                X = run_expm8<FastOps, family>(g, A, deg, sj);
             st_stream(reinterpret_cast<double2*>(out + (m0 + j) * 64) + lane, make_double2(X.v[0], X.v[1]));
         }
         rd = nrd;
