@@ -85,7 +85,7 @@ ROOFLINE_BOUND = {"cfg1": "tensor", "cfg2": "hbm", "cfg3": "hbm", "cfg4": "tenso
                   "cfg5": "tensor"}
 KERNEL_NAME = {
     "cfg1": "expm64_cluster_kernel (1 launch per step)",
-    "cfg2": "expm8_f64_kernel (1 launch per step)",
+    "cfg2": "expm8_pipe_kernel (1 launch per step)",
     "cfg3": "select32 + scatter32 pre-pass, expm32_pairs_kernel (3 launches per step; "
             "the pair kernel ~92% of the step)",
     "cfg4": "gemm_dmma_kernel<*> chain (all launches of the step; GEMMs dominate)",
