@@ -80,9 +80,10 @@ struct Group8T {
     //   quad of lanes owns a 2x2 block of units, r = 2(l>>3) + ((l>>1)&1),
     //   q = 2((l>>2)&1) + (l&1). The shared-memory pipe merges identical addresses
     //   only inside an aligned lane quad and serves 8 (quad, address) requests
-    //   per LDS.128 wavefront (tools/lds_patterns.cu), so the X-row loads
-    //   (address by r) and the Y column-pair loads (address by q) cost 2
-    //   wavefronts each, against 2 and 4 with lane = 4r + q: 28 instead of 44
+    //   per LDS.128 wavefront, never fewer than 2 wavefronts per LDS.128
+    //   (tools/lds_patterns.cu), so the X-row loads (address by r) and the Y
+    //   column-pair loads (address by q) cost 2 wavefronts each, against 2
+    //   and 4 with lane = 4r + q: 28 instead of 44
     //   wavefronts per product, which is what bounds the reference-rounded
     //   product (profiles/cfg2_variants_r2.txt). Same arithmetic per element,
     //   so the same bits; the owner of unit (r, q) loads and stores it at

@@ -35,7 +35,7 @@ __global__ void k(int pat, int iters, unsigned* out) {
         if (BYTES == 16) {
             unsigned a, b, c, d;
             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(p + ((i * 7) & 7) * 512) : "memory");
-            acc += a * 3 + d;
+            acc += a * 3 + b * 5 + c * 7 + d;
         } else {
             unsigned a, b;
             asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(p + ((i * 7) & 7) * 512) : "memory");
