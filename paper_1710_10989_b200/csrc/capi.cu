@@ -363,6 +363,18 @@ int launch_n8_pipe(const double* a, double* out, mexp_selection* sel, int64_t ba
     prm.exact_from_s = rounding == MEXP_ROUND_REFERENCE ? 0
                        : rounding == MEXP_ROUND_AUTO    ? smin
                                                         : INT_MAX;
+    // rounds dealt round-robin before the ticket takes over, as a percentage of
+    // the batch (MEXP_N8_STATIC_PCT): 0 = every round after a warp's first is claimed
+    static const int static_pct = [] {
+        const char* e = std::getenv("MEXP_N8_STATIC_PCT");
+        const int v = e ? std::atoi(e) : 0;
+        return v < 0 ? 0 : v > 100 ? 100 : v;
+    }();
+    const uint32_t nwarps = uint32_t(grid) * kN8WarpsPerBlock;
+    const uint64_t rounds = uint64_t((batch + 3) / 4);
+    uint64_t passes = rounds * uint64_t(static_pct) / 100 / nwarps;
+    if (passes < 1) passes = 1;  // the first round of every warp is its own
+    prm.static_rounds = uint32_t(passes * nwarps);
     kern<<<grid, 32 * kN8WarpsPerBlock, 0, st>>>(a, out, sel, batch, prm, ticket);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     MEXP_CUDA(cudaGetLastError());

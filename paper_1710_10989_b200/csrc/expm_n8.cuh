@@ -490,6 +490,8 @@ struct N8Params {
     int accuracy;      // mexp_accuracy (the rare non-finite path's select_device)
     int exact_from_s;  // matrices with s >= this run reference rounding
                        // (0: all, REFERENCE; INT_MAX: none, FAST)
+    uint32_t static_rounds;  // rounds [0, static_rounds) are dealt round-robin (a multiple
+                             // of the warp count), the rest by the work ticket
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -657,10 +659,13 @@ __global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
         for (int j = 0; j < kN8Mpw; ++j) {
             // plain atom (inline asm): the compiler's warp-aggregated form
             // shuffles the result at once and would wait for the round trip here
-            if (j == kClaimAt && lane == 0)
+            // the next round: round-robin while it lies in the static part,
+            // else claimed from the ticket
+            const bool dyn = kClaimAt >= 0 && rd + rstride >= prm.static_rounds;
+            if (j == kClaimAt && dyn && lane == 0)
                 asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(ticket) : "memory");
             if (j == kPF) {
-                nrd = kClaimAt < 0 ? rd + rstride : rstride + __shfl_sync(0xffffffffu, t, 0);
+                nrd = dyn ? prm.static_rounds + __shfl_sync(0xffffffffu, t, 0) : rd + rstride;
                 if (nrd < rounds) copy_round(nrd, cur ^ kSet);
             }
             const int inf = infos[wib][j];

@@ -37,18 +37,18 @@ np.savez(sys.argv[1], *outs)
 """
 
 
-def run_variant(variant, path):
-    env = dict(os.environ, MEXP_N8_VARIANT=str(variant))
+def run_variant(variant, path, **extra):
+    env = dict(os.environ, MEXP_N8_VARIANT=str(variant), **extra)
     subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT), path], check=True, env=env,
                    timeout=600)
     with np.load(path) as z:
         return [z[k] for k in z.files]
 
 
-@pytest.mark.parametrize("variant", [12, 15])
-def test_pipelined_kernel_bitwise_equals_default(cuda, tmp_path, variant):
+@pytest.mark.parametrize("variant,extra", [(12, {}), (15, {}), (12, {"MEXP_N8_STATIC_PCT": "50"})])
+def test_pipelined_kernel_bitwise_equals_default(cuda, tmp_path, variant, extra):
     base = run_variant(0, str(tmp_path / "v0.npz"))
-    got = run_variant(variant, str(tmp_path / f"v{variant}.npz"))
+    got = run_variant(variant, str(tmp_path / f"v{variant}.npz"), **extra)
     assert len(base) == len(got) == 18
     for i, (b, g) in enumerate(zip(base, got)):
         assert np.array_equal(b, g), f"array {i} differs (variant {variant})"
