@@ -54,6 +54,58 @@ def test_exact_path_and_norm_loads():
         assert len({word(i, l) % 16 for l in range(8)}) == 8
 
 
+# ---- the quad lane mapping of the reference-rounded path (Group8T::set_lanes) ----
+# An aligned quad of lanes owns a 2x2 block of units. The shared-memory pipe
+# merges identical addresses only inside an aligned lane quad and serves 8
+# (quad, address) requests per 128-bit wavefront, at least 2 wavefronts per
+# LDS.128 (tools/lds_patterns.cu, profiles/lds_patterns_r2.csv).
+
+def quad_lane(l):
+    return ((l >> 3) << 1) | ((l >> 1) & 1), (((l >> 2) & 1) << 1) | (l & 1)
+
+
+def wavefronts_128(addr_of_lane):
+    """LDS.128 / STS.128 cost under the measured merge rule, bank conflicts included."""
+    reqs = []  # (quad, unit) requests in lane order, merged inside a quad
+    for l in range(32):
+        r = (l >> 2, addr_of_lane(l))
+        if r not in reqs:
+            reqs.append(r)
+    total = 0
+    for w in range(0, len(reqs), 8):
+        units = {u for _, u in reqs[w:w + 8]}
+        per_group = {}
+        for u in units:
+            per_group[u % 8] = per_group.get(u % 8, 0) + 1
+        total += max(per_group.values())
+    return max(2, total)
+
+
+def test_quad_mapping_matches_kernel_source():
+    src = open(f"{ROOT}/paper_1710_10989_b200/csrc/expm_n8.cuh").read()
+    assert "r = quads ? ((lane >> 3) << 1) | ((lane >> 1) & 1) : lane >> 2;" in src
+    assert "q = quads ? (((lane >> 2) & 1) << 1) | (lane & 1) : lane & 3;" in src
+
+
+def test_quad_mapping_is_a_bijection_of_2x2_quads():
+    assert sorted(quad_lane(l) for l in range(32)) == [(r, q) for r in range(8) for q in range(4)]
+    for g in range(8):
+        rs = {quad_lane(l)[0] for l in range(4 * g, 4 * g + 4)}
+        qs = {quad_lane(l)[1] for l in range(4 * g, 4 * g + 4)}
+        assert len(rs) == 2 and len(qs) == 2
+
+
+def test_reference_product_wavefronts():
+    """28 wavefronts per product with the quad mapping, 44 with lane = 4r + q."""
+    def product(rq):
+        store = wavefronts_128(lambda l: slot(*rq(l)))
+        xrow = sum(wavefronts_128(lambda l, c=c: slot(rq(l)[0], c)) for c in range(4))
+        ycol = sum(wavefronts_128(lambda l, k=k: slot(k, rq(l)[1])) for k in range(8))
+        return store, xrow, ycol
+    assert product(quad_lane) == (4, 8, 16)
+    assert product(lambda l: (l >> 2, l & 3)) == (4, 8, 32)
+
+
 # ---- fp32 operand buffers (expm_small_f32.cu, n = 32 and 64) ----
 # chunk c (16 bytes) of row i is stored at chunk c ^ swz(i); a lane (ti, tj)
 # owns rows 4 ti + r and the column chunks tj and tj + GC (GC = n / 8).
