@@ -340,10 +340,10 @@ int launch_pade8(const double* a, double* out, mexp_selection* sel, int64_t batc
 // The pipelined 8x8 kernel (expm_n8.cuh expm8_pipe_kernel): the default for
 // the Taylor families. kClaimAt / kPF: the matrix of a round before which the
 // next round is claimed / its copy issued.
-template <int kFamily, int kClaimAt, int kPF>
+template <int kFamily, int kClaimAt, int kPF, int kMinBlocks = 8>
 int launch_n8_pipe(const double* a, double* out, mexp_selection* sel, int64_t batch, int accuracy,
                    int rounding, int smin, cudaStream_t st) {
-    auto kern = expm8_pipe_kernel<kFamily, kClaimAt, kPF>;
+    auto kern = expm8_pipe_kernel<kFamily, kClaimAt, kPF, kMinBlocks>;
     static int blocks_per_sm = [&] {
         int b = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * kN8WarpsPerBlock, 0);

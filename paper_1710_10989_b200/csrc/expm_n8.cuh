@@ -530,8 +530,8 @@ __device__ __forceinline__ typename G::Frag run_expm8(const G& g, typename G::Fr
 constexpr int kN8InfoBad = 1 << 30;   // status != MEXP_OK: the result is NaN
 constexpr int kN8InfoSkip = 1 << 29;  // past the end of the batch
 
-template <int kFamily = MEXP_FAMILY_TAYLOR_NEW, int kClaimAt = 1, int kPF = 3>
-__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, 8)
+template <int kFamily = MEXP_FAMILY_TAYLOR_NEW, int kClaimAt = 1, int kPF = 3, int kMinBlocks = 8>
+__global__ void __launch_bounds__(32 * kN8WarpsPerBlock, kMinBlocks)
     expm8_pipe_kernel(const double* __restrict__ a, double* __restrict__ out,
                       mexp_selection* __restrict__ sel, int64_t batch, const N8Params prm,
                       unsigned long long* __restrict__ ticket) {
