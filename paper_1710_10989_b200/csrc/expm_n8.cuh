@@ -24,6 +24,12 @@
 
 namespace mexp_b200 {
 
+#ifdef MEXP_N8_NOSYNC_EXPERIMENT  // measurement only: compiler barrier instead of the warp barrier
+#define MEXP_N8_SYNC() asm volatile("" ::: "memory")
+#else
+#define MEXP_N8_SYNC() __syncwarp()
+#endif
+
 // Byte offset of the 16-byte unit (i, c) = (M[i][2c], M[i][2c+1]) in a
 // warp's 512-byte tile. The slot
 //   8*(i>>1) | 4*((i&1) ^ (i>>2)) | 2*(((c>>1) ^ (i>>1)) & 1) | (c&1)
@@ -179,11 +185,11 @@ struct Group8T {
     __device__ __forceinline__ Frag mm_impl(const Frag& X, const Frag& Y, bool same,
                                             const Frag* init) const {
         Frag C;
-        __syncwarp();  // readers of the previous product are done with the tile
+        MEXP_N8_SYNC();  // readers of the previous product are done with the tile
         if constexpr (Ops::kExact) {
             *reinterpret_cast<double2*>(tile + st) = make_double2(X.v[0], X.v[1]);
             if (!same) *reinterpret_cast<double2*>(ybase() + st) = make_double2(Y.v[0], Y.v[1]);
-            __syncwarp();
+            MEXP_N8_SYNC();
             const char* ty = same ? tile : ybase();
             double c0 = 0.0, c1 = 0.0;
             // row r of X in two halves (k ascending): 8 registers live, not 16
@@ -207,7 +213,7 @@ struct Group8T {
             C.v[1] = c1;
         } else {
             *reinterpret_cast<double2*>(tile + st) = make_double2(Y.v[0], Y.v[1]);
-            __syncwarp();
+            MEXP_N8_SYNC();
             const double y0 = *reinterpret_cast<const double*>(tile + ld0);
             const double y1 = *reinterpret_cast<const double*>(tile + ld1);
             C.v[0] = init ? init->v[0] : 0.0;
