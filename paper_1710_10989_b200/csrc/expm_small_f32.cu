@@ -339,6 +339,22 @@ __global__ void __launch_bounds__(32 * ShapeF32<N>::W * GPC)
     g.bar_id = 1 + gid;
     g.ti = g.tid / G::GC;
     g.tj = g.tid % G::GC;
+    if constexpr (N == 32) {
+        // An aligned quad of lanes owns a 2x2 block of lane tiles (bit 8 of
+        // acc_arg; MEXP_F32_LANES=0 keeps lane = 4 ti + tj). The shared-memory
+        // pipe merges identical addresses only inside an aligned lane quad and
+        // serves 8 (quad, address) requests per LDS.128 wavefront
+        // (tools/lds_patterns.cu): the Y row loads (address by tj) then cost 2
+        // wavefronts instead of 4, the X loads (address by ti) 2 as before --
+        // 24 instead of 40 wavefronts per 4 k. Lanes move only inside their
+        // group of 8, so every per-phase bank-conflict property of the swizzle
+        // holds; same arithmetic per element, so the same bits.
+        if (acc_arg & 0x100) {
+            const int l = g.lane;
+            g.ti = ((l >> 3) << 1) | ((l >> 1) & 1);
+            g.tj = (((l >> 2) & 1) << 1) | (l & 1);
+        }
+    }
 
     constexpr int64_t NN = int64_t(N) * N;
     const int64_t stride = int64_t(gridDim.x) * GPC;
@@ -438,7 +454,11 @@ int launch_f32(const float* a, float* out, mexp_selection* sel, int64_t batch, i
     const int64_t cap = int64_t(bps) * sm_count();
     const int grid = int(want < cap ? want : cap);
     if (grid == 0) return MEXP_OK;
-    kern<<<grid, G::THREADS * GPC, smem, st>>>(a, out, sel, batch, accuracy);
+    static const int quad_lanes = [] {
+        const char* e = std::getenv("MEXP_F32_LANES");
+        return (e ? std::atoi(e) : 1) ? 0x100 : 0;
+    }();
+    kern<<<grid, G::THREADS * GPC, smem, st>>>(a, out, sel, batch, accuracy | quad_lanes);
     launches->fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? MEXP_OK : MEXP_ERR_CUDA;
 }
